@@ -1,0 +1,283 @@
+/*
+ * uuv_b200.h — C ABI of the B200-native batched 6-DOF Fossen step.
+ *
+ * Drop-in boundary for the reference hot path (Python `uuvsim`, /root/reference):
+ *
+ *   uuv_step        replaces uuvsim/engine.py:465-484 step_batch
+ *                   (and its callees _step_slice 405-418, _substeps 421-449,
+ *                    _advance_rotors 335-352, _actuator_wrench_batch 355-402,
+ *                    hydrodynamics.py:125-197, kinematics.py:245-266)
+ *   uuv_reset       replaces uuvsim/engine.py:487-512 reset_envs for declarative
+ *                   samplers (default_sampler 265-266; the task samplers
+ *                   tasks/core.py:282-289 + 402-407/454-460/503-507; DR draws
+ *                   randomization.py:213-234; overlay math vehicles/__init__.py:418-505)
+ *   uuv_task_step   replaces uuvsim/tasks/core.py:328-370 VecTaskEnv.step
+ *                   (physics + observe 316-321 + rewards 170-214 + auto-reset)
+ *   uuv_task_reset  replaces uuvsim/tasks/core.py:294-301 VecTaskEnv.reset
+ *   uuv_observe     replaces uuvsim/tasks/core.py:316-321 VecTaskEnv.observe
+ *   uuv_rollout_stats  (no reference analogue; reduces the per-block task
+ *                   statistics accumulated by uuv_task_step, deterministic order)
+ *
+ * Conventions
+ *  - Every array is DEVICE memory owned by the caller and borrowed for the
+ *    call; nothing is retained and nothing is allocated inside uuv_step /
+ *    uuv_task_step.  All work is enqueued on `stream` (a cudaStream_t, NULL =
+ *    legacy default stream); no call synchronises the host.
+ *  - Per-env state is struct-of-arrays: component c of env i lives at
+ *    base[c * ld + i] (ld >= n_envs).  Commands and observations are
+ *    row-major (n_envs, width) with an explicit row stride.
+ *  - Real arrays are float32 or float64 as given by uuv_state.dtype; steps /
+ *    episodes are int32; flags are uint8 (0/1).
+ *  - Non-finite rows never raise: they freeze and set diverged (engine.py:414-449).
+ *  - Return value is a uuv_status; uuv_last_error() holds a thread-local message.
+ */
+#ifndef UUV_B200_H
+#define UUV_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define UUV_ABI_VERSION 1
+#define UUV_MAX_ACT 8        /* actuator columns per vehicle type             */
+#define UUV_MAX_TYPES 6      /* vehicle types in one batch (mixed fleets)     */
+#define UUV_MLP_MAX_PARAMS 128 /* packed weights+biases of one rotor network  */
+#define UUV_MLP_MAX_WIDTH 16   /* widest layer of a rotor network             */
+#define UUV_MLP_MAX_LAYERS 4
+#define UUV_MAX_DRAWS 16     /* overlay keys per DR spec                      */
+#define UUV_PW_MAX 64        /* piecewise breakpoint + cdf table entries     */
+
+typedef enum {
+  UUV_OK = 0,
+  UUV_ERR_ARG = 1,         /* bad pointer / size / enum                     */
+  UUV_ERR_SHAPE = 2,       /* inconsistent dimensions                        */
+  UUV_ERR_CUDA = 3,        /* launch or runtime failure                      */
+  UUV_ERR_UNSUPPORTED = 4  /* valid request outside this build's envelope   */
+} uuv_status;
+
+typedef enum { UUV_F32 = 0, UUV_F64 = 1 } uuv_dtype;
+
+/* Actuator kinds / rotor families (engine.py:80-81). */
+enum { UUV_PROPELLER = 0, UUV_RUDDER = 1, UUV_TILTROTOR = 2 };
+enum { UUV_ZERO_ORDER = 0, UUV_FIRST_ORDER = 1, UUV_DATA_DRIVEN = 2 };
+
+/* Hull flags. */
+enum { UUV_HULL_DIAGONAL = 1 /* M_A, D_lin, D_quad all diagonal */ };
+
+/*
+ * One vehicle type, float64, as compiled from a VehicleConfig
+ * (compile_layout engine.py:129-189 + BatchParams.write_row 220-234).
+ * Matrices are row-major.  Tilt rotors carry their thrust axis already
+ * rotated to the default tilt (engine.py:139-143).  For rudders `axis` is
+ * the hinge and fin_xf/fin_yf its in-plane basis (engine.py:118-126).
+ * The library factors the base composite mass matrix M_RB + M_A itself.
+ */
+typedef struct {
+  int32_t n_act;
+  int32_t flags;
+  int32_t kind[UUV_MAX_ACT];
+  int32_t model[UUV_MAX_ACT];
+  int32_t mlp_layers;                      /* number of dense layers (0: none) */
+  int32_t mlp_sizes[UUV_MLP_MAX_LAYERS + 1];
+  int32_t mlp_relu;                        /* 0 tanh, 1 relu */
+  int32_t pad_;
+  double mass, volume, rho, g;
+  double r_g[3], r_b[3];
+  double inertia[9];
+  double M_A[36], D_lin[36], D_quad[36];
+  double limit[UUV_MAX_ACT], deadzone[UUV_MAX_ACT], reaction[UUV_MAX_ACT];
+  double thrust_coeff[UUV_MAX_ACT], time_constant[UUV_MAX_ACT];
+  double mount[UUV_MAX_ACT][3], axis[UUV_MAX_ACT][3];
+  double fin_xf[UUV_MAX_ACT][3], fin_yf[UUV_MAX_ACT][3];
+  double fin_area[UUV_MAX_ACT], fin_cla[UUV_MAX_ACT], fin_cd0[UUV_MAX_ACT];
+  double fin_kd[UUV_MAX_ACT], fin_stall[UUV_MAX_ACT], fin_rho[UUV_MAX_ACT];
+  double mlp[UUV_MLP_MAX_PARAMS];          /* W0 (out,in) row-major, b0, W1, b1, ... */
+} uuv_hull;
+
+/*
+ * Per-env DR overlay record.  The record is a float64 array [n_slots][ld]
+ * in both precisions (sampled values are kept bit-exact; derived parameters
+ * are formed from it in float64 once per launch);
+ * slot[k] gives the first slot of key k or -1 when the key is inactive in the
+ * batch.  Inactive keys and rows without an overlay hold identity values
+ * (ratios 1, cobm 0 = "absent", payload 0, positions/jitter 0) so that
+ * overlay-free rows reproduce the base vehicle exactly (engine.py:497-502).
+ */
+enum {
+  UUV_OV_MASS = 0,         /* mass*            */
+  UUV_OV_VOLUME,           /* volume*          */
+  UUV_OV_INERTIA,          /* inertia*         */
+  UUV_OV_ADDED_MASS,       /* added_mass*      */
+  UUV_OV_DAMPING,          /* damping*         */
+  UUV_OV_TIME_CONSTANT,    /* time_constant*   */
+  UUV_OV_THRUST_COEFF,     /* thrust_coeff*    */
+  UUV_OV_COBM,             /* cobm (0 = absent)*/
+  UUV_OV_PAYLOAD_MASS,     /* payload_mass*    */
+  UUV_OV_PAYLOAD_POS,      /* payload_position, 3 slots */
+  UUV_OV_JITTER,           /* mount_position_jitter, 3*UUV_MAX_ACT slots (actuator-major) */
+  UUV_OV_COUNT
+};
+
+typedef struct {
+  int32_t dtype;           /* uuv_dtype of every Real array below           */
+  int32_t a_max;           /* actuator columns of act / commands            */
+  int64_t n_envs;
+  int64_t ld;              /* SoA leading dimension                          */
+  int64_t env_offset;      /* global index of row 0 (RNG keys under sharding)*/
+  void* p;                 /* [3][ld]  NED position                          */
+  void* q;                 /* [4][ld]  body->NED quaternion (w,x,y,z)        */
+  void* nu;                /* [6][ld]  body velocity                         */
+  void* act;               /* [a_max][ld] rotor speeds / fin angles          */
+  void* current_ned;       /* [3][ld]  or NULL: no current in this batch     */
+  int32_t* steps;          /* [ld]                                           */
+  int32_t* episodes;       /* [ld]                                           */
+  uint8_t* diverged;       /* [ld]                                           */
+  const uint8_t* type_id;  /* [ld] index into the hull list, or NULL (type 0)*/
+  double* overlay;         /* [n_slots][ld] float64 (bit-exact draws) or NULL*/
+  uint16_t* overlay_keys;  /* [ld] bit k set: key k present in the row's overlay, or NULL */
+  int32_t n_slots;
+  int32_t slot[UUV_OV_COUNT];
+} uuv_state;
+
+/* One draw of a DR key (randomization.py:48-117): uniform or piecewise. */
+enum { UUV_DIST_UNIFORM = 0, UUV_DIST_PIECEWISE = 1 };
+typedef struct {
+  int32_t key;             /* UUV_OV_* (overlay draws) */
+  int32_t dist;
+  int32_t n_draws;         /* 1 scalar, 3 vector keys  */
+  int32_t pw_bins;         /* piecewise: K bins        */
+  int32_t pw_offset;       /* into pw_table: K+1 breakpoints then K cdf values */
+  int32_t pad_;
+  double lo, hi;
+} uuv_draw;
+
+enum { UUV_START_IDENTITY = 0, UUV_START_BOX = 1 };
+enum { UUV_CURRENT_NONE = 0, UUV_CURRENT_RANDOM_HEADING = 1, UUV_CURRENT_HEADING_DRAW = 2 };
+
+/*
+ * Declarative episode sampler.  Draw order per reset (Philox stream keyed
+ * (seed, env_offset + i), counter word 1 = episode):
+ *   overlay draws in the given (sorted-key) order,
+ *   current speed [, heading],
+ *   start box: p = p_base + U(p_lo, p_hi) (3), euler = U(eul_lo, eul_hi) (3),
+ *              nu = U(nu_lo, nu_hi) (6).
+ */
+typedef struct {
+  int32_t n_overlay;
+  int32_t current_mode;
+  int32_t start_mode;
+  int32_t pad_;
+  uuv_draw overlay[UUV_MAX_DRAWS];
+  uuv_draw current_speed, current_heading;
+  double p_base[3], p_lo[3], p_hi[3];
+  double eul_lo[3], eul_hi[3];
+  double nu_lo[6], nu_hi[6];
+  double pw_table[UUV_PW_MAX];
+} uuv_sampler;
+
+enum { UUV_TASK_STATION = 0, UUV_TASK_TRACKING = 1, UUV_TASK_DOCKING = 2 };
+enum { UUV_TRAJ_HELIX = 0, UUV_TRAJ_LISSAJOUS = 1 };
+
+/* Task constants (tasks/core.py:98-167, trajectories.py:23-53). */
+typedef struct {
+  int32_t kind;
+  int32_t episode_length;
+  int32_t traj_kind;
+  int32_t obs_dim;
+  double bounds, nu_max, fail_penalty;
+  double w_p, w_a, w_v, w_u, w_b, r_tol, speed_cap;
+  double dock_bonus, w_dock_dist, w_impact, w_level;
+  double target_p[3], target_q[4];
+  double success_tol;
+  double dock_centre[3], dock_radius;
+  double traj_radius, traj_rate, traj_climb, traj_z0, traj_phase;
+  double traj_amp[3], traj_rates[3];
+} uuv_task;
+
+/* Real outputs of uuv_task_step: [UUV_TR_COUNT][ld]. */
+enum { UUV_TR_REWARD = 0, UUV_TR_POS_ERR, UUV_TR_ATT_ERR, UUV_TR_METRIC, UUV_TR_TIME,
+       UUV_TR_CONTACT_DIST, UUV_TR_CONTACT_SPEED, UUV_TR_CONTACT_ATT, UUV_TR_COUNT };
+/* Flag outputs of uuv_task_step: uint8 [UUV_TF_COUNT][ld]. */
+enum { UUV_TF_TERMINATED = 0, UUV_TF_TRUNCATED, UUV_TF_FINISHED, UUV_TF_FAILURE,
+       UUV_TF_SUCCESS, UUV_TF_DIVERGED, UUV_TF_CONTACT, UUV_TF_COUNT };
+/* Per-block rollout statistics accumulated by uuv_task_step (float64 sums). */
+enum { UUV_ST_REWARD = 0, UUV_ST_FINISHED, UUV_ST_SUCCESS, UUV_ST_FAILURE, UUV_ST_TRUNCATED,
+       UUV_ST_METRIC_FINISHED, UUV_ST_DIVERGED, UUV_ST_FRAMES, UUV_ST_COUNT };
+
+typedef struct {
+  void* prev_u;            /* [a_max][ld] previous (clipped) command          */
+  void* dev_sum;           /* [ld] tracking deviation accumulator or NULL     */
+  void* obs;               /* (n, obs_ld) row-major next observation          */
+  int64_t obs_ld;
+  void* term_obs;          /* (n, obs_ld) final obs of finished rows or NULL  */
+  void* real_out;          /* [UUV_TR_COUNT][ld] or NULL (reset/observe)      */
+  uint8_t* flag_out;       /* [UUV_TF_COUNT][ld] or NULL                      */
+  double* stats;           /* [n_blocks][UUV_ST_COUNT] running sums or NULL   */
+} uuv_task_io;
+
+typedef struct uuv_ctx uuv_ctx;
+
+const char* uuv_last_error(void);
+int32_t uuv_abi_version(void);
+/* sizeof of the ABI structs, for binding self-checks: hull, state, sampler, task, task_io. */
+void uuv_abi_sizes(int64_t out[5]);
+
+/* Context: owns the hull list of one batch (host copy; travels by value in each launch). */
+uuv_status uuv_ctx_create(const uuv_hull* hulls, int32_t n_types, uuv_ctx** out);
+uuv_status uuv_ctx_set_hulls(uuv_ctx* ctx, const uuv_hull* hulls, int32_t n_types);
+void uuv_ctx_destroy(uuv_ctx* ctx);
+
+/* Advance every env one control step of `substeps` fused physics substeps
+ * (dt_sub = dt / substeps).  commands: (n_envs, cmd_ld) row-major Real,
+ * clipped to [-1, 1] inside. */
+uuv_status uuv_step(uuv_ctx* ctx, const uuv_state* st, const void* commands, int64_t cmd_ld,
+                    int32_t substeps, double dt, void* stream);
+
+/* Reset rows with mask[i] != 0 (mask NULL = all rows) from the declarative sampler. */
+uuv_status uuv_reset(uuv_ctx* ctx, const uuv_state* st, const uint8_t* mask,
+                     const uuv_sampler* sampler, uint64_t seed, void* stream);
+
+/* Fused task step: physics, reward/termination/info, auto-reset, next obs. */
+uuv_status uuv_task_step(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task,
+                         const uuv_sampler* sampler, uint64_t seed, const void* commands,
+                         int64_t cmd_ld, int32_t substeps, double dt, const uuv_task_io* io,
+                         void* stream);
+
+/* Reset masked rows (prev_u and dev_sum zeroed too), then observe all rows. */
+uuv_status uuv_task_reset(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task,
+                          const uuv_sampler* sampler, uint64_t seed, const uint8_t* mask,
+                          double dt, const uuv_task_io* io, void* stream);
+
+/* Observation of every row into io->obs. */
+uuv_status uuv_observe(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task, double dt,
+                       const uuv_task_io* io, void* stream);
+
+/* Number of stat blocks uuv_task_step uses for n_envs (size io->stats to this). */
+int64_t uuv_stats_blocks(int64_t n_envs);
+
+/* Reduce io->stats over blocks (fixed order) into out[UUV_ST_COUNT] (device float64);
+ * reset != 0 zeroes the running sums afterwards. */
+uuv_status uuv_rollout_stats(const double* stats, int64_t n_blocks, double* out, int32_t reset,
+                             void* stream);
+
+/* Materialise per-env derived parameters (the reference's BatchParams rows,
+ * engine.py:193-234) into float64 device buffers, for inspection and tests:
+ * out12 = [mass, volume, r_g(3), r_b(3), W, B, added_mass_scale, damping_scale] per env,
+ * minv = M^-1 (36 per env), ct_tau = thrust_coeff (a_max) then time_constant (a_max),
+ * mounts = (a_max*3) per env.  Any output may be NULL. */
+uuv_status uuv_derive_params(uuv_ctx* ctx, const uuv_state* st, double* out12, double* minv,
+                             double* ct_tau, double* mounts, void* stream);
+
+/* Validation entry: the first substep's intermediates for every env, without
+ * writing state (the quantities engine.py:425-433 forms), into out (n_envs, 48)
+ * float64 rows: tau[6] hydro[6] c_rb[6] acc[6] nu_new[6] p_new[3] q_new[4]
+ * act_new[8] ok[1] pad[2].  commands as in uuv_step; dt_sub = dt / substeps. */
+uuv_status uuv_substep_terms(uuv_ctx* ctx, const uuv_state* st, const void* commands,
+                             int64_t cmd_ld, double dt_sub, double* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* UUV_B200_H */

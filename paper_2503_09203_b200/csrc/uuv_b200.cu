@@ -1,0 +1,945 @@
+// uuv_b200.cu — sm_100a kernels and the C ABI declared in include/uuv_b200.h.
+//
+// Kernels (one env per thread, 128-thread CTAs, SoA state, K substeps fused):
+//   k_step        step_batch            (engine.py:465-484)
+//   k_task_step   VecTaskEnv.step       (tasks/core.py:328-370), fused physics +
+//                 reward/termination + auto-reset + next observation + stats
+//   k_reset       reset_envs            (engine.py:487-512), declarative samplers
+//   k_task_reset  VecTaskEnv.reset / observe (tasks/core.py:294-321)
+//   k_stats       deterministic reduction of the per-CTA rollout statistics
+//   k_derive      BatchParams rows for inspection (engine.py:193-234)
+//   k_terms       first-substep intermediates for parity tests
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "uuv_task.cuh"
+
+using namespace uuv;
+
+namespace {
+
+constexpr int kBlock = 128;
+constexpr int kObsMax = 12 + UUV_MAX_ACT + 3;
+
+thread_local std::string g_err;
+
+uuv_status fail(uuv_status s, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+uuv_status fail(uuv_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+uuv_status check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(UUV_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return UUV_OK;
+}
+
+// ------------------------------------------------------------------ host-side hull compilation
+bool is_diag(const double* M) {
+  for (int r = 0; r < 6; ++r)
+    for (int c = 0; c < 6; ++c)
+      if (r != c && M[6 * r + c] != 0.0) return false;
+  return true;
+}
+
+template <typename R>
+void build_hull(const uuv_hull& src, Hull<R>& dst) {
+  memset(&dst, 0, sizeof dst);
+  HullR<R>& h = dst.r;
+  HullD& d = dst.d;
+  h.n_act = src.n_act;
+  h.flags = src.flags;
+  if (is_diag(src.M_A) && is_diag(src.D_lin) && is_diag(src.D_quad)) h.flags |= UUV_HULL_DIAGONAL;
+  else h.flags &= ~UUV_HULL_DIAGONAL;
+  h.mlp_layers = src.mlp_layers;
+  h.mlp_relu = src.mlp_relu;
+  for (int k = 0; k <= UUV_MLP_MAX_LAYERS; ++k) h.mlp_sizes[k] = src.mlp_sizes[k];
+  for (int j = 0; j < UUV_MAX_ACT; ++j) {
+    h.kind[j] = src.kind[j];
+    h.model[j] = src.model[j];
+    h.limit[j] = (R)src.limit[j];
+    h.deadzone[j] = (R)src.deadzone[j];
+    h.reaction[j] = (R)src.reaction[j];
+    for (int c = 0; c < 3; ++c) {
+      h.axis[j][c] = (R)src.axis[j][c];
+      h.fin_xf[j][c] = (R)src.fin_xf[j][c];
+      h.fin_yf[j][c] = (R)src.fin_yf[j][c];
+      h.mount[j][c] = (R)src.mount[j][c];
+      d.mount[j][c] = src.mount[j][c];
+    }
+    h.fin_area[j] = (R)src.fin_area[j];
+    h.fin_cla[j] = (R)src.fin_cla[j];
+    h.fin_cd0[j] = (R)src.fin_cd0[j];
+    h.fin_kd[j] = (R)src.fin_kd[j];
+    h.fin_stall[j] = (R)src.fin_stall[j];
+    h.fin_rho[j] = (R)src.fin_rho[j];
+    h.ct[j] = (R)src.thrust_coeff[j];
+    h.tc[j] = (R)src.time_constant[j];
+    d.ct[j] = src.thrust_coeff[j];
+    d.tc[j] = src.time_constant[j] > 0 ? src.time_constant[j] : 1.0;
+  }
+  for (int k = 0; k < 36; ++k) {
+    h.M_A[k] = (R)src.M_A[k];
+    h.D_lin[k] = (R)src.D_lin[k];
+    h.D_quad[k] = (R)src.D_quad[k];
+  }
+  for (int k = 0; k < UUV_MLP_MAX_PARAMS; ++k) h.mlp[k] = (R)src.mlp[k];
+  d.mass = src.mass;
+  d.volume = src.volume;
+  d.rhog = src.rho * src.g;  // B = (rho * g) * V  (hydrodynamics.py:179)
+  d.g = src.g;
+  for (int c = 0; c < 3; ++c) { d.r_g[c] = src.r_g[c]; d.r_b[c] = src.r_b[c]; }
+  for (int k = 0; k < 9; ++k) d.inertia[k] = src.inertia[k];
+  for (int i = 0; i < 6; ++i)
+    for (int j = 0; j <= i; ++j) d.M_A[tri(i, j)] = src.M_A[6 * i + j];
+  // base derived parameters (overlay-free rows)
+  EnvD e;
+  e.mass = d.mass; e.volume = d.volume; e.W = d.mass * d.g; e.B = d.rhog * d.volume;
+  e.a = 1.0; e.d = 1.0; e.rt = 1.0; e.rc = 1.0;
+  for (int c = 0; c < 3; ++c) { e.r_g[c] = d.r_g[c]; e.r_b[c] = d.r_b[c]; }
+  for (int k = 0; k < 9; ++k) e.I[k] = d.inertia[k];
+  double M[21], L[15], Di[6];
+  mass_matrix(d, e, M);
+  ldl6<double>(M, L, Di);
+  for (int k = 0; k < 15; ++k) h.L[k] = (R)L[k];
+  for (int k = 0; k < 6; ++k) h.dinv[k] = (R)Di[k];
+  h.mass = (R)e.mass; h.W = (R)e.W; h.B = (R)e.B;
+  for (int c = 0; c < 3; ++c) { h.r_g[c] = (R)e.r_g[c]; h.r_b[c] = (R)e.r_b[c]; }
+  h.I[0] = (R)e.I[0]; h.I[1] = (R)e.I[4]; h.I[2] = (R)e.I[8];
+  h.I[3] = (R)e.I[1]; h.I[4] = (R)e.I[2]; h.I[5] = (R)e.I[5];
+}
+
+template <typename R>
+void build_task(const uuv_task& s, TaskR<R>& t) {
+  t.kind = s.kind; t.episode_length = s.episode_length; t.traj_kind = s.traj_kind;
+  t.obs_dim = s.obs_dim;
+  t.bounds = (R)s.bounds; t.nu_max = (R)s.nu_max; t.fail_penalty = (R)s.fail_penalty;
+  t.w_p = (R)s.w_p; t.w_a = (R)s.w_a; t.w_v = (R)s.w_v; t.w_u = (R)s.w_u; t.w_b = (R)s.w_b;
+  t.r_tol = (R)s.r_tol; t.speed_cap = (R)s.speed_cap;
+  t.dock_bonus = (R)s.dock_bonus; t.w_dock_dist = (R)s.w_dock_dist;
+  t.w_impact = (R)s.w_impact; t.w_level = (R)s.w_level;
+  for (int c = 0; c < 3; ++c) {
+    t.target_p[c] = (R)s.target_p[c];
+    t.dock_centre[c] = (R)s.dock_centre[c];
+    t.traj_amp[c] = (R)s.traj_amp[c];
+    t.traj_rates[c] = (R)s.traj_rates[c];
+  }
+  for (int c = 0; c < 4; ++c) t.target_q[c] = (R)s.target_q[c];
+  t.success_tol = (R)s.success_tol; t.dock_radius = (R)s.dock_radius;
+  t.traj_radius = (R)s.traj_radius; t.traj_rate = (R)s.traj_rate; t.traj_climb = (R)s.traj_climb;
+  t.traj_z0 = (R)s.traj_z0; t.traj_phase = (R)s.traj_phase;
+}
+
+template <typename R>
+StateView<R> make_view(const uuv_state& s) {
+  StateView<R> v;
+  v.p = (R*)s.p; v.q = (R*)s.q; v.nu = (R*)s.nu; v.act = (R*)s.act; v.cur = (R*)s.current_ned;
+  v.steps = s.steps; v.episodes = s.episodes; v.diverged = s.diverged; v.type_id = s.type_id;
+  v.ov = s.overlay; v.ov_keys = s.overlay_keys;
+  for (int k = 0; k < UUV_OV_COUNT; ++k) v.slot[k] = s.overlay ? s.slot[k] : -1;
+  v.n_slots = s.n_slots; v.a_max = s.a_max;
+  v.n = s.n_envs; v.ld = s.ld; v.env_offset = s.env_offset;
+  return v;
+}
+
+}  // namespace
+
+struct uuv_ctx {
+  std::vector<uuv_hull> hulls;
+  std::vector<Hull<float>> hf;
+  std::vector<Hull<double>> hd;
+};
+
+// ================================================================== kernels
+
+template <typename R, int NT> struct StepArgs {
+  Hull<R> hull[NT];
+  StateView<R> sv;
+  const R* cmd;
+  int64_t cmd_ld;
+  int32_t K;
+  R dt;
+};
+
+// Load env i's kinematic state (SoA, coalesced).
+template <typename R>
+UUV_D void load_state(const StateView<R>& sv, int64_t i, int A, R& px, R& py, R& pz, Q4<R>& q,
+                      R* nu, R* act) {
+  const int64_t ld = sv.ld;
+  px = sv.p[i]; py = sv.p[ld + i]; pz = sv.p[2 * ld + i];
+  q = Q4<R>{sv.q[i], sv.q[ld + i], sv.q[2 * ld + i], sv.q[3 * ld + i]};
+#pragma unroll
+  for (int k = 0; k < 6; ++k) nu[k] = sv.nu[k * ld + i];
+#pragma unroll
+  for (int j = 0; j < UUV_MAX_ACT; ++j) act[j] = j < A ? sv.act[j * ld + i] : R(0);
+}
+
+template <typename R>
+UUV_D void store_state(const StateView<R>& sv, int64_t i, int A, R px, R py, R pz, Q4<R> q,
+                       const R* nu, const R* act) {
+  const int64_t ld = sv.ld;
+  sv.p[i] = px; sv.p[ld + i] = py; sv.p[2 * ld + i] = pz;
+  sv.q[i] = q.w; sv.q[ld + i] = q.x; sv.q[2 * ld + i] = q.y; sv.q[3 * ld + i] = q.z;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) sv.nu[k * ld + i] = nu[k];
+#pragma unroll
+  for (int j = 0; j < UUV_MAX_ACT; ++j)
+    if (j < A) sv.act[j * ld + i] = act[j];
+}
+
+// Physics of one control step for env i; returns the post-step diverged flag.
+template <typename R, bool DR>
+UUV_D bool physics(const Hull<R>& H, const StateView<R>& sv, int64_t i, int K, R dt, const R* u,
+                   R& px, R& py, R& pz, Q4<R>& q, R* nu, R* act) {
+  Sub<R> s;
+  const double* jit = nullptr;
+  if (DR) {
+    EnvD e;
+    derive_env(H.d, sv.ov, sv.ld, i, sv.slot, e);
+    sub_from_env<R>(H.d, e, dt, s);
+    if (sv.slot[UUV_OV_JITTER] >= 0) jit = sv.ov + sv.slot[UUV_OV_JITTER] * sv.ld + i;
+  }
+  const bool has_cur = sv.cur != nullptr;
+  V3<R> cur{R(0), R(0), R(0)};
+  if (has_cur) cur = V3<R>{sv.cur[i], sv.cur[sv.ld + i], sv.cur[2 * sv.ld + i]};
+  bool ok = true;
+  for (int k = 0; k < K; ++k) {
+    if (!substep<R, DR, false>(H.r, s, jit, sv.ld, px, py, pz, q, nu, act, u, has_cur, cur, dt,
+                               nullptr)) {
+      ok = false;
+      break;
+    }
+  }
+  return !ok;
+}
+
+template <typename R, int NT, bool DR>
+__global__ void __launch_bounds__(kBlock) k_step(const __grid_constant__ StepArgs<R, NT> a) {
+  const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+  const StateView<R>& sv = a.sv;
+  if (i >= sv.n) return;
+  const int t = NT > 1 ? (int)sv.type_id[i] : 0;
+  const Hull<R>& H = a.hull[t];
+  const int A = H.r.n_act;
+  const int32_t steps = sv.steps[i];
+  if (sv.diverged[i]) {  // frozen rows stay frozen (engine.py:411, 441-449)
+    sv.steps[i] = steps + 1;
+    return;
+  }
+  R u[UUV_MAX_ACT];
+  const R* crow = a.cmd + i * a.cmd_ld;
+#pragma unroll
+  for (int j = 0; j < UUV_MAX_ACT; ++j) u[j] = j < A ? clip_<R>(crow[j], R(-1), R(1)) : R(0);
+  R px, py, pz, nu[6], act[UUV_MAX_ACT];
+  Q4<R> q;
+  load_state(sv, i, A, px, py, pz, q, nu, act);
+  const bool div = physics<R, DR>(H, sv, i, a.K, a.dt, u, px, py, pz, q, nu, act);
+  store_state(sv, i, A, px, py, pz, q, nu, act);
+  sv.diverged[i] = div ? 1 : 0;
+  sv.steps[i] = steps + 1;
+}
+
+// ------------------------------------------------------------------ task step
+template <typename R> struct TaskArgs {
+  Hull<R> hull[1];
+  StateView<R> sv;
+  TaskR<R> task;
+  uuv_sampler smp;
+  uint64_t seed;
+  const R* cmd;
+  int64_t cmd_ld;
+  int32_t K;
+  R dt_sub;
+  R dt;  // control dt (time / tracking reference)
+  R* prev_u;
+  R* dev_sum;
+  R* obs;
+  int64_t obs_ld;
+  R* term_obs;
+  R* rout;
+  uint8_t* fout;
+  double* stats;
+  const uint8_t* mask;  // task reset only
+  int32_t mode;         // task reset kernel: 0 observe only, 1 reset masked then observe
+};
+
+// Write the CTA's staged observation rows out with coalesced stores.
+template <typename R>
+UUV_D void flush_obs(const R* s_obs, R* obs, int64_t obs_ld, int obs_dim, int64_t row0, int64_t n) {
+  const int rows = (int)min((int64_t)kBlock, n - row0);
+  const int total = rows * obs_dim;
+  for (int e = threadIdx.x; e < total; e += kBlock) {
+    const int r = e / obs_dim, c = e - r * obs_dim;
+    obs[(row0 + r) * obs_ld + c] = s_obs[e];
+  }
+}
+
+template <typename R, bool DR>
+__global__ void __launch_bounds__(kBlock) k_task_step(const __grid_constant__ TaskArgs<R> a) {
+  __shared__ R s_obs[kBlock * kObsMax];
+  __shared__ double s_red[kBlock / 32][UUV_ST_COUNT];
+  const int64_t row0 = (int64_t)blockIdx.x * kBlock;
+  const int64_t i = row0 + threadIdx.x;
+  const StateView<R>& sv = a.sv;
+  const Hull<R>& H = a.hull[0];
+  const TaskR<R>& T = a.task;
+  const int A = H.r.n_act;
+  const int od = T.obs_dim;
+  const int64_t ld = sv.ld;
+  double st[UUV_ST_COUNT];
+#pragma unroll
+  for (int k = 0; k < UUV_ST_COUNT; ++k) st[k] = 0.0;
+  if (i < sv.n) {
+    // u = clip(commands); du = u - prev_u; prev_u = u  (tasks/core.py:329-335)
+    R u[UUV_MAX_ACT], du[UUV_MAX_ACT];
+    const R* crow = a.cmd + i * a.cmd_ld;
+#pragma unroll
+    for (int j = 0; j < UUV_MAX_ACT; ++j) {
+      if (j < A) {
+        u[j] = clip_<R>(crow[j], R(-1), R(1));
+        du[j] = u[j] - a.prev_u[j * ld + i];
+      } else {
+        u[j] = R(0);
+        du[j] = R(0);
+      }
+    }
+    int32_t steps = sv.steps[i];
+    bool div = sv.diverged[i] != 0;
+    R px, py, pz, nu[6], act[UUV_MAX_ACT];
+    Q4<R> q;
+    load_state(sv, i, A, px, py, pz, q, nu, act);
+    if (!div) div = physics<R, DR>(H, sv, i, a.K, a.dt_sub, u, px, py, pz, q, nu, act);
+    steps += 1;
+    R dev = a.dev_sum != nullptr ? a.dev_sum[i] : R(0);
+    TaskOut<R> o;
+    task_eval<R>(T, A, px, py, pz, q, nu, du, steps, div, a.dt, &dev, o);
+    if (a.rout != nullptr) {
+      a.rout[UUV_TR_REWARD * ld + i] = o.reward;
+      a.rout[UUV_TR_POS_ERR * ld + i] = o.pos_err;
+      a.rout[UUV_TR_ATT_ERR * ld + i] = o.att_err;
+      a.rout[UUV_TR_METRIC * ld + i] = o.metric;
+      a.rout[UUV_TR_TIME * ld + i] = o.time;
+      if (T.kind == UUV_TASK_DOCKING) {
+        a.rout[UUV_TR_CONTACT_DIST * ld + i] = o.c_dist;
+        a.rout[UUV_TR_CONTACT_SPEED * ld + i] = o.c_speed;
+        a.rout[UUV_TR_CONTACT_ATT * ld + i] = o.c_att;
+      }
+    }
+    if (a.fout != nullptr) {
+      a.fout[UUV_TF_TERMINATED * ld + i] = o.terminated;
+      a.fout[UUV_TF_TRUNCATED * ld + i] = o.truncated;
+      a.fout[UUV_TF_FINISHED * ld + i] = o.finished;
+      a.fout[UUV_TF_FAILURE * ld + i] = o.failure;
+      a.fout[UUV_TF_SUCCESS * ld + i] = o.success;
+      a.fout[UUV_TF_DIVERGED * ld + i] = div;
+      a.fout[UUV_TF_CONTACT * ld + i] = o.contact;
+    }
+    st[UUV_ST_REWARD] = (double)o.reward;
+    st[UUV_ST_FINISHED] = o.finished;
+    st[UUV_ST_SUCCESS] = o.success;
+    st[UUV_ST_FAILURE] = o.failure;
+    st[UUV_ST_TRUNCATED] = o.truncated;
+    st[UUV_ST_METRIC_FINISHED] = o.finished ? (double)o.metric : 0.0;
+    st[UUV_ST_DIVERGED] = div;
+    st[UUV_ST_FRAMES] = 1.0;
+    R* srow = s_obs + threadIdx.x * od;
+    if (o.finished) {
+      if (a.term_obs != nullptr)  // final observation of the ended episode
+        observe_row<R>(T, A, px, py, pz, q, nu, u, steps, a.dt, a.term_obs + i * a.obs_ld, nullptr);
+      V3<R> cur;
+      reset_env<R>(sv, i, a.smp, a.seed, px, py, pz, q, nu, cur);
+#pragma unroll
+      for (int j = 0; j < UUV_MAX_ACT; ++j) { act[j] = R(0); u[j] = R(0); }
+      steps = 0;
+      div = false;
+      dev = R(0);
+    }
+    observe_row<R>(T, A, px, py, pz, q, nu, u, steps, a.dt, srow, nullptr);
+    store_state(sv, i, A, px, py, pz, q, nu, act);
+    sv.steps[i] = steps;
+    sv.diverged[i] = div ? 1 : 0;
+#pragma unroll
+    for (int j = 0; j < UUV_MAX_ACT; ++j)
+      if (j < A) a.prev_u[j * ld + i] = u[j];
+    if (a.dev_sum != nullptr) a.dev_sum[i] = dev;
+  }
+  __syncthreads();
+  flush_obs<R>(s_obs, a.obs, a.obs_ld, od, row0, sv.n);
+  if (a.stats != nullptr) {
+    // deterministic CTA reduction: fixed shuffle tree, then warps in order
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < UUV_ST_COUNT; ++k) {
+      double v = st[k];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+      if (lane == 0) s_red[warp][k] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < UUV_ST_COUNT) {
+      double v = 0.0;
+      for (int w = 0; w < kBlock / 32; ++w) v += s_red[w][threadIdx.x];
+      a.stats[blockIdx.x * UUV_ST_COUNT + threadIdx.x] += v;
+    }
+  }
+}
+
+// Task reset (mode 1: masked rows reset, prev_u / dev_sum cleared) + observe all rows.
+template <typename R>
+__global__ void __launch_bounds__(kBlock) k_task_reset(const __grid_constant__ TaskArgs<R> a) {
+  __shared__ R s_obs[kBlock * kObsMax];
+  const int64_t row0 = (int64_t)blockIdx.x * kBlock;
+  const int64_t i = row0 + threadIdx.x;
+  const StateView<R>& sv = a.sv;
+  const TaskR<R>& T = a.task;
+  const int A = a.hull[0].r.n_act;
+  const int64_t ld = sv.ld;
+  if (i < sv.n) {
+    R px, py, pz, nu[6], act[UUV_MAX_ACT], pu[UUV_MAX_ACT];
+    Q4<R> q;
+    load_state(sv, i, A, px, py, pz, q, nu, act);
+    int32_t steps = sv.steps[i];
+    const bool do_reset = a.mode == 1 && (a.mask == nullptr || a.mask[i] != 0);
+    if (do_reset) {
+      V3<R> cur;
+      reset_env<R>(sv, i, a.smp, a.seed, px, py, pz, q, nu, cur);
+#pragma unroll
+      for (int j = 0; j < UUV_MAX_ACT; ++j) act[j] = R(0);
+      steps = 0;
+      store_state(sv, i, A, px, py, pz, q, nu, act);
+      sv.steps[i] = 0;
+      sv.diverged[i] = 0;
+      for (int j = 0; j < A; ++j) a.prev_u[j * ld + i] = R(0);
+      if (a.dev_sum != nullptr) a.dev_sum[i] = R(0);
+    }
+#pragma unroll
+    for (int j = 0; j < UUV_MAX_ACT; ++j) pu[j] = j < A ? a.prev_u[j * ld + i] : R(0);
+    observe_row<R>(T, A, px, py, pz, q, nu, pu, steps, a.dt, s_obs + threadIdx.x * T.obs_dim,
+                   nullptr);
+  }
+  __syncthreads();
+  flush_obs<R>(s_obs, a.obs, a.obs_ld, T.obs_dim, row0, sv.n);
+}
+
+// ------------------------------------------------------------------ engine reset
+template <typename R> struct ResetArgs {
+  StateView<R> sv;
+  uuv_sampler smp;
+  uint64_t seed;
+  const uint8_t* mask;
+  int32_t a_max;
+};
+
+template <typename R>
+__global__ void __launch_bounds__(kBlock) k_reset(const __grid_constant__ ResetArgs<R> a) {
+  const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+  const StateView<R>& sv = a.sv;
+  if (i >= sv.n) return;
+  if (a.mask != nullptr && a.mask[i] == 0) return;
+  R px, py, pz, nu[6];
+  Q4<R> q;
+  V3<R> cur;
+  reset_env<R>(sv, i, a.smp, a.seed, px, py, pz, q, nu, cur);
+  R act[UUV_MAX_ACT];
+#pragma unroll
+  for (int j = 0; j < UUV_MAX_ACT; ++j) act[j] = R(0);
+  store_state(sv, i, a.a_max, px, py, pz, q, nu, act);
+  sv.steps[i] = 0;
+  sv.diverged[i] = 0;
+}
+
+// ------------------------------------------------------------------ statistics
+__global__ void k_stats(const double* stats, int64_t n_blocks, double* out, int32_t reset,
+                        double* stats_rw) {
+  // one CTA; thread k sums statistic k over blocks in index order (deterministic)
+  const int k = threadIdx.x;
+  if (k >= UUV_ST_COUNT) return;
+  double v = 0.0;
+  for (int64_t b = 0; b < n_blocks; ++b) v += stats[b * UUV_ST_COUNT + k];
+  out[k] = v;
+  if (reset)
+    for (int64_t b = 0; b < n_blocks; ++b) stats_rw[b * UUV_ST_COUNT + k] = 0.0;
+}
+
+// ------------------------------------------------------------------ inspection kernels
+template <typename R, int NT> struct DeriveArgs {
+  Hull<R> hull[NT];
+  StateView<R> sv;
+  double* out12;
+  double* minv;
+  double* ct_tau;
+  double* mounts;
+};
+
+template <typename R, int NT>
+__global__ void __launch_bounds__(kBlock) k_derive(const __grid_constant__ DeriveArgs<R, NT> a) {
+  const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+  const StateView<R>& sv = a.sv;
+  if (i >= sv.n) return;
+  const Hull<R>& H = a.hull[NT > 1 ? (int)sv.type_id[i] : 0];
+  EnvD e;
+  if (sv.ov != nullptr) {
+    derive_env(H.d, sv.ov, sv.ld, i, sv.slot, e);
+  } else {
+    e.mass = H.d.mass; e.volume = H.d.volume; e.W = H.d.mass * H.d.g; e.B = H.d.rhog * H.d.volume;
+    e.a = e.d = e.rt = e.rc = 1.0;
+    for (int c = 0; c < 3; ++c) { e.r_g[c] = H.d.r_g[c]; e.r_b[c] = H.d.r_b[c]; }
+    for (int k = 0; k < 9; ++k) e.I[k] = H.d.inertia[k];
+  }
+  if (a.out12 != nullptr) {
+    double* o = a.out12 + i * 12;
+    o[0] = e.mass; o[1] = e.volume;
+    for (int c = 0; c < 3; ++c) { o[2 + c] = e.r_g[c]; o[5 + c] = e.r_b[c]; }
+    o[8] = e.W; o[9] = e.B; o[10] = e.a; o[11] = e.d;
+  }
+  if (a.minv != nullptr) {  // M^-1 columns by LDL^T solves of unit vectors
+    double M[21], L[15], Di[6];
+    mass_matrix(H.d, e, M);
+    ldl6<double>(M, L, Di);
+    for (int c = 0; c < 6; ++c) {
+      double b[6] = {0, 0, 0, 0, 0, 0}, x[6];
+      b[c] = 1.0;
+      ldl6_solve<double>(L, Di, b, x);
+      for (int r = 0; r < 6; ++r) a.minv[i * 36 + 6 * r + c] = x[r];
+    }
+  }
+  const int am = sv.a_max;
+  for (int j = 0; j < am; ++j) {
+    if (a.ct_tau != nullptr) {
+      a.ct_tau[i * 2 * am + j] = __dmul_rn(H.d.ct[j], e.rc);
+      a.ct_tau[i * 2 * am + am + j] = __dmul_rn(H.d.tc[j], e.rt);
+    }
+    if (a.mounts != nullptr) {
+      for (int c = 0; c < 3; ++c) {
+        double m = H.d.mount[j][c];
+        if (sv.ov != nullptr && sv.slot[UUV_OV_JITTER] >= 0)
+          m = __dadd_rn(m, sv.ov[(sv.slot[UUV_OV_JITTER] + 3 * j + c) * sv.ld + i]);
+        a.mounts[(i * am + j) * 3 + c] = m;
+      }
+    }
+  }
+}
+
+template <typename R, int NT> struct TermsArgs {
+  Hull<R> hull[NT];
+  StateView<R> sv;
+  const R* cmd;
+  int64_t cmd_ld;
+  R dt;
+  double* out;
+};
+
+template <typename R, int NT, bool DR>
+__global__ void __launch_bounds__(kBlock) k_terms(const __grid_constant__ TermsArgs<R, NT> a) {
+  const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+  const StateView<R>& sv = a.sv;
+  if (i >= sv.n) return;
+  const Hull<R>& H = a.hull[NT > 1 ? (int)sv.type_id[i] : 0];
+  const int A = H.r.n_act;
+  R u[UUV_MAX_ACT];
+  for (int j = 0; j < UUV_MAX_ACT; ++j)
+    u[j] = j < A ? clip_<R>(a.cmd[i * a.cmd_ld + j], R(-1), R(1)) : R(0);
+  R px, py, pz, nu[6], act[UUV_MAX_ACT];
+  Q4<R> q;
+  load_state(sv, i, A, px, py, pz, q, nu, act);
+  Sub<R> s;
+  const double* jit = nullptr;
+  if (DR) {
+    EnvD e;
+    derive_env(H.d, sv.ov, sv.ld, i, sv.slot, e);
+    sub_from_env<R>(H.d, e, a.dt, s);
+    if (sv.slot[UUV_OV_JITTER] >= 0) jit = sv.ov + sv.slot[UUV_OV_JITTER] * sv.ld + i;
+  }
+  const bool has_cur = sv.cur != nullptr;
+  V3<R> cur{R(0), R(0), R(0)};
+  if (has_cur) cur = V3<R>{sv.cur[i], sv.cur[sv.ld + i], sv.cur[2 * sv.ld + i]};
+  Terms<R> tm;
+  const bool ok = substep<R, DR, true>(H.r, s, jit, sv.ld, px, py, pz, q, nu, act, u, has_cur, cur,
+                                       a.dt, &tm);
+  double* o = a.out + i * 48;
+  for (int k = 0; k < 6; ++k) {
+    o[k] = tm.tau[k]; o[6 + k] = tm.hydro[k]; o[12 + k] = tm.c_rb[k]; o[18 + k] = tm.acc[k];
+    o[24 + k] = nu[k];
+  }
+  o[30] = px; o[31] = py; o[32] = pz;
+  o[33] = q.w; o[34] = q.x; o[35] = q.y; o[36] = q.z;
+  for (int j = 0; j < UUV_MAX_ACT; ++j) o[37 + j] = act[j];
+  o[45] = ok ? 1.0 : 0.0;
+  o[46] = o[47] = 0.0;
+}
+
+// ================================================================== host dispatch
+namespace {
+
+int64_t grid_for(int64_t n) { return (n + kBlock - 1) / kBlock; }
+
+uuv_status check_state(const uuv_ctx* ctx, const uuv_state* st) {
+  if (ctx == nullptr || st == nullptr) return fail(UUV_ERR_ARG, "null ctx or state");
+  if (st->dtype != UUV_F32 && st->dtype != UUV_F64)
+    return fail(UUV_ERR_ARG, "state: unknown dtype %d", st->dtype);
+  if (st->n_envs < 0 || st->ld < st->n_envs) return fail(UUV_ERR_SHAPE, "state: ld < n_envs");
+  if (st->a_max < 1 || st->a_max > UUV_MAX_ACT)
+    return fail(UUV_ERR_SHAPE, "state: a_max %d outside [1, %d]", st->a_max, UUV_MAX_ACT);
+  if (!st->p || !st->q || !st->nu || !st->act || !st->steps || !st->episodes || !st->diverged)
+    return fail(UUV_ERR_ARG, "state: null state array");
+  if (ctx->hulls.empty()) return fail(UUV_ERR_ARG, "context has no hulls");
+  if (ctx->hulls.size() > 1 && st->type_id == nullptr)
+    return fail(UUV_ERR_ARG, "state: mixed fleet needs type_id");
+  for (const auto& h : ctx->hulls)
+    if (h.n_act > st->a_max) return fail(UUV_ERR_SHAPE, "state: a_max < hull actuators");
+  if (st->overlay != nullptr)
+    for (int k = 0; k < UUV_OV_COUNT; ++k)
+      if (st->slot[k] >= st->n_slots) return fail(UUV_ERR_SHAPE, "state: slot beyond n_slots");
+  return UUV_OK;
+}
+
+template <typename R> const std::vector<Hull<R>>& hulls_of(const uuv_ctx* c);
+template <> const std::vector<Hull<float>>& hulls_of<float>(const uuv_ctx* c) { return c->hf; }
+template <> const std::vector<Hull<double>>& hulls_of<double>(const uuv_ctx* c) { return c->hd; }
+
+template <typename R, int NT>
+void fill_hulls(const uuv_ctx* ctx, Hull<R>* dst, double dt_sub) {
+  const auto& hs = hulls_of<R>(ctx);
+  for (int t = 0; t < NT; ++t) {
+    dst[t] = hs[t < (int)hs.size() ? t : 0];
+    for (int j = 0; j < UUV_MAX_ACT; ++j) dst[t].r.kdt0[j] = (R)(dt_sub / dst[t].d.tc[j]);
+  }
+}
+
+template <typename R, int NT, bool DR>
+uuv_status launch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd, int64_t cmd_ld,
+                       int32_t K, double dt, cudaStream_t s) {
+  StepArgs<R, NT> a;
+  const double dt_sub = dt / K;
+  fill_hulls<R, NT>(ctx, a.hull, dt_sub);
+  a.sv = make_view<R>(*st);
+  a.cmd = (const R*)cmd;
+  a.cmd_ld = cmd_ld;
+  a.K = K;
+  a.dt = (R)dt_sub;
+  k_step<R, NT, DR><<<(unsigned)grid_for(st->n_envs), kBlock, 0, s>>>(a);
+  return check_launch("uuv_step");
+}
+
+template <typename R>
+uuv_status dispatch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd, int64_t cmd_ld,
+                         int32_t K, double dt, cudaStream_t s) {
+  const bool dr = st->overlay != nullptr;
+  if (ctx->hulls.size() == 1)
+    return dr ? launch_step<R, 1, true>(ctx, st, cmd, cmd_ld, K, dt, s)
+              : launch_step<R, 1, false>(ctx, st, cmd, cmd_ld, K, dt, s);
+  return dr ? launch_step<R, UUV_MAX_TYPES, true>(ctx, st, cmd, cmd_ld, K, dt, s)
+            : launch_step<R, UUV_MAX_TYPES, false>(ctx, st, cmd, cmd_ld, K, dt, s);
+}
+
+uuv_status check_sampler(const uuv_sampler* smp) {
+  if (smp == nullptr) return fail(UUV_ERR_ARG, "null sampler");
+  if (smp->n_overlay < 0 || smp->n_overlay > UUV_MAX_DRAWS)
+    return fail(UUV_ERR_ARG, "sampler: n_overlay %d", smp->n_overlay);
+  for (int d = 0; d < smp->n_overlay; ++d) {
+    const uuv_draw& dr = smp->overlay[d];
+    if (dr.key < 0 || dr.key >= UUV_OV_COUNT) return fail(UUV_ERR_ARG, "sampler: bad key");
+    if (dr.n_draws != 1 && dr.n_draws != 3) return fail(UUV_ERR_ARG, "sampler: bad n_draws");
+    if (dr.dist == UUV_DIST_PIECEWISE &&
+        (dr.pw_bins < 1 || dr.pw_offset < 0 || dr.pw_offset + 2 * dr.pw_bins + 1 > UUV_PW_MAX))
+      return fail(UUV_ERR_ARG, "sampler: piecewise table out of range");
+  }
+  return UUV_OK;
+}
+
+template <typename R>
+void fill_task_args(const uuv_ctx* ctx, const uuv_state* st, const uuv_task* task,
+                    const uuv_sampler* smp, uint64_t seed, double dt, int32_t K,
+                    const uuv_task_io* io, TaskArgs<R>& a) {
+  fill_hulls<R, 1>(ctx, a.hull, dt / K);
+  a.sv = make_view<R>(*st);
+  build_task<R>(*task, a.task);
+  if (smp) a.smp = *smp;
+  else memset(&a.smp, 0, sizeof a.smp);
+  a.seed = seed;
+  a.K = K;
+  a.dt_sub = (R)(dt / K);
+  a.dt = (R)dt;
+  a.prev_u = (R*)io->prev_u;
+  a.dev_sum = (R*)io->dev_sum;
+  a.obs = (R*)io->obs;
+  a.obs_ld = io->obs_ld;
+  a.term_obs = (R*)io->term_obs;
+  a.rout = (R*)io->real_out;
+  a.fout = io->flag_out;
+  a.stats = io->stats;
+  a.mask = nullptr;
+  a.mode = 0;
+  a.cmd = nullptr;
+  a.cmd_ld = 0;
+}
+
+uuv_status check_task(const uuv_ctx* ctx, const uuv_state* st, const uuv_task* task,
+                      const uuv_task_io* io) {
+  if (task == nullptr || io == nullptr) return fail(UUV_ERR_ARG, "null task or io");
+  if (ctx->hulls.size() != 1) return fail(UUV_ERR_UNSUPPORTED, "tasks need a single-vehicle batch");
+  const int A = ctx->hulls[0].n_act;
+  const int extra = task->kind == UUV_TASK_TRACKING ? 3 : (task->kind == UUV_TASK_DOCKING ? 1 : 0);
+  if (task->obs_dim != 12 + A + extra)
+    return fail(UUV_ERR_SHAPE, "task: obs_dim %d != 12 + A + extra = %d", task->obs_dim,
+                12 + A + extra);
+  if (io->obs == nullptr || io->prev_u == nullptr || io->obs_ld < task->obs_dim)
+    return fail(UUV_ERR_ARG, "task io: obs / prev_u missing or obs_ld too small");
+  if (task->kind == UUV_TASK_TRACKING && io->dev_sum == nullptr)
+    return fail(UUV_ERR_ARG, "task io: tracking needs dev_sum");
+  return UUV_OK;
+}
+
+}  // namespace
+
+template <typename R, int NT>
+static uuv_status derive_launch(const uuv_ctx* ctx, const uuv_state* st, double* o12, double* minv,
+                                double* ct_tau, double* mounts, cudaStream_t cs) {
+  DeriveArgs<R, NT> a;
+  fill_hulls<R, NT>(ctx, a.hull, 1.0);
+  a.sv = make_view<R>(*st);
+  a.out12 = o12; a.minv = minv; a.ct_tau = ct_tau; a.mounts = mounts;
+  k_derive<R, NT><<<(unsigned)grid_for(st->n_envs), kBlock, 0, cs>>>(a);
+  return check_launch("uuv_derive_params");
+}
+
+template <typename R, int NT, bool DR>
+static uuv_status terms_launch(const uuv_ctx* ctx, const uuv_state* st, const void* cmd,
+                               int64_t cmd_ld, double dt_sub, double* out, cudaStream_t cs) {
+  TermsArgs<R, NT> a;
+  fill_hulls<R, NT>(ctx, a.hull, dt_sub);
+  a.sv = make_view<R>(*st);
+  a.cmd = (const R*)cmd;
+  a.cmd_ld = cmd_ld;
+  a.dt = (R)dt_sub;
+  a.out = out;
+  k_terms<R, NT, DR><<<(unsigned)grid_for(st->n_envs), kBlock, 0, cs>>>(a);
+  return check_launch("uuv_substep_terms");
+}
+
+template <typename R>
+static uuv_status terms_dispatch(const uuv_ctx* ctx, const uuv_state* st, const void* cmd,
+                                 int64_t cmd_ld, double dt_sub, double* out, cudaStream_t cs) {
+  const bool dr = st->overlay != nullptr, multi = ctx->hulls.size() > 1;
+  if (multi)
+    return dr ? terms_launch<R, UUV_MAX_TYPES, true>(ctx, st, cmd, cmd_ld, dt_sub, out, cs)
+              : terms_launch<R, UUV_MAX_TYPES, false>(ctx, st, cmd, cmd_ld, dt_sub, out, cs);
+  return dr ? terms_launch<R, 1, true>(ctx, st, cmd, cmd_ld, dt_sub, out, cs)
+            : terms_launch<R, 1, false>(ctx, st, cmd, cmd_ld, dt_sub, out, cs);
+}
+
+static uuv_status task_reset_impl(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task,
+                                  const uuv_sampler* sampler, uint64_t seed, const uint8_t* mask,
+                                  double dt, const uuv_task_io* io, int mode, void* stream) {
+  uuv_status s = check_state(ctx, st);
+  if (s != UUV_OK) return s;
+  if ((s = check_task(ctx, st, task, io)) != UUV_OK) return s;
+  if (mode == 1 && (s = check_sampler(sampler)) != UUV_OK) return s;
+  if (st->n_envs == 0) return UUV_OK;
+  cudaStream_t cs = (cudaStream_t)stream;
+  const unsigned g = (unsigned)grid_for(st->n_envs);
+  if (st->dtype == UUV_F32) {
+    TaskArgs<float> a;
+    fill_task_args<float>(ctx, st, task, sampler, seed, dt, 1, io, a);
+    a.mask = mask;
+    a.mode = mode;
+    k_task_reset<float><<<g, kBlock, 0, cs>>>(a);
+  } else {
+    TaskArgs<double> a;
+    fill_task_args<double>(ctx, st, task, sampler, seed, dt, 1, io, a);
+    a.mask = mask;
+    a.mode = mode;
+    k_task_reset<double><<<g, kBlock, 0, cs>>>(a);
+  }
+  return check_launch(mode ? "uuv_task_reset" : "uuv_observe");
+}
+
+// ================================================================== C ABI
+extern "C" {
+
+const char* uuv_last_error(void) { return g_err.c_str(); }
+int32_t uuv_abi_version(void) { return UUV_ABI_VERSION; }
+void uuv_abi_sizes(int64_t out[5]) {
+  out[0] = sizeof(uuv_hull);
+  out[1] = sizeof(uuv_state);
+  out[2] = sizeof(uuv_sampler);
+  out[3] = sizeof(uuv_task);
+  out[4] = sizeof(uuv_task_io);
+}
+
+uuv_status uuv_ctx_set_hulls(uuv_ctx* ctx, const uuv_hull* hulls, int32_t n_types) {
+  if (ctx == nullptr || hulls == nullptr) return fail(UUV_ERR_ARG, "null ctx or hulls");
+  if (n_types < 1 || n_types > UUV_MAX_TYPES)
+    return fail(UUV_ERR_UNSUPPORTED, "n_types %d outside [1, %d]", n_types, UUV_MAX_TYPES);
+  for (int t = 0; t < n_types; ++t) {
+    const uuv_hull& h = hulls[t];
+    if (h.n_act < 1 || h.n_act > UUV_MAX_ACT)
+      return fail(UUV_ERR_UNSUPPORTED, "hull %d: %d actuators outside [1, %d]", t, h.n_act,
+                  UUV_MAX_ACT);
+    if (h.mlp_layers < 0 || h.mlp_layers > UUV_MLP_MAX_LAYERS)
+      return fail(UUV_ERR_UNSUPPORTED, "hull %d: rotor net depth %d", t, h.mlp_layers);
+    int params = 0;
+    for (int l = 0; l < h.mlp_layers; ++l) {
+      if (h.mlp_sizes[l] < 1 || h.mlp_sizes[l] > UUV_MLP_MAX_WIDTH ||
+          h.mlp_sizes[l + 1] < 1 || h.mlp_sizes[l + 1] > UUV_MLP_MAX_WIDTH)
+        return fail(UUV_ERR_UNSUPPORTED, "hull %d: rotor net width", t);
+      params += h.mlp_sizes[l] * h.mlp_sizes[l + 1] + h.mlp_sizes[l + 1];
+    }
+    if (params > UUV_MLP_MAX_PARAMS)
+      return fail(UUV_ERR_UNSUPPORTED, "hull %d: rotor net has %d > %d parameters", t, params,
+                  UUV_MLP_MAX_PARAMS);
+    if (!(h.mass > 0)) return fail(UUV_ERR_ARG, "hull %d: mass must be > 0", t);
+  }
+  ctx->hulls.assign(hulls, hulls + n_types);
+  ctx->hf.resize(n_types);
+  ctx->hd.resize(n_types);
+  for (int t = 0; t < n_types; ++t) {
+    build_hull<float>(hulls[t], ctx->hf[t]);
+    build_hull<double>(hulls[t], ctx->hd[t]);
+    double dinv_min = 1e300;
+    for (int k = 0; k < 6; ++k) dinv_min = ctx->hd[t].r.dinv[k] < dinv_min ? ctx->hd[t].r.dinv[k] : dinv_min;
+    if (!(dinv_min > 0)) return fail(UUV_ERR_ARG, "hull %d: mass matrix not positive definite", t);
+  }
+  return UUV_OK;
+}
+
+uuv_status uuv_ctx_create(const uuv_hull* hulls, int32_t n_types, uuv_ctx** out) {
+  if (out == nullptr) return fail(UUV_ERR_ARG, "null out");
+  uuv_ctx* c = new uuv_ctx();
+  uuv_status s = uuv_ctx_set_hulls(c, hulls, n_types);
+  if (s != UUV_OK) {
+    delete c;
+    *out = nullptr;
+    return s;
+  }
+  *out = c;
+  return UUV_OK;
+}
+
+void uuv_ctx_destroy(uuv_ctx* ctx) { delete ctx; }
+
+uuv_status uuv_step(uuv_ctx* ctx, const uuv_state* st, const void* commands, int64_t cmd_ld,
+                    int32_t substeps, double dt, void* stream) {
+  uuv_status s = check_state(ctx, st);
+  if (s != UUV_OK) return s;
+  if (commands == nullptr) return fail(UUV_ERR_ARG, "commands: null");
+  if (cmd_ld < st->a_max && ctx->hulls.size() > 1)
+    return fail(UUV_ERR_SHAPE, "commands: row stride %lld < a_max %d", (long long)cmd_ld, st->a_max);
+  if (cmd_ld < ctx->hulls[0].n_act)
+    return fail(UUV_ERR_SHAPE, "commands: row stride %lld < action_dim %d", (long long)cmd_ld,
+                ctx->hulls[0].n_act);
+  if (substeps < 1) return fail(UUV_ERR_ARG, "substeps must be >= 1, got %d", substeps);
+  if (!(dt > 0)) return fail(UUV_ERR_ARG, "dt must be > 0");
+  if (st->n_envs == 0) return UUV_OK;
+  cudaStream_t cs = (cudaStream_t)stream;
+  return st->dtype == UUV_F32 ? dispatch_step<float>(ctx, st, commands, cmd_ld, substeps, dt, cs)
+                              : dispatch_step<double>(ctx, st, commands, cmd_ld, substeps, dt, cs);
+}
+
+uuv_status uuv_reset(uuv_ctx* ctx, const uuv_state* st, const uint8_t* mask,
+                     const uuv_sampler* sampler, uint64_t seed, void* stream) {
+  uuv_status s = check_state(ctx, st);
+  if (s != UUV_OK) return s;
+  if ((s = check_sampler(sampler)) != UUV_OK) return s;
+  if (st->n_envs == 0) return UUV_OK;
+  cudaStream_t cs = (cudaStream_t)stream;
+  const unsigned g = (unsigned)grid_for(st->n_envs);
+  if (st->dtype == UUV_F32) {
+    ResetArgs<float> a{make_view<float>(*st), *sampler, seed, mask, st->a_max};
+    k_reset<float><<<g, kBlock, 0, cs>>>(a);
+  } else {
+    ResetArgs<double> a{make_view<double>(*st), *sampler, seed, mask, st->a_max};
+    k_reset<double><<<g, kBlock, 0, cs>>>(a);
+  }
+  return check_launch("uuv_reset");
+}
+
+uuv_status uuv_task_step(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task,
+                         const uuv_sampler* sampler, uint64_t seed, const void* commands,
+                         int64_t cmd_ld, int32_t substeps, double dt, const uuv_task_io* io,
+                         void* stream) {
+  uuv_status s = check_state(ctx, st);
+  if (s != UUV_OK) return s;
+  if ((s = check_task(ctx, st, task, io)) != UUV_OK) return s;
+  if ((s = check_sampler(sampler)) != UUV_OK) return s;
+  if (commands == nullptr || cmd_ld < ctx->hulls[0].n_act)
+    return fail(UUV_ERR_SHAPE, "commands: null or row stride < action_dim");
+  if (substeps < 1 || !(dt > 0)) return fail(UUV_ERR_ARG, "substeps >= 1 and dt > 0 required");
+  if (st->n_envs == 0) return UUV_OK;
+  cudaStream_t cs = (cudaStream_t)stream;
+  const unsigned g = (unsigned)grid_for(st->n_envs);
+  const bool dr = st->overlay != nullptr;
+  if (st->dtype == UUV_F32) {
+    TaskArgs<float> a;
+    fill_task_args<float>(ctx, st, task, sampler, seed, dt, substeps, io, a);
+    a.cmd = (const float*)commands;
+    a.cmd_ld = cmd_ld;
+    if (dr) k_task_step<float, true><<<g, kBlock, 0, cs>>>(a);
+    else k_task_step<float, false><<<g, kBlock, 0, cs>>>(a);
+  } else {
+    TaskArgs<double> a;
+    fill_task_args<double>(ctx, st, task, sampler, seed, dt, substeps, io, a);
+    a.cmd = (const double*)commands;
+    a.cmd_ld = cmd_ld;
+    if (dr) k_task_step<double, true><<<g, kBlock, 0, cs>>>(a);
+    else k_task_step<double, false><<<g, kBlock, 0, cs>>>(a);
+  }
+  return check_launch("uuv_task_step");
+}
+
+uuv_status uuv_task_reset(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task,
+                          const uuv_sampler* sampler, uint64_t seed, const uint8_t* mask,
+                          double dt, const uuv_task_io* io, void* stream) {
+  return task_reset_impl(ctx, st, task, sampler, seed, mask, dt, io, 1, stream);
+}
+
+uuv_status uuv_observe(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task, double dt,
+                       const uuv_task_io* io, void* stream) {
+  return task_reset_impl(ctx, st, task, nullptr, 0, nullptr, dt, io, 0, stream);
+}
+
+int64_t uuv_stats_blocks(int64_t n_envs) { return grid_for(n_envs); }
+
+uuv_status uuv_rollout_stats(const double* stats, int64_t n_blocks, double* out, int32_t reset,
+                             void* stream) {
+  if (stats == nullptr || out == nullptr || n_blocks < 0)
+    return fail(UUV_ERR_ARG, "rollout_stats: bad arguments");
+  k_stats<<<1, 32, 0, (cudaStream_t)stream>>>(stats, n_blocks, out, reset, (double*)stats);
+  return check_launch("uuv_rollout_stats");
+}
+
+uuv_status uuv_derive_params(uuv_ctx* ctx, const uuv_state* st, double* out12, double* minv,
+                             double* ct_tau, double* mounts, void* stream) {
+  uuv_status s = check_state(ctx, st);
+  if (s != UUV_OK) return s;
+  if (st->n_envs == 0) return UUV_OK;
+  cudaStream_t cs = (cudaStream_t)stream;
+  const bool multi = ctx->hulls.size() > 1;
+  if (st->dtype == UUV_F32)
+    return multi ? derive_launch<float, UUV_MAX_TYPES>(ctx, st, out12, minv, ct_tau, mounts, cs)
+                 : derive_launch<float, 1>(ctx, st, out12, minv, ct_tau, mounts, cs);
+  return multi ? derive_launch<double, UUV_MAX_TYPES>(ctx, st, out12, minv, ct_tau, mounts, cs)
+               : derive_launch<double, 1>(ctx, st, out12, minv, ct_tau, mounts, cs);
+}
+
+uuv_status uuv_substep_terms(uuv_ctx* ctx, const uuv_state* st, const void* commands,
+                             int64_t cmd_ld, double dt_sub, double* out, void* stream) {
+  uuv_status s = check_state(ctx, st);
+  if (s != UUV_OK) return s;
+  if (commands == nullptr || out == nullptr) return fail(UUV_ERR_ARG, "null commands/out");
+  if (st->n_envs == 0) return UUV_OK;
+  cudaStream_t cs = (cudaStream_t)stream;
+  return st->dtype == UUV_F32 ? terms_dispatch<float>(ctx, st, commands, cmd_ld, dt_sub, out, cs)
+                              : terms_dispatch<double>(ctx, st, commands, cmd_ld, dt_sub, out, cs);
+}
+
+}  // extern "C"

@@ -1,0 +1,739 @@
+"""Batched lockstep engine over the B200 kernels — the reference API, on device.
+
+Drop-in for ``uuvsim/engine.py``: ``SimConfig`` (63-77), ``make_batch``
+(298-320), ``step_batch`` (465-484), ``reset_envs`` (487-512),
+``env_snapshot`` (515-527), ``throughput_probe`` (541-564), ``EnvInit`` /
+``default_sampler`` (252-266), ``BatchState.env_rng`` (291-295).
+
+State fields keep the reference names and shapes — ``p`` (N,3), ``q``
+(N,4) wxyz body->NED, ``nu`` (N,6), ``act`` (N,A), ``current_ned`` (N,3),
+``steps`` / ``episodes`` (N,), ``diverged`` (N,) — but are torch CUDA tensors
+that view a struct-of-arrays HBM layout (component-major, rows padded to a
+multiple of 32), so every kernel load is a fully coalesced 128-byte line.
+``steps`` / ``episodes`` are int32.  float32 is the default compute dtype;
+``dtype=torch.float64`` selects the validation build (parity ~1e-12).
+
+Every step is ONE kernel launch (``uuv_step``) with K substeps fused in
+registers; no host synchronisation happens inside ``step_batch``.
+Per-(seed, env, episode) randomness is numpy-compatible Philox4x64-10:
+``Philox(key=[seed, env_offset + i], counter=[0, episode, 0, 0])``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import time
+from dataclasses import dataclass, field
+from typing import Callable
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .randomization import CURRENT_KEYS, Piecewise, Uniform
+from .vehicles import (
+    DATA_DRIVEN, FIRST_ORDER, KIND_CODE, MODEL_CODE, RUDDER, TILTROTOR, VehicleConfig,
+    fin_basis, tilt_rotation, validate_overlay,
+)
+
+M64 = (1 << 64) - 1
+_ALIGN = 32
+
+
+class EngineError(ValueError):
+    pass
+
+
+@dataclass
+class SimConfig:
+    dt: float = 0.02
+    substeps: int = 1
+    batch_size: int = 1
+    workers: int = 1  # accepted for API parity; results never depend on it
+
+    def __post_init__(self):
+        if self.dt <= 0:
+            raise EngineError(f"dt must be > 0, got {self.dt}")
+        if self.substeps < 1:
+            raise EngineError(f"substeps must be >= 1, got {self.substeps}")
+        if self.batch_size < 1:
+            raise EngineError(f"batch_size must be >= 1, got {self.batch_size}")
+        if self.workers < 1:
+            raise EngineError(f"workers must be >= 1, got {self.workers}")
+
+
+@dataclass
+class Pose:
+    p: np.ndarray = field(default_factory=lambda: np.zeros(3))
+    q: np.ndarray = field(default_factory=lambda: np.array([1.0, 0.0, 0.0, 0.0]))
+
+    def __post_init__(self):
+        self.p = np.asarray(self.p, dtype=float)
+        self.q = np.asarray(self.q, dtype=float)
+
+
+@dataclass
+class EnvInit:
+    pose: Pose
+    nu: np.ndarray = field(default_factory=lambda: np.zeros(6))
+    overlay: dict = field(default_factory=dict)
+    current_ned: np.ndarray = field(default_factory=lambda: np.zeros(3))
+
+
+InitSampler = Callable[[int, int, np.random.Generator], EnvInit]
+
+
+def default_sampler(env_index: int, episode: int, rng) -> EnvInit:
+    """Identity pose, zero velocity, no overlay, no current (engine.py:265-266)."""
+    return EnvInit(pose=Pose())
+
+
+def philox_generator(seed: int, env_index: int, episode: int) -> np.random.Generator:
+    """Host twin of the device stream (same bits as the reset kernel)."""
+    return np.random.Generator(np.random.Philox(
+        key=np.array([int(seed) & M64, int(env_index) & M64], dtype=np.uint64),
+        counter=np.array([0, int(episode) & M64, 0, 0], dtype=np.uint64)))
+
+
+# ================================================================ hull packing
+
+
+def pack_hull(veh: VehicleConfig) -> N.Hull:
+    """Compile one vehicle into the ABI hull table (compile_layout, engine.py:129-189)."""
+    acts = veh.actuators
+    A = len(acts)
+    if not 1 <= A <= N.MAX_ACT:
+        raise EngineError(f"{veh.name}: {A} actuators, the device build supports 1..{N.MAX_ACT}")
+    h = N.Hull()
+    h.n_act = A
+    rb, co = veh.rb, veh.coeffs
+    h.mass, h.volume, h.rho, h.g = rb.mass, rb.displaced_volume, co.fluid_density, co.gravity
+    for k in range(3):
+        h.r_g[k], h.r_b[k] = rb.r_g[k], rb.r_b[k]
+    for k, v in enumerate(np.asarray(rb.inertia, float).ravel()):
+        h.inertia[k] = v
+    for name in ("M_A", "D_lin", "D_quad"):
+        dst = getattr(h, name)
+        for k, v in enumerate(np.asarray(getattr(co, name), float).ravel()):
+            dst[k] = v
+    nets = []
+    for j, a in enumerate(acts):
+        h.kind[j] = KIND_CODE[a.kind]
+        h.model[j] = MODEL_CODE[a.rotor_model]
+        h.limit[j] = a.state_limit
+        h.deadzone[j] = a.deadzone
+        h.reaction[j] = a.reaction_coeff
+        h.thrust_coeff[j] = a.thrust_coeff
+        h.time_constant[j] = a.time_constant
+        axis = tilt_rotation(a.mount_axis, a.tilt_axis, a.tilt_angle_default) \
+            if a.kind == TILTROTOR else a.mount_axis
+        for c in range(3):
+            h.mount[j][c] = a.mount_position[c]
+            h.axis[j][c] = axis[c]
+        if a.kind == RUDDER:
+            xf, yf = fin_basis(a.mount_axis)
+            for c in range(3):
+                h.fin_xf[j][c], h.fin_yf[j][c] = xf[c], yf[c]
+            g = a.rudder
+            h.fin_area[j], h.fin_cla[j], h.fin_cd0[j] = g.area, g.c_l_alpha, g.c_d0
+            h.fin_kd[j], h.fin_stall[j], h.fin_rho[j] = g.k_d, g.stall_angle, g.fluid_density
+        if a.rotor_model == DATA_DRIVEN:
+            if a.mlp is None:
+                raise EngineError(f"actuator {j}: data_driven model has no weights")
+            if all(a.mlp is not n for n in nets):
+                nets.append(a.mlp)
+    if len(nets) > 1:
+        raise EngineError(f"{veh.name}: the device build supports one rotor network per vehicle")
+    if nets:
+        net = nets[0]
+        sizes = list(net.layer_sizes)
+        if len(sizes) - 1 > N.MLP_MAX_LAYERS or max(sizes) > N.MLP_MAX_WIDTH:
+            raise EngineError(f"{veh.name}: rotor network {sizes} exceeds the device envelope")
+        flat = np.concatenate([np.concatenate([np.asarray(w, float).ravel(),
+                                               np.asarray(b, float).ravel()])
+                               for w, b in zip(net.weights, net.biases)])
+        if flat.size > N.MLP_MAX_PARAMS:
+            raise EngineError(f"{veh.name}: rotor network has {flat.size} > "
+                              f"{N.MLP_MAX_PARAMS} parameters")
+        h.mlp_layers = len(sizes) - 1
+        for k, s in enumerate(sizes):
+            h.mlp_sizes[k] = s
+        h.mlp_relu = 1 if net.activation == "relu" else 0
+        for k, v in enumerate(flat):
+            h.mlp[k] = v
+    return h
+
+
+# ================================================================ declarative samplers
+
+
+@dataclass
+class DeviceSampler:
+    """An episode sampler the reset kernel evaluates (tasks/core.py:282-289).
+
+    ``overlay_spec``: DR spec without current keys, drawn in sorted key order;
+    ``current_spec``: spec holding ``current_velocity`` [+ ``current_direction``];
+    ``start``: None (identity pose) or the 7-tuple of ``tasks.start_box``.
+    """
+
+    overlay_spec: dict | None = None
+    current_spec: dict | None = None
+    start: tuple | None = None
+
+    def keys(self):
+        return sorted(self.overlay_spec) if self.overlay_spec else []
+
+    def pack(self) -> N.Sampler:
+        s = N.Sampler()
+        pw = []
+
+        def fill(d: N.Draw, key_code, dist, n_draws):
+            d.key = key_code
+            d.n_draws = n_draws
+            if isinstance(dist, Uniform):
+                d.dist, d.lo, d.hi = N.DIST_UNIFORM, dist.lo, dist.hi
+            elif isinstance(dist, Piecewise):
+                d.dist = N.DIST_PIECEWISE
+                d.pw_bins = dist.densities.size
+                d.pw_offset = len(pw)
+                pw.extend(list(dist.breakpoints) + list(dist._cdf))
+            else:
+                raise EngineError(f"{type(dist).__name__} distributions are sampled by the "
+                                  "host reset path, not the device sampler")
+
+        keys = self.keys()
+        if len(keys) > N.MAX_DRAWS:
+            raise EngineError(f"at most {N.MAX_DRAWS} overlay keys")
+        s.n_overlay = len(keys)
+        for d, key in enumerate(keys):
+            p = self.overlay_spec[key]
+            fill(s.overlay[d], N.OV_INDEX[key], p.distribution, 3 if p.vector_valued else 1)
+        cs = self.current_spec or {}
+        if "current_velocity" in cs:
+            fill(s.current_speed, 0, cs["current_velocity"].distribution, 1)
+            if "current_direction" in cs:
+                s.current_mode = N.CURRENT_HEADING_DRAW
+                fill(s.current_heading, 0, cs["current_direction"].distribution, 1)
+            else:
+                s.current_mode = N.CURRENT_RANDOM_HEADING
+        if self.start is not None:
+            s.start_mode = N.START_BOX
+            base, plo, phi, elo, ehi, nlo, nhi = self.start
+            for c in range(3):
+                s.p_base[c], s.p_lo[c], s.p_hi[c] = base[c], plo[c], phi[c]
+                s.eul_lo[c], s.eul_hi[c] = elo[c], ehi[c]
+            for c in range(6):
+                s.nu_lo[c], s.nu_hi[c] = nlo[c], nhi[c]
+        if len(pw) > N.PW_MAX:
+            raise EngineError(f"piecewise tables exceed {N.PW_MAX} entries")
+        for k, v in enumerate(pw):
+            s.pw_table[k] = v
+        return s
+
+
+def spec_sampler(dr_spec: dict | None, start=None) -> DeviceSampler:
+    """Device sampler for a DR spec (current keys split off) and a start box."""
+    if dr_spec is None:
+        return DeviceSampler(None, None, start)
+    dyn = {k: p for k, p in dr_spec.items() if k not in CURRENT_KEYS}
+    cur = {k: p for k, p in dr_spec.items() if k in CURRENT_KEYS}
+    return DeviceSampler(dyn or None, cur or None, start)
+
+
+_IDENTITY = DeviceSampler()
+
+
+# ================================================================ batch state
+
+
+class ParamsView:
+    """Per-env parameters (BatchParams, engine.py:193-234), derived on device from
+    the hull table and the overlay record; float64, read-only copies."""
+
+    def __init__(self, state: "BatchState"):
+        self._st = state
+
+    def _derive(self):
+        st = self._st
+        n, am = st.n_envs, st.a_max
+        dev = st.device
+        out12 = torch.empty((n, 12), dtype=torch.float64, device=dev)
+        minv = torch.empty((n, 6, 6), dtype=torch.float64, device=dev)
+        ct_tau = torch.empty((n, 2, am), dtype=torch.float64, device=dev)
+        mounts = torch.empty((n, am, 3), dtype=torch.float64, device=dev)
+        lib = N.load()
+        N.check(lib.uuv_derive_params(st._ctx, C.byref(st._cstate()), out12.data_ptr(),
+                                      minv.data_ptr(), ct_tau.data_ptr(), mounts.data_ptr(),
+                                      st._stream()), EngineError)
+        return out12, minv, ct_tau, mounts
+
+    def __getattr__(self, name):
+        if name.startswith("_"):
+            raise AttributeError(name)
+        o12, minv, ct_tau, mounts = self._derive()
+        table = {"mass": o12[:, 0], "volume": o12[:, 1], "r_g": o12[:, 2:5], "r_b": o12[:, 5:8],
+                 "weight": o12[:, 8], "buoyancy": o12[:, 9], "added_mass_scale": o12[:, 10],
+                 "damping_scale": o12[:, 11], "M_inv": minv, "thrust_coeff": ct_tau[:, 0],
+                 "time_constant": ct_tau[:, 1], "mounts": mounts}
+        if name not in table:
+            raise AttributeError(name)
+        return table[name]
+
+    def write_row(self, i, cfg: VehicleConfig):
+        """Give env ``i`` the parameters of ``cfg`` (same actuator layout), as a new hull type."""
+        self._st._assign_vehicle(int(i), cfg)
+
+
+class BatchState:
+    """N environments of one vehicle (or a mixed fleet) resident in HBM."""
+
+    def __init__(self, vehicles, counts, sim: SimConfig, master_seed=0, device=None,
+                 dtype=torch.float32, env_offset=0):
+        if dtype not in (torch.float32, torch.float64):
+            raise EngineError("dtype must be torch.float32 or torch.float64")
+        self.sim = sim
+        self.vehicles = list(vehicles)
+        self.vehicle = self.vehicles[0]
+        self.master_seed = int(master_seed)
+        self.env_offset = int(env_offset)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.dtype = dtype
+        n = int(sum(counts))
+        if n != sim.batch_size:
+            raise EngineError(f"fleet counts sum to {n}, batch_size is {sim.batch_size}")
+        self.n_envs = n
+        self.a_max = max(v.action_dim for v in self.vehicles)
+        self._ld = ld = max(_ALIGN, -(-n // _ALIGN) * _ALIGN)
+        kw = dict(device=self.device)
+        self._p = torch.zeros((3, ld), dtype=dtype, **kw)
+        self._q = torch.zeros((4, ld), dtype=dtype, **kw)
+        self._q[0] = 1.0
+        self._nu = torch.zeros((6, ld), dtype=dtype, **kw)
+        self._act = torch.zeros((self.a_max, ld), dtype=dtype, **kw)
+        self._cur = None
+        self.steps = torch.zeros(ld, dtype=torch.int32, **kw)[:n]
+        self.episodes = torch.full((ld,), -1, dtype=torch.int32, **kw)[:n]
+        self.diverged = torch.zeros(ld, dtype=torch.bool, **kw)[:n]
+        self._type = None
+        if len(self.vehicles) > 1:
+            ids = np.repeat(np.arange(len(counts), dtype=np.uint8), counts)
+            self._type = torch.zeros(ld, dtype=torch.uint8, **kw)
+            self._type[:n] = torch.from_numpy(ids).to(self.device)
+        self._ov = None
+        self._ov_keys = None
+        self._slots = {}
+        self._host_overlays = {}
+        self._hulls = [pack_hull(v) for v in self.vehicles]
+        self._ctx = C.c_void_p()
+        arr = (N.Hull * len(self._hulls))(*self._hulls)
+        N.check(N.load().uuv_ctx_create(arr, len(self._hulls), C.byref(self._ctx)), EngineError)
+        self.params = ParamsView(self)
+        self.layout = _Layout(self)
+
+    def __del__(self):
+        ctx = getattr(self, "_ctx", None)
+        if ctx is not None and ctx.value:
+            try:
+                N.load().uuv_ctx_destroy(ctx)
+            except Exception:
+                pass
+
+    # ---------------------------------------------------------------- reference fields
+    @property
+    def p(self):
+        return self._p[:, :self.n_envs].t()
+
+    @property
+    def q(self):
+        return self._q[:, :self.n_envs].t()
+
+    @property
+    def nu(self):
+        return self._nu[:, :self.n_envs].t()
+
+    @property
+    def act(self):
+        return self._act[:, :self.n_envs].t()
+
+    @property
+    def current_ned(self):
+        """(N,3) NED current.  Touching it enables the current term in the kernel."""
+        self._enable_current()
+        return self._cur[:, :self.n_envs].t()
+
+    @property
+    def type_id(self):
+        return None if self._type is None else self._type[:self.n_envs]
+
+    @property
+    def tilt(self):
+        """Tilt angles stay at their defaults (engine.py:139-143, 507)."""
+        cols = [[a.tilt_angle_default for a in v.actuators] + [0.0] * (self.a_max - v.action_dim)
+                for v in self.vehicles]
+        t = torch.tensor(cols, dtype=self.dtype, device=self.device)
+        ids = self.type_id.long() if self._type is not None else torch.zeros(
+            self.n_envs, dtype=torch.long, device=self.device)
+        return t[ids]
+
+    @property
+    def overlays(self) -> list:
+        """Per-env overlay dicts of the last reset (copied to the host)."""
+        n = self.n_envs
+        out = [dict(self._host_overlays.get(i, {})) for i in range(n)]
+        if self._ov is None:
+            return out
+        ov = self._ov[:, :n].cpu().numpy()
+        keys = self._ov_keys[:n].cpu().numpy().astype(np.int64) & 0xFFFF
+        for i in range(n):
+            if i in self._host_overlays or keys[i] == 0:
+                continue
+            d = {}
+            for name, s0 in self._slots.items():
+                if keys[i] >> N.OV_INDEX[name] & 1:
+                    if name == "payload_position":
+                        d[name] = ov[s0:s0 + 3, i].copy()
+                    elif name == "mount_position_jitter":
+                        d[name] = ov[s0:s0 + 3, i].copy()
+                    else:
+                        d[name] = float(ov[s0, i])
+            out[i] = d
+        return out
+
+    def env_rng(self, i: int) -> np.random.Generator:
+        """The counter-based substream of env i's current episode (engine.py:291-295)."""
+        return philox_generator(self.master_seed, self.env_offset + int(i),
+                                int(self.episodes[int(i)].item()))
+
+    # ---------------------------------------------------------------- internals
+    def _stream(self):
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def _enable_current(self):
+        if self._cur is None:
+            self._cur = torch.zeros((3, self._ld), dtype=self.dtype, device=self.device)
+
+    def _ensure_slots(self, keys):
+        keys = [k for k in keys if k in N.OV_INDEX]
+        missing = [k for k in keys if k not in self._slots]
+        if not missing:
+            return
+        names = sorted(set(self._slots) | set(missing), key=lambda k: N.OV_INDEX[k])
+        slots, n_slots = {}, 0
+        for k in names:
+            slots[k] = n_slots
+            n_slots += N.OV_WIDTH[k]
+        ov = torch.empty((n_slots, self._ld), dtype=torch.float64, device=self.device)
+        for k in names:
+            s0, w = slots[k], N.OV_WIDTH[k]
+            if k in self._slots:
+                o0 = self._slots[k]
+                ov[s0:s0 + w] = self._ov[o0:o0 + w]
+            else:
+                ov[s0:s0 + w] = N.OV_IDENTITY[k]
+        self._ov, self._slots = ov, slots
+        if self._ov_keys is None:
+            self._ov_keys = torch.zeros(self._ld, dtype=torch.int16, device=self.device)
+
+    def _cstate(self) -> N.State:
+        s = N.State()
+        s.dtype = N.F32 if self.dtype == torch.float32 else N.F64
+        s.a_max = self.a_max
+        s.n_envs, s.ld, s.env_offset = self.n_envs, self._ld, self.env_offset
+        s.p, s.q, s.nu, s.act = (self._p.data_ptr(), self._q.data_ptr(), self._nu.data_ptr(),
+                                 self._act.data_ptr())
+        s.current_ned = self._cur.data_ptr() if self._cur is not None else None
+        s.steps, s.episodes = self.steps.data_ptr(), self.episodes.data_ptr()
+        s.diverged = self.diverged.data_ptr()
+        s.type_id = self._type.data_ptr() if self._type is not None else None
+        s.overlay = self._ov.data_ptr() if self._ov is not None else None
+        s.overlay_keys = self._ov_keys.data_ptr() if self._ov_keys is not None else None
+        s.n_slots = 0 if self._ov is None else self._ov.shape[0]
+        for k in range(N.OV_COUNT):
+            s.slot[k] = -1
+        for name, s0 in self._slots.items():
+            s.slot[N.OV_INDEX[name]] = s0
+        return s
+
+    def _assign_vehicle(self, i, cfg):
+        if cfg.action_dim > self.a_max:
+            raise EngineError("write_row: vehicle has more actuators than the batch")
+        for t, v in enumerate(self.vehicles):
+            if v is cfg:
+                break
+        else:
+            if len(self.vehicles) >= N.MAX_TYPES:
+                raise EngineError(f"write_row: at most {N.MAX_TYPES} distinct parameter sets "
+                                  "per batch in the device build")
+            self.vehicles.append(cfg)
+            self._hulls.append(pack_hull(cfg))
+            t = len(self.vehicles) - 1
+            arr = (N.Hull * len(self._hulls))(*self._hulls)
+            N.check(N.load().uuv_ctx_set_hulls(self._ctx, arr, len(self._hulls)), EngineError)
+        if self._type is None:
+            self._type = torch.zeros(self._ld, dtype=torch.uint8, device=self.device)
+        self._type[i] = t
+
+
+class _Layout:
+    def __init__(self, st: BatchState):
+        self.action_dim = st.vehicle.action_dim
+        self.a_max = st.a_max
+        self.fluid_density = st.vehicle.coeffs.fluid_density
+        self.gravity = st.vehicle.coeffs.gravity
+
+
+# ================================================================ public API
+
+
+def make_batch(vehicle: VehicleConfig, sim: SimConfig, master_seed: int = 0, *, device=None,
+               dtype=torch.float32, env_offset: int = 0) -> BatchState:
+    """Allocate a batch primed with the base vehicle; call reset_envs to start."""
+    return BatchState([vehicle], [sim.batch_size], sim, master_seed, device, dtype, env_offset)
+
+
+def make_fleet_batch(vehicles, counts, sim: SimConfig, master_seed: int = 0, *, device=None,
+                     dtype=torch.float32, env_offset: int = 0) -> BatchState:
+    """Mixed-vehicle batch: contiguous env blocks per vehicle type, commands padded to A_max."""
+    if len(vehicles) != len(counts) or not 1 <= len(vehicles) <= N.MAX_TYPES:
+        raise EngineError(f"need 1..{N.MAX_TYPES} vehicles with one count each")
+    return BatchState(vehicles, counts, sim, master_seed, device, dtype, env_offset)
+
+
+def _commands(state: BatchState, commands, width):
+    n = state.n_envs
+    if torch.is_tensor(commands):
+        t = commands
+        if tuple(t.shape) != (n, width):
+            raise EngineError(f"commands: expected shape {(n, width)}, got {tuple(t.shape)}")
+        if t.device != state.device or t.dtype != state.dtype:
+            t = t.to(device=state.device, dtype=state.dtype)
+    else:
+        arr = np.asarray(commands, dtype=np.float64)
+        if arr.shape != (n, width):
+            raise EngineError(f"commands: expected shape {(n, width)}, got {arr.shape}")
+        t = torch.from_numpy(arr).to(device=state.device, dtype=state.dtype)
+    if t.stride(1) != 1 or t.stride(0) < width:
+        t = t.contiguous()
+    return t
+
+
+def step_batch(state: BatchState, commands) -> BatchState:
+    """Advance every environment one control step (engine.py:465-484)."""
+    width = state.a_max if len(state.vehicles) > 1 or state._type is not None else \
+        state.vehicle.action_dim
+    cmd = _commands(state, commands, width)
+    N.check(N.load().uuv_step(state._ctx, C.byref(state._cstate()), cmd.data_ptr(),
+                              cmd.stride(0), state.sim.substeps, state.sim.dt, state._stream()),
+            EngineError)
+    return state
+
+
+def _mask(state: BatchState, mask):
+    n = state.n_envs
+    if torch.is_tensor(mask):
+        m = mask
+        if tuple(m.shape) != (n,):
+            raise EngineError(f"mask: expected shape {(n,)}, got {tuple(m.shape)}")
+        return m.to(device=state.device, dtype=torch.bool).contiguous()
+    arr = np.asarray(mask, dtype=bool)
+    if arr.shape != (n,):
+        raise EngineError(f"mask: expected shape {(n,)}, got {arr.shape}")
+    return torch.from_numpy(arr).to(state.device)
+
+
+def reset_envs(state: BatchState, mask, sampler: InitSampler = default_sampler) -> BatchState:
+    """Re-initialise masked envs from their episode substreams (engine.py:487-512).
+
+    ``default_sampler`` and ``DeviceSampler`` objects run in the reset kernel;
+    any other Python callable runs on the host, one call per masked row, with
+    the same Philox stream, and the rows are uploaded.
+    """
+    m = _mask(state, mask)
+    if sampler is default_sampler:
+        sampler = _IDENTITY
+    if isinstance(sampler, DeviceSampler):
+        _device_reset(state, m, sampler)
+    else:
+        _host_reset(state, m, sampler)
+    return state
+
+
+def _device_reset(state: BatchState, m, sampler: DeviceSampler):
+    keys = sampler.keys()
+    if keys:
+        state._ensure_slots(keys)
+    if sampler.current_spec:
+        state._enable_current()
+    rows_mask = m.to(torch.uint8)
+    packed = sampler.pack()
+    if state._host_overlays:
+        idx = torch.nonzero(m).flatten().cpu().tolist()
+        for i in idx:
+            state._host_overlays.pop(i, None)
+    N.check(N.load().uuv_reset(state._ctx, C.byref(state._cstate()), rows_mask.data_ptr(),
+                               C.byref(packed), state.master_seed & M64, state._stream()),
+            EngineError)
+
+
+def _host_reset(state: BatchState, m, sampler):
+    rows = torch.nonzero(m).flatten().cpu().numpy()
+    if rows.size == 0:
+        return
+    eps = state.episodes[torch.from_numpy(rows).to(state.device)].cpu().numpy().astype(np.int64) + 1
+    inits = []
+    for i, ep in zip(rows, eps):
+        init = sampler(int(i), int(ep), philox_generator(state.master_seed,
+                                                         state.env_offset + int(i), int(ep)))
+        ov = dict(init.overlay)
+        if ov:
+            validate_overlay(state.vehicles[0] if state._type is None else state.vehicle, ov)
+        inits.append((init, ov))
+    keys = sorted({k for _, ov in inits for k in ov if k in N.OV_INDEX})
+    if keys:
+        state._ensure_slots(keys)
+    cur = np.array([np.asarray(init.current_ned, float) for init, _ in inits])
+    if np.any(cur != 0.0):
+        state._enable_current()
+    dev = state.device
+    idx = torch.from_numpy(rows).to(dev)
+    dt = state.dtype
+    p = torch.from_numpy(np.array([init.pose.p for init, _ in inits], float)).to(dev, dt)
+    q = torch.from_numpy(np.array([init.pose.q for init, _ in inits], float)).to(dev, dt)
+    nu = torch.from_numpy(np.array([np.asarray(init.nu, float) for init, _ in inits])).to(dev, dt)
+    state._p[:, idx] = p.t()
+    state._q[:, idx] = q.t()
+    state._nu[:, idx] = nu.t()
+    state._act[:, idx] = 0.0
+    if state._cur is not None:
+        state._cur[:, idx] = torch.from_numpy(cur).to(dev, dt).t()
+    state.steps[idx] = 0
+    state.diverged[idx] = False
+    state.episodes[idx] = torch.from_numpy(eps.astype(np.int32)).to(dev)
+    if state._ov is not None:
+        block = np.empty((state._ov.shape[0], rows.size))
+        kbits = np.zeros(rows.size, dtype=np.int64)
+        for name, s0 in state._slots.items():
+            block[s0:s0 + N.OV_WIDTH[name]] = N.OV_IDENTITY[name]
+        for r, (_, ov) in enumerate(inits):
+            for name, v in ov.items():
+                if name not in state._slots:
+                    continue
+                s0 = state._slots[name]
+                kbits[r] |= 1 << N.OV_INDEX[name]
+                if name == "payload_position":
+                    block[s0:s0 + 3, r] = np.asarray(v, float)
+                elif name == "mount_position_jitter":
+                    jv = np.asarray(v, float)
+                    jm = np.zeros((N.MAX_ACT, 3))
+                    jm[:] = jv if jv.ndim == 1 else 0.0
+                    if jv.ndim == 2:
+                        jm[:jv.shape[0]] = jv
+                    block[s0:s0 + 3 * N.MAX_ACT, r] = jm.ravel()
+                else:
+                    block[s0, r] = float(v)
+        state._ov[:, idx] = torch.from_numpy(block).to(dev)
+        state._ov_keys[idx] = torch.from_numpy(kbits.astype(np.int16)).to(dev)
+    for r, i in enumerate(rows):
+        state._host_overlays[int(i)] = inits[r][1]
+
+
+def env_snapshot(state: BatchState, i: int) -> dict:
+    """One env's state and reset context as host copies (engine.py:515-527)."""
+    i = int(i)
+    snap = {
+        "p": state.p[i].double().cpu().numpy().copy(),
+        "q": state.q[i].double().cpu().numpy().copy(),
+        "nu": state.nu[i].double().cpu().numpy().copy(),
+        "act": state.act[i, :state.vehicles[0].action_dim if state._type is None else
+                         state.a_max].double().cpu().numpy().copy(),
+        "current_ned": (state._cur[:, i].double().cpu().numpy().copy()
+                        if state._cur is not None else np.zeros(3)),
+        "steps": int(state.steps[i].item()),
+        "episode": int(state.episodes[i].item()),
+        "diverged": bool(state.diverged[i].item()),
+        "overlay": dict(state.overlays[i]),
+    }
+    return snap
+
+
+def current_in_body(q, current_ned):
+    """Irrotational current as a body-frame 6-vector (engine.py:329-332), torch."""
+    q = torch.as_tensor(q)
+    c = torch.as_tensor(current_ned, dtype=q.dtype, device=q.device)
+    w, u = q[..., :1], -q[..., 1:]
+    uv = torch.linalg.cross(u, c.expand_as(u))
+    lin = c + 2.0 * (w * uv + torch.linalg.cross(u, uv))
+    return torch.cat([lin, torch.zeros_like(lin)], dim=-1)
+
+
+@dataclass
+class ThroughputReport:
+    batch_size: int
+    workers: int
+    n_steps: int
+    elapsed_s: float
+    aggregate_steps_per_s: float
+    per_env_steps_per_s: float
+    diverged_envs: int = 0
+
+
+def throughput_probe(sim: SimConfig, vehicle: VehicleConfig, duration: float = 2.0,
+                     warmup_steps: int = 20, seed: int = 0, *, dtype=torch.float32,
+                     device=None, graph: bool = True) -> ThroughputReport:
+    """Stepping rate with active rotors (engine.py:541-564), device-timed.
+
+    Commands are ``default_rng(seed).uniform(-1, 1, (N, A))`` held fixed, as in
+    the reference; steps are replayed from a captured CUDA graph of 100 launches
+    (``graph=False`` launches from Python) and timed with CUDA events.
+    """
+    st = make_batch(vehicle, sim, master_seed=seed, device=device, dtype=dtype)
+    reset_envs(st, np.ones(sim.batch_size, bool))
+    cmds = torch.from_numpy(np.random.default_rng(seed).uniform(
+        -1.0, 1.0, size=(sim.batch_size, vehicle.action_dim))).to(st.device, dtype)
+    for _ in range(warmup_steps):
+        step_batch(st, cmds)
+    chunk = 100
+    run = (lambda: [step_batch(st, cmds) for _ in range(chunk)])
+    if graph:
+        s = torch.cuda.Stream(st.device)
+        s.wait_stream(torch.cuda.current_stream(st.device))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            step_batch(st, cmds)
+            with torch.cuda.graph(g, stream=s):
+                for _ in range(chunk):
+                    step_batch(st, cmds)
+        torch.cuda.current_stream(st.device).wait_stream(s)
+        run = g.replay
+    torch.cuda.synchronize(st.device)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n_steps, t_wall = 0, time.perf_counter()
+    e0.record()
+    while True:
+        run()
+        n_steps += chunk
+        if time.perf_counter() - t_wall >= duration:
+            break
+    e1.record()
+    torch.cuda.synchronize(st.device)
+    el = e0.elapsed_time(e1) / 1e3
+    return ThroughputReport(batch_size=sim.batch_size, workers=sim.workers, n_steps=n_steps,
+                            elapsed_s=el, aggregate_steps_per_s=sim.batch_size * n_steps / el,
+                            per_env_steps_per_s=n_steps / el,
+                            diverged_envs=int(st.diverged.sum().item()))
+
+
+def substep_terms(state: BatchState, commands) -> dict:
+    """First-substep intermediates (tau, w_hydro, C_RB nu, nudot, next state) without
+    advancing the batch — the quantities engine.py:425-433 forms; for parity checks."""
+    width = state.a_max if state._type is not None else state.vehicle.action_dim
+    cmd = _commands(state, commands, width)
+    out = torch.empty((state.n_envs, 48), dtype=torch.float64, device=state.device)
+    N.check(N.load().uuv_substep_terms(state._ctx, C.byref(state._cstate()), cmd.data_ptr(),
+                                       cmd.stride(0), state.sim.dt / state.sim.substeps,
+                                       out.data_ptr(), state._stream()), EngineError)
+    A = width
+    return {"tau": out[:, 0:6], "hydro": out[:, 6:12], "c_rb": out[:, 12:18],
+            "acc": out[:, 18:24], "nu_new": out[:, 24:30], "p_new": out[:, 30:33],
+            "q_new": out[:, 33:37], "act_new": out[:, 37:37 + A], "ok": out[:, 45] > 0.5}

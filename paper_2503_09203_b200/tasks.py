@@ -159,3 +159,271 @@ def target_yaw_quat(yaw: float) -> np.ndarray:
     cy, sy = np.cos(yaw / 2), np.sin(yaw / 2)
     q = np.array([cy, 0.0, 0.0, sy])
     return q / np.sqrt((q * q).sum())
+
+
+# ================================================================ environments
+
+import ctypes as _C  # noqa: E402
+
+import torch  # noqa: E402
+
+from . import _native as _N  # noqa: E402
+from .engine import (  # noqa: E402
+    BatchState, EngineError, SimConfig, make_batch, spec_sampler,
+)
+from .vehicles import load_vehicle  # noqa: E402
+
+_KIND_CODE = {STATION_KEEPING: _N.TASK_STATION, TRACKING: _N.TASK_TRACKING,
+              DOCKING: _N.TASK_DOCKING}
+_EXTRA = {STATION_KEEPING: 0, TRACKING: 3, DOCKING: 1}
+_METRIC = {STATION_KEEPING: "distance_to_target_m", TRACKING: "mean_deviation_m",
+           DOCKING: "contact_distance_m"}
+
+
+class _Info(dict):
+    """info dict whose ``terminal_observation`` is materialised on first access.
+
+    The fused kernel writes the final observation of an ended episode only for
+    the rows that finished; every other row's final observation IS the returned
+    observation, so the full array is ``where(finished, term_rows, obs)``.
+    """
+
+    def __init__(self, *a, obs=None, term=None, finished=None, **kw):
+        super().__init__(*a, **kw)
+        self._lazy = (obs, term, finished)
+
+    def _materialise(self):
+        if not dict.__contains__(self, "terminal_observation") and self._lazy[0] is not None:
+            obs, term, fin = self._lazy
+            super().__setitem__("terminal_observation", torch.where(fin[:, None], term, obs))
+
+    def __getitem__(self, k):
+        if k == "terminal_observation":
+            self._materialise()
+        return super().__getitem__(k)
+
+    def __contains__(self, k):
+        return k == "terminal_observation" or super().__contains__(k)
+
+    def keys(self):
+        self._materialise()
+        return super().keys()
+
+    def get(self, k, default=None):
+        return self[k] if k in self else default
+
+    def items(self):
+        self._materialise()
+        return super().items()
+
+
+class VecTaskEnv:
+    """Batched task environment over one engine batch (tasks/core.py:217-383)."""
+
+    def __init__(self, task: TaskConfig, sim: SimConfig, dr=None, seed: int = 0, *,
+                 device=None, dtype=torch.float32, env_offset: int = 0):
+        self.task = task
+        self.sim = sim
+        self.vehicle = load_vehicle(task.vehicle)
+        self.seed = int(seed)
+        self._dr = level_spec(task.level, dr)
+        if task.task == TRACKING:
+            horizon = task.episode_length * sim.dt
+            if task.trajectory.duration < horizon:
+                raise TaskError(f"trajectory duration {task.trajectory.duration} s is shorter than "
+                                f"the episode horizon {horizon} s")
+        self.state: BatchState = make_batch(self.vehicle, sim, master_seed=self.seed,
+                                            device=device, dtype=dtype, env_offset=env_offset)
+        self.n_envs = sim.batch_size
+        self.action_dim = self.vehicle.action_dim
+        self.metric_name = _METRIC[task.task]
+        self.extra_dim = _EXTRA[task.task]
+        st = self.state
+        self._sampler = spec_sampler(self._dr, start_box(task))
+        self._sampler_c = self._sampler.pack()
+        if self._sampler.keys():
+            st._ensure_slots(self._sampler.keys())
+        if self._sampler.current_spec:
+            st._enable_current()
+        ld, dev = st._ld, st.device
+        self._prev_u = torch.zeros((self.action_dim, ld), dtype=dtype, device=dev)
+        self._dev_sum = torch.zeros(ld, dtype=dtype, device=dev) if task.task == TRACKING else None
+        self._stats = torch.zeros((_N.load().uuv_stats_blocks(self.n_envs), len(_N.ST_NAMES)),
+                                  dtype=torch.float64, device=dev)
+        self._task_c = self._pack_task()
+
+    # -------------------------------------------------------------- layout
+    @property
+    def obs_dim(self) -> int:
+        return 12 + self.action_dim + self.extra_dim
+
+    def obs_layout(self) -> list:
+        a = self.action_dim
+        out = [("position_error_body", 0, 3), ("attitude_error", 3, 6), ("velocity", 6, 12),
+               ("prev_command", 12, 12 + a)]
+        if self.task.task == TRACKING:
+            out.append(("reference_velocity_body", 12 + a, 15 + a))
+        elif self.task.task == DOCKING:
+            out.append(("height_above_dock", 12 + a, 13 + a))
+        return out
+
+    def spaces(self) -> dict:
+        return {"task": self.task.task, "vehicle": self.vehicle.name, "level": self.task.level,
+                "n_envs": self.n_envs, "obs_dim": self.obs_dim, "action_dim": self.action_dim,
+                "dt": self.sim.dt, "episode_length": self.task.episode_length,
+                "metric": self.metric_name, "obs_layout": [list(s) for s in self.obs_layout()]}
+
+    def reward_bound(self) -> float:
+        w = self.task.weights
+        d = 2.0 * np.sqrt(3.0) * self.task.bounds
+        shaped = (w.w_p * d + w.w_a * np.pi + w.w_v * w.speed_cap
+                  + w.w_u * 2.0 * np.sqrt(self.action_dim) + w.w_b)
+        terminal = abs(w.dock_bonus) + w.w_dock_dist * self.task.dock.radius \
+            + w.w_impact * w.speed_cap + w.w_level * np.pi
+        return max(shaped + terminal, self.task.fail_penalty)
+
+    @property
+    def prev_u(self):
+        return self._prev_u[:, :self.n_envs].t()
+
+    # -------------------------------------------------------------- packing
+    def _pack_task(self) -> _N.Task:
+        t, w = self.task, self.task.weights
+        c = _N.Task()
+        c.kind = _KIND_CODE[t.task]
+        c.episode_length = t.episode_length
+        c.obs_dim = self.obs_dim
+        c.bounds, c.nu_max, c.fail_penalty = t.bounds, t.nu_max, t.fail_penalty
+        for name in ("w_p", "w_a", "w_v", "w_u", "w_b", "r_tol", "speed_cap", "dock_bonus",
+                     "w_dock_dist", "w_impact", "w_level"):
+            setattr(c, name, getattr(w, name))
+        if t.task == STATION_KEEPING:
+            tq = target_yaw_quat(t.target_yaw)
+            tp = np.asarray(t.target_position, float)
+        else:
+            tq = np.array([1.0, 0.0, 0.0, 0.0])
+            tp = np.zeros(3)
+        for k in range(3):
+            c.target_p[k] = tp[k]
+            c.dock_centre[k] = t.dock.centre[k]
+        for k in range(4):
+            c.target_q[k] = tq[k]
+        c.success_tol = t.success_tol
+        c.dock_radius = t.dock.radius
+        tr = t.trajectory
+        c.traj_kind = _N.TRAJ_HELIX if tr.kind == HELIX else _N.TRAJ_LISSAJOUS
+        c.traj_radius, c.traj_rate, c.traj_climb = tr.radius, tr.angular_rate, tr.climb_rate
+        c.traj_z0, c.traj_phase = tr.z0, tr.phase
+        for k in range(3):
+            c.traj_amp[k], c.traj_rates[k] = tr.amplitude[k], tr.rates[k]
+        return c
+
+    def _io(self, obs, term=None, rout=None, fout=None, stats=True) -> _N.TaskIO:
+        io = _N.TaskIO()
+        io.prev_u = self._prev_u.data_ptr()
+        io.dev_sum = self._dev_sum.data_ptr() if self._dev_sum is not None else None
+        io.obs = obs.data_ptr()
+        io.obs_ld = obs.stride(0)
+        io.term_obs = term.data_ptr() if term is not None else None
+        io.real_out = rout.data_ptr() if rout is not None else None
+        io.flag_out = fout.data_ptr() if fout is not None else None
+        io.stats = self._stats.data_ptr() if stats else None
+        return io
+
+    def _new_obs(self):
+        return torch.empty((self.n_envs, self.obs_dim), dtype=self.state.dtype,
+                           device=self.state.device)
+
+    # -------------------------------------------------------------- episode start
+    def reset(self, mask=None):
+        """Reset masked rows (default all) and return the observation of every row."""
+        st = self.state
+        if mask is None:
+            m = None
+        else:
+            if torch.is_tensor(mask):
+                m = mask.to(st.device, torch.bool)
+            else:
+                m = torch.from_numpy(np.asarray(mask, dtype=bool)).to(st.device)
+            if tuple(m.shape) != (self.n_envs,):
+                raise TaskError(f"mask: expected shape {(self.n_envs,)}, got {tuple(m.shape)}")
+            m = m.to(torch.uint8).contiguous()
+        obs = self._new_obs()
+        lib = _N.load()
+        _N.check(lib.uuv_task_reset(st._ctx, _C.byref(st._cstate()), _C.byref(self._task_c),
+                                    _C.byref(self._sampler_c), self.seed & ((1 << 64) - 1),
+                                    m.data_ptr() if m is not None else None, self.sim.dt,
+                                    _C.byref(self._io(obs, stats=False)), st._stream()),
+                 TaskError)
+        return obs
+
+    def observe(self):
+        st = self.state
+        obs = self._new_obs()
+        _N.check(_N.load().uuv_observe(st._ctx, _C.byref(st._cstate()), _C.byref(self._task_c),
+                                       self.sim.dt, _C.byref(self._io(obs, stats=False)),
+                                       st._stream()), TaskError)
+        return obs
+
+    # -------------------------------------------------------------- stepping
+    def step(self, commands):
+        """One fused launch: physics, reward/termination/info, auto-reset, next obs."""
+        st = self.state
+        n, a = self.n_envs, self.action_dim
+        if torch.is_tensor(commands):
+            u = commands
+            if tuple(u.shape) != (n, a):
+                raise TaskError(f"commands: expected shape {(n, a)}, got {tuple(u.shape)}")
+            u = u.to(st.device, st.dtype)
+        else:
+            arr = np.asarray(commands, dtype=float)
+            if arr.shape != (n, a):
+                raise TaskError(f"commands: expected shape {(n, a)}, got {arr.shape}")
+            u = torch.from_numpy(arr).to(st.device, st.dtype)
+        if u.stride(1) != 1:
+            u = u.contiguous()
+        dev, dt = st.device, st.dtype
+        obs = self._new_obs()
+        term = self._new_obs()
+        rout = torch.empty((len(_N.TR_NAMES), st._ld), dtype=dt, device=dev)
+        fout = torch.empty((len(_N.TF_NAMES), st._ld), dtype=torch.uint8, device=dev)
+        _N.check(_N.load().uuv_task_step(
+            st._ctx, _C.byref(st._cstate()), _C.byref(self._task_c), _C.byref(self._sampler_c),
+            self.seed & ((1 << 64) - 1), u.data_ptr(), u.stride(0), self.sim.substeps,
+            self.sim.dt, _C.byref(self._io(obs, term, rout, fout)), st._stream()), TaskError)
+        R = {k: rout[i, :n] for i, k in enumerate(_N.TR_NAMES)}
+        F = {k: fout[i, :n].view(torch.bool) for i, k in enumerate(_N.TF_NAMES)}
+        info = _Info(obs=obs, term=term, finished=F["finished"])
+        info.update({"position_error": R["position_error"], "attitude_error": R["attitude_error"],
+                     "finished": F["finished"], "failure": F["failure"],
+                     "diverged": F["diverged"], "time": R["time"], "success": F["success"],
+                     "metric": R["metric"]})
+        if self.task.task == DOCKING:
+            info.update({"contact": F["contact"], "contact_distance": R["contact_distance"],
+                         "contact_speed": R["contact_speed"],
+                         "contact_attitude": R["contact_attitude"]})
+        return obs, R["reward"], F["terminated"], F["truncated"], info
+
+    # -------------------------------------------------------------- rollout statistics
+    def rollout_stats(self, reset: bool = True, group=None) -> dict:
+        """Sums since the last call: reward, finished, success, failure, truncated,
+        metric over finished rows, diverged, frames — reduced on device in a fixed
+        order, then all-reduced over ``group`` (NCCL) when torch.distributed is up."""
+        out = torch.empty(len(_N.ST_NAMES), dtype=torch.float64, device=self.state.device)
+        _N.check(_N.load().uuv_rollout_stats(self._stats.data_ptr(), self._stats.shape[0],
+                                             out.data_ptr(), 1 if reset else 0,
+                                             self.state._stream()), TaskError)
+        from .distributed import allreduce_sum
+
+        out = allreduce_sum(out, group)
+        return dict(zip(_N.ST_NAMES, out.tolist()))
+
+
+StationKeepingEnv = TrackingEnv = DockingEnv = VecTaskEnv
+
+
+def make_env(task: TaskConfig, sim: SimConfig, dr=None, seed: int = 0, **kw) -> VecTaskEnv:
+    """Build the vectorised environment for a task/vehicle/level (tasks/core.py:533-538)."""
+    if task.task not in TASK_KINDS:
+        raise TaskError(f"unknown task '{task.task}', expected one of {TASK_KINDS}")
+    return VecTaskEnv(task, sim, dr=dr, seed=seed, **kw)
