@@ -6,7 +6,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude --cudart 
 PKG := paper_2503_09203_b200
 LIB := $(PKG)/libuuvb200.so
 SRC := $(PKG)/csrc/uuv_b200.cu
-HDR := include/uuv_b200.h $(PKG)/csrc/uuv_device.cuh $(PKG)/csrc/uuv_task.cuh
+HDR := include/uuv_b200.h $(wildcard $(PKG)/csrc/*.cuh)
 
 all: $(LIB)
 

@@ -267,11 +267,11 @@ def run_b200(args, rank, world, local_rank):
     host_out = torch.empty((13, n), dtype=torch.float32).pin_memory()
     cur = torch.cuda.current_stream(dev)
 
+    pose_rows = st._soa[:13, :n]  # p, q, nu: one [13][N] span of the SoA block
+
     def e2e_step(t):
         E.step_batch(st, host_cmds[t].to(dev, non_blocking=True))
-        host_out[0:3].copy_(st._p[:, :n], non_blocking=True)
-        host_out[3:7].copy_(st._q[:, :n], non_blocking=True)
-        host_out[7:13].copy_(st._nu[:, :n], non_blocking=True)
+        host_out.copy_(pose_rows, non_blocking=True)
         cur.synchronize()
 
     for t in range(min(args.warmup, k_total)):

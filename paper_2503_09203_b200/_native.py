@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libuuvb200.so")
+LIB_PATH = os.environ.get("UUV_B200_LIB") or os.path.join(_HERE, "libuuvb200.so")
 
 MAX_ACT = 8
 MAX_TYPES = 6

@@ -12,6 +12,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -22,6 +23,17 @@ using namespace uuv;
 namespace {
 
 constexpr int kBlock = 128;
+// Minimum resident CTAs per SM requested from ptxas (register cap = 65536 /
+// (kBlock * minB)); tuned on B200 with scripts/sweep.py.
+#ifndef UUV_MINB_F32
+#define UUV_MINB_F32 4
+#endif
+#ifndef UUV_MINB_F64
+#define UUV_MINB_F64 2
+#endif
+template <typename R> struct MinB;
+template <> struct MinB<float> { static constexpr int value = UUV_MINB_F32; };
+template <> struct MinB<double> { static constexpr int value = UUV_MINB_F64; };
 constexpr int kObsMax = 12 + UUV_MAX_ACT + 3;
 
 thread_local std::string g_err;
@@ -108,8 +120,8 @@ void build_hull(const uuv_hull& src, Hull<R>& dst) {
   for (int c = 0; c < 3; ++c) { e.r_g[c] = d.r_g[c]; e.r_b[c] = d.r_b[c]; }
   for (int k = 0; k < 9; ++k) e.I[k] = d.inertia[k];
   double M[21], L[15], Di[6];
-  mass_matrix(d, e, M);
-  ldl6<double>(M, L, Di);
+  mass_matrix_d(d, e, M);
+  ldl6_factor<double>(M, L, Di, Rcp<double>());
   for (int k = 0; k < 15; ++k) h.L[k] = (R)L[k];
   for (int k = 0; k < 6; ++k) h.dinv[k] = (R)Di[k];
   h.mass = (R)e.mass; h.W = (R)e.W; h.B = (R)e.B;
@@ -168,7 +180,48 @@ template <typename R, int NT> struct StepArgs {
   int64_t cmd_ld;
   int32_t K;
   R dt;
+  int32_t early_trigger;  // single-wave grid: let the next step's CTAs launch now
 };
+
+// Programmatic dependent launch (PDL).  Step kernels are launched with
+// programmatic stream serialisation, so kernel k+1 of a rollout is scheduled
+// while kernel k drains; griddepcontrol.wait then blocks until kernel k has
+// completed and its writes are visible.  Nothing reads global memory before
+// the wait.  A single-wave grid also triggers its dependents at entry.
+UUV_D void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+UUV_D void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+template <typename Kernel, typename Args>
+cudaError_t launch_pdl(Kernel k, unsigned grid, cudaStream_t s, const Args& a) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kBlock);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, a);
+}
+
+// Largest grid that is resident in one wave (CTAs per SM from the occupancy API).
+template <typename Kernel>
+int64_t one_wave_ctas(Kernel k) {
+  static thread_local std::map<std::pair<int, const void*>, int64_t> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_pair(dev, (const void*)k);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int sms = 0, per_sm = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kBlock, 0);
+  const int64_t v = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+  cache[key] = v;
+  return v;
+}
 
 // Load env i's kinematic state (SoA, coalesced).
 template <typename R>
@@ -197,7 +250,7 @@ UUV_D void store_state(const StateView<R>& sv, int64_t i, int A, R px, R py, R p
 }
 
 // Physics of one control step for env i; returns the post-step diverged flag.
-template <typename R, bool DR>
+template <typename R, bool DR, int AC>
 UUV_D bool physics(const Hull<R>& H, const StateView<R>& sv, int64_t i, int K, R dt, const R* u,
                    R& px, R& py, R& pz, Q4<R>& q, R* nu, R* act) {
   Sub<R> s;
@@ -205,7 +258,7 @@ UUV_D bool physics(const Hull<R>& H, const StateView<R>& sv, int64_t i, int K, R
   if (DR) {
     EnvD e;
     derive_env(H.d, sv.ov, sv.ld, i, sv.slot, e);
-    sub_from_env<R>(H.d, e, dt, s);
+    sub_from_env<R>(H.r, e, s);
     if (sv.slot[UUV_OV_JITTER] >= 0) jit = sv.ov + sv.slot[UUV_OV_JITTER] * sv.ld + i;
   }
   const bool has_cur = sv.cur != nullptr;
@@ -213,7 +266,7 @@ UUV_D bool physics(const Hull<R>& H, const StateView<R>& sv, int64_t i, int K, R
   if (has_cur) cur = V3<R>{sv.cur[i], sv.cur[sv.ld + i], sv.cur[2 * sv.ld + i]};
   bool ok = true;
   for (int k = 0; k < K; ++k) {
-    if (!substep<R, DR, false>(H.r, s, jit, sv.ld, px, py, pz, q, nu, act, u, has_cur, cur, dt,
+    if (!substep<R, DR, false, AC>(H.r, s, jit, sv.ld, px, py, pz, q, nu, act, u, has_cur, cur, dt,
                                nullptr)) {
       ok = false;
       break;
@@ -222,8 +275,10 @@ UUV_D bool physics(const Hull<R>& H, const StateView<R>& sv, int64_t i, int K, R
   return !ok;
 }
 
-template <typename R, int NT, bool DR>
-__global__ void __launch_bounds__(kBlock) k_step(const __grid_constant__ StepArgs<R, NT> a) {
+template <typename R, int NT, bool DR, int AC>
+__global__ void __launch_bounds__(kBlock, MinB<R>::value) k_step(const __grid_constant__ StepArgs<R, NT> a) {
+  if (a.early_trigger) pdl_trigger();
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
   const StateView<R>& sv = a.sv;
   if (i >= sv.n) return;
@@ -242,7 +297,7 @@ __global__ void __launch_bounds__(kBlock) k_step(const __grid_constant__ StepArg
   R px, py, pz, nu[6], act[UUV_MAX_ACT];
   Q4<R> q;
   load_state(sv, i, A, px, py, pz, q, nu, act);
-  const bool div = physics<R, DR>(H, sv, i, a.K, a.dt, u, px, py, pz, q, nu, act);
+  const bool div = physics<R, DR, AC>(H, sv, i, a.K, a.dt, u, px, py, pz, q, nu, act);
   store_state(sv, i, A, px, py, pz, q, nu, act);
   sv.diverged[i] = div ? 1 : 0;
   sv.steps[i] = steps + 1;
@@ -283,8 +338,8 @@ UUV_D void flush_obs(const R* s_obs, R* obs, int64_t obs_ld, int obs_dim, int64_
   }
 }
 
-template <typename R, bool DR>
-__global__ void __launch_bounds__(kBlock) k_task_step(const __grid_constant__ TaskArgs<R> a) {
+template <typename R, bool DR, int AC>
+__global__ void __launch_bounds__(kBlock, MinB<R>::value) k_task_step(const __grid_constant__ TaskArgs<R> a) {
   __shared__ R s_obs[kBlock * kObsMax];
   __shared__ double s_red[kBlock / 32][UUV_ST_COUNT];
   const int64_t row0 = (int64_t)blockIdx.x * kBlock;
@@ -317,7 +372,7 @@ __global__ void __launch_bounds__(kBlock) k_task_step(const __grid_constant__ Ta
     R px, py, pz, nu[6], act[UUV_MAX_ACT];
     Q4<R> q;
     load_state(sv, i, A, px, py, pz, q, nu, act);
-    if (!div) div = physics<R, DR>(H, sv, i, a.K, a.dt_sub, u, px, py, pz, q, nu, act);
+    if (!div) div = physics<R, DR, AC>(H, sv, i, a.K, a.dt_sub, u, px, py, pz, q, nu, act);
     steps += 1;
     R dev = a.dev_sum != nullptr ? a.dev_sum[i] : R(0);
     TaskOut<R> o;
@@ -503,12 +558,12 @@ __global__ void __launch_bounds__(kBlock) k_derive(const __grid_constant__ Deriv
   }
   if (a.minv != nullptr) {  // M^-1 columns by LDL^T solves of unit vectors
     double M[21], L[15], Di[6];
-    mass_matrix(H.d, e, M);
-    ldl6<double>(M, L, Di);
+    mass_matrix_d(H.d, e, M);
+    ldl6_factor<double>(M, L, Di, Rcp<double>());
     for (int c = 0; c < 6; ++c) {
       double b[6] = {0, 0, 0, 0, 0, 0}, x[6];
       b[c] = 1.0;
-      ldl6_solve<double>(L, Di, b, x);
+      ldl6_apply<double>(L, Di, b, x);
       for (int r = 0; r < 6; ++r) a.minv[i * 36 + 6 * r + c] = x[r];
     }
   }
@@ -538,7 +593,7 @@ template <typename R, int NT> struct TermsArgs {
   double* out;
 };
 
-template <typename R, int NT, bool DR>
+template <typename R, int NT, bool DR, int AC>
 __global__ void __launch_bounds__(kBlock) k_terms(const __grid_constant__ TermsArgs<R, NT> a) {
   const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
   const StateView<R>& sv = a.sv;
@@ -556,14 +611,14 @@ __global__ void __launch_bounds__(kBlock) k_terms(const __grid_constant__ TermsA
   if (DR) {
     EnvD e;
     derive_env(H.d, sv.ov, sv.ld, i, sv.slot, e);
-    sub_from_env<R>(H.d, e, a.dt, s);
+    sub_from_env<R>(H.r, e, s);
     if (sv.slot[UUV_OV_JITTER] >= 0) jit = sv.ov + sv.slot[UUV_OV_JITTER] * sv.ld + i;
   }
   const bool has_cur = sv.cur != nullptr;
   V3<R> cur{R(0), R(0), R(0)};
   if (has_cur) cur = V3<R>{sv.cur[i], sv.cur[sv.ld + i], sv.cur[2 * sv.ld + i]};
   Terms<R> tm;
-  const bool ok = substep<R, DR, true>(H.r, s, jit, sv.ld, px, py, pz, q, nu, act, u, has_cur, cur,
+  const bool ok = substep<R, DR, true, AC>(H.r, s, jit, sv.ld, px, py, pz, q, nu, act, u, has_cur, cur,
                                        a.dt, &tm);
   double* o = a.out + i * 48;
   for (int k = 0; k < 6; ++k) {
@@ -602,6 +657,16 @@ uuv_status check_state(const uuv_ctx* ctx, const uuv_state* st) {
   return UUV_OK;
 }
 
+// Actuator class of a single-vehicle batch (see substep): A first-order thrusters.
+int act_class(const uuv_ctx* ctx) {
+  if (ctx->hulls.size() != 1) return 0;
+  const uuv_hull& h = ctx->hulls[0];
+  if (h.n_act != 6 && h.n_act != 8) return 0;
+  for (int j = 0; j < h.n_act; ++j)
+    if (h.kind[j] == UUV_RUDDER || h.model[j] != UUV_FIRST_ORDER) return 0;
+  return h.n_act;
+}
+
 template <typename R> const std::vector<Hull<R>>& hulls_of(const uuv_ctx* c);
 template <> const std::vector<Hull<float>>& hulls_of<float>(const uuv_ctx* c) { return c->hf; }
 template <> const std::vector<Hull<double>>& hulls_of<double>(const uuv_ctx* c) { return c->hd; }
@@ -615,7 +680,7 @@ void fill_hulls(const uuv_ctx* ctx, Hull<R>* dst, double dt_sub) {
   }
 }
 
-template <typename R, int NT, bool DR>
+template <typename R, int NT, bool DR, int AC>
 uuv_status launch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd, int64_t cmd_ld,
                        int32_t K, double dt, cudaStream_t s) {
   StepArgs<R, NT> a;
@@ -626,7 +691,10 @@ uuv_status launch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd,
   a.cmd_ld = cmd_ld;
   a.K = K;
   a.dt = (R)dt_sub;
-  k_step<R, NT, DR><<<(unsigned)grid_for(st->n_envs), kBlock, 0, s>>>(a);
+  const int64_t grid = grid_for(st->n_envs);
+  a.early_trigger = grid <= one_wave_ctas(k_step<R, NT, DR, AC>) ? 1 : 0;
+  cudaError_t e = launch_pdl(k_step<R, NT, DR, AC>, (unsigned)grid, s, a);
+  if (e != cudaSuccess) return fail(UUV_ERR_CUDA, "uuv_step: %s", cudaGetErrorString(e));
   return check_launch("uuv_step");
 }
 
@@ -634,11 +702,21 @@ template <typename R>
 uuv_status dispatch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd, int64_t cmd_ld,
                          int32_t K, double dt, cudaStream_t s) {
   const bool dr = st->overlay != nullptr;
-  if (ctx->hulls.size() == 1)
-    return dr ? launch_step<R, 1, true>(ctx, st, cmd, cmd_ld, K, dt, s)
-              : launch_step<R, 1, false>(ctx, st, cmd, cmd_ld, K, dt, s);
-  return dr ? launch_step<R, UUV_MAX_TYPES, true>(ctx, st, cmd, cmd_ld, K, dt, s)
-            : launch_step<R, UUV_MAX_TYPES, false>(ctx, st, cmd, cmd_ld, K, dt, s);
+  if (ctx->hulls.size() == 1) {
+    switch (act_class(ctx)) {
+      case 6:
+        return dr ? launch_step<R, 1, true, 6>(ctx, st, cmd, cmd_ld, K, dt, s)
+                  : launch_step<R, 1, false, 6>(ctx, st, cmd, cmd_ld, K, dt, s);
+      case 8:
+        return dr ? launch_step<R, 1, true, 8>(ctx, st, cmd, cmd_ld, K, dt, s)
+                  : launch_step<R, 1, false, 8>(ctx, st, cmd, cmd_ld, K, dt, s);
+      default:
+        return dr ? launch_step<R, 1, true, 0>(ctx, st, cmd, cmd_ld, K, dt, s)
+                  : launch_step<R, 1, false, 0>(ctx, st, cmd, cmd_ld, K, dt, s);
+    }
+  }
+  return dr ? launch_step<R, UUV_MAX_TYPES, true, 0>(ctx, st, cmd, cmd_ld, K, dt, s)
+            : launch_step<R, UUV_MAX_TYPES, false, 0>(ctx, st, cmd, cmd_ld, K, dt, s);
 }
 
 uuv_status check_sampler(const uuv_sampler* smp) {
@@ -683,6 +761,20 @@ void fill_task_args(const uuv_ctx* ctx, const uuv_state* st, const uuv_task* tas
   a.cmd_ld = 0;
 }
 
+template <typename R>
+void launch_task_step(bool dr, int ac, unsigned g, cudaStream_t cs, const TaskArgs<R>& a) {
+  if (ac == 6) {
+    if (dr) k_task_step<R, true, 6><<<g, kBlock, 0, cs>>>(a);
+    else k_task_step<R, false, 6><<<g, kBlock, 0, cs>>>(a);
+  } else if (ac == 8) {
+    if (dr) k_task_step<R, true, 8><<<g, kBlock, 0, cs>>>(a);
+    else k_task_step<R, false, 8><<<g, kBlock, 0, cs>>>(a);
+  } else {
+    if (dr) k_task_step<R, true, 0><<<g, kBlock, 0, cs>>>(a);
+    else k_task_step<R, false, 0><<<g, kBlock, 0, cs>>>(a);
+  }
+}
+
 uuv_status check_task(const uuv_ctx* ctx, const uuv_state* st, const uuv_task* task,
                       const uuv_task_io* io) {
   if (task == nullptr || io == nullptr) return fail(UUV_ERR_ARG, "null task or io");
@@ -712,7 +804,7 @@ static uuv_status derive_launch(const uuv_ctx* ctx, const uuv_state* st, double*
   return check_launch("uuv_derive_params");
 }
 
-template <typename R, int NT, bool DR>
+template <typename R, int NT, bool DR, int AC>
 static uuv_status terms_launch(const uuv_ctx* ctx, const uuv_state* st, const void* cmd,
                                int64_t cmd_ld, double dt_sub, double* out, cudaStream_t cs) {
   TermsArgs<R, NT> a;
@@ -722,7 +814,7 @@ static uuv_status terms_launch(const uuv_ctx* ctx, const uuv_state* st, const vo
   a.cmd_ld = cmd_ld;
   a.dt = (R)dt_sub;
   a.out = out;
-  k_terms<R, NT, DR><<<(unsigned)grid_for(st->n_envs), kBlock, 0, cs>>>(a);
+  k_terms<R, NT, DR, AC><<<(unsigned)grid_for(st->n_envs), kBlock, 0, cs>>>(a);
   return check_launch("uuv_substep_terms");
 }
 
@@ -731,10 +823,19 @@ static uuv_status terms_dispatch(const uuv_ctx* ctx, const uuv_state* st, const 
                                  int64_t cmd_ld, double dt_sub, double* out, cudaStream_t cs) {
   const bool dr = st->overlay != nullptr, multi = ctx->hulls.size() > 1;
   if (multi)
-    return dr ? terms_launch<R, UUV_MAX_TYPES, true>(ctx, st, cmd, cmd_ld, dt_sub, out, cs)
-              : terms_launch<R, UUV_MAX_TYPES, false>(ctx, st, cmd, cmd_ld, dt_sub, out, cs);
-  return dr ? terms_launch<R, 1, true>(ctx, st, cmd, cmd_ld, dt_sub, out, cs)
-            : terms_launch<R, 1, false>(ctx, st, cmd, cmd_ld, dt_sub, out, cs);
+    return dr ? terms_launch<R, UUV_MAX_TYPES, true, 0>(ctx, st, cmd, cmd_ld, dt_sub, out, cs)
+              : terms_launch<R, UUV_MAX_TYPES, false, 0>(ctx, st, cmd, cmd_ld, dt_sub, out, cs);
+  switch (act_class(ctx)) {
+    case 6:
+      return dr ? terms_launch<R, 1, true, 6>(ctx, st, cmd, cmd_ld, dt_sub, out, cs)
+                : terms_launch<R, 1, false, 6>(ctx, st, cmd, cmd_ld, dt_sub, out, cs);
+    case 8:
+      return dr ? terms_launch<R, 1, true, 8>(ctx, st, cmd, cmd_ld, dt_sub, out, cs)
+                : terms_launch<R, 1, false, 8>(ctx, st, cmd, cmd_ld, dt_sub, out, cs);
+    default:
+      return dr ? terms_launch<R, 1, true, 0>(ctx, st, cmd, cmd_ld, dt_sub, out, cs)
+                : terms_launch<R, 1, false, 0>(ctx, st, cmd, cmd_ld, dt_sub, out, cs);
+  }
 }
 
 static uuv_status task_reset_impl(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task,
@@ -883,15 +984,13 @@ uuv_status uuv_task_step(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task
     fill_task_args<float>(ctx, st, task, sampler, seed, dt, substeps, io, a);
     a.cmd = (const float*)commands;
     a.cmd_ld = cmd_ld;
-    if (dr) k_task_step<float, true><<<g, kBlock, 0, cs>>>(a);
-    else k_task_step<float, false><<<g, kBlock, 0, cs>>>(a);
+    launch_task_step<float>(dr, act_class(ctx), g, cs, a);
   } else {
     TaskArgs<double> a;
     fill_task_args<double>(ctx, st, task, sampler, seed, dt, substeps, io, a);
     a.cmd = (const double*)commands;
     a.cmd_ld = cmd_ld;
-    if (dr) k_task_step<double, true><<<g, kBlock, 0, cs>>>(a);
-    else k_task_step<double, false><<<g, kBlock, 0, cs>>>(a);
+    launch_task_step<double>(dr, act_class(ctx), g, cs, a);
   }
   return check_launch("uuv_task_step");
 }

@@ -306,12 +306,14 @@ class BatchState:
         self.a_max = max(v.action_dim for v in self.vehicles)
         self._ld = ld = max(_ALIGN, -(-n // _ALIGN) * _ALIGN)
         kw = dict(device=self.device)
-        self._p = torch.zeros((3, ld), dtype=dtype, **kw)
-        self._q = torch.zeros((4, ld), dtype=dtype, **kw)
+        # one SoA block: rows 0-2 p, 3-6 q, 7-12 nu, 13.. act (p/q/nu are one
+        # contiguous [13][ld] span, so a host snapshot of the pose is one copy)
+        self._soa = torch.zeros((13 + self.a_max, ld), dtype=dtype, **kw)
+        self._p, self._q = self._soa[0:3], self._soa[3:7]
+        self._nu, self._act = self._soa[7:13], self._soa[13:]
         self._q[0] = 1.0
-        self._nu = torch.zeros((6, ld), dtype=dtype, **kw)
-        self._act = torch.zeros((self.a_max, ld), dtype=dtype, **kw)
         self._cur = None
+        self._cs = None
         self.steps = torch.zeros(ld, dtype=torch.int32, **kw)[:n]
         self.episodes = torch.full((ld,), -1, dtype=torch.int32, **kw)[:n]
         self.diverged = torch.zeros(ld, dtype=torch.bool, **kw)[:n]
@@ -412,6 +414,7 @@ class BatchState:
     def _enable_current(self):
         if self._cur is None:
             self._cur = torch.zeros((3, self._ld), dtype=self.dtype, device=self.device)
+            self._cs = None
 
     def _ensure_slots(self, keys):
         keys = [k for k in keys if k in N.OV_INDEX]
@@ -432,10 +435,16 @@ class BatchState:
             else:
                 ov[s0:s0 + w] = N.OV_IDENTITY[k]
         self._ov, self._slots = ov, slots
+        self._cs = None
         if self._ov_keys is None:
             self._ov_keys = torch.zeros(self._ld, dtype=torch.int16, device=self.device)
 
     def _cstate(self) -> N.State:
+        if self._cs is None:
+            self._cs = self._build_cstate()
+        return self._cs
+
+    def _build_cstate(self) -> N.State:
         s = N.State()
         s.dtype = N.F32 if self.dtype == torch.float32 else N.F64
         s.a_max = self.a_max
@@ -473,6 +482,7 @@ class BatchState:
         if self._type is None:
             self._type = torch.zeros(self._ld, dtype=torch.uint8, device=self.device)
         self._type[i] = t
+        self._cs = None
 
 
 class _Layout:

@@ -1,0 +1,115 @@
+"""Throughput sweep of the step kernel over batch size and configuration.
+
+Prints one JSON line per case: device-timed (CUDA events around a CUDA-graph
+replay of `steps` launches) frames/s, us/launch, algorithmic GB/s and the
+fraction of the measured HBM copy bandwidth.  Used for profiles/, not the
+driver's bench line.
+
+    python scripts/sweep.py [--cases cfg2,cfg3,bluerov_1m] [--steps 200]
+"""
+
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2503_09203_b200 import engine as E  # noqa: E402
+from paper_2503_09203_b200.randomization import DRParameter, Uniform, preset  # noqa: E402
+from paper_2503_09203_b200.vehicles import BUILTIN_VEHICLES, load_vehicle  # noqa: E402
+
+PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
+    if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+
+
+def frame_bytes(a, n_dr, cur, dtype_bytes=4, mixed=False):
+    b = dtype_bytes * (2 * (13 + a) + a) + 2 + 8 + 8 * n_dr
+    if cur:
+        b += 3 * dtype_bytes
+    if mixed:
+        b += 1
+    return b
+
+
+def make_case(name, n):
+    dev = torch.device("cuda", 0)
+    if name == "cfg3":  # five vehicles mixed, no DR
+        vehs = [load_vehicle(v) for v in BUILTIN_VEHICLES]
+        counts = [n // 5 + (1 if i < n % 5 else 0) for i in range(5)]
+        st = E.make_fleet_batch(vehs, counts, E.SimConfig(batch_size=n), device=dev)
+        E.reset_envs(st, torch.ones(n, dtype=torch.bool, device=dev))
+        a_mean = sum(v.action_dim * c for v, c in zip(vehs, counts)) / n
+        width = st.a_max
+        bpf = frame_bytes(a_mean, 0, False, mixed=True)
+    elif name.startswith("cfg2") or name.startswith("bluerov"):
+        veh = load_vehicle("bluerov")
+        substeps = 8 if name.endswith("k8") else 1
+        st = E.make_batch(veh, E.SimConfig(batch_size=n, substeps=substeps), device=dev)
+        keys = ("damping*", "mass*", "thrust_coeff*", "volume*") if name.startswith("cfg2") else ()
+        spec = {k: DRParameter(k, Uniform(0.8, 1.2)) for k in keys}
+        E.reset_envs(st, torch.ones(n, dtype=torch.bool, device=dev),
+                     E.spec_sampler(spec or None))
+        width = 6
+        bpf = frame_bytes(6, len(keys), False)
+    elif name == "cfg5_physics":  # bluerov_heavy + train preset (7 ratios) + current
+        veh = load_vehicle("bluerov_heavy")
+        st = E.make_batch(veh, E.SimConfig(batch_size=n), device=dev)
+        E.reset_envs(st, torch.ones(n, dtype=torch.bool, device=dev),
+                     E.spec_sampler(preset("train")))
+        width = 8
+        bpf = frame_bytes(8, 7, True)
+    else:
+        raise ValueError(name)
+    return st, width, bpf
+
+
+def measure(name, n, steps):
+    st, width, bpf = make_case(name, n)
+    dev = st.device
+    cmds = torch.rand((n, width), device=dev) * 2 - 1
+    s = torch.cuda.Stream(dev)
+    with torch.cuda.stream(s):
+        for _ in range(5):
+            E.step_batch(st, cmds)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(steps):
+                E.step_batch(st, cmds)
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = None
+    for _ in range(3):
+        with torch.cuda.stream(s):
+            e0.record(s)
+            g.replay()
+            e1.record(s)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / 1e3 / steps
+        best = t if best is None else min(best, t)
+    gbs = n * bpf / best / 1e9
+    return {"case": name, "n": n, "us_per_step": best * 1e6, "frames_per_s": n / best,
+            "bytes_per_frame": bpf, "gbs": gbs, "frac_hbm": gbs / PEAK,
+            "diverged": int(st.diverged.sum().item())}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cases", default="cfg2,cfg3,bluerov,cfg5_physics,cfg2_k8")
+    ap.add_argument("--sizes", default="4096,65536,262144,1048576,4194304")
+    ap.add_argument("--steps", type=int, default=100)
+    args = ap.parse_args()
+    for case in args.cases.split(","):
+        for n in (int(x) for x in args.sizes.split(",")):
+            print(json.dumps(measure(case, n, args.steps)), flush=True)
+
+
+if __name__ == "__main__":
+    main()
