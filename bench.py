@@ -9,9 +9,10 @@ commands U(-1, 1).  A step is one control step (one ``uuv_step`` launch).
   CUDA events on the launching stream, barrier + max over ranks.  Each step
   reads a fresh command buffer from a ring larger than L2 (env state stays
   resident, as in an RL loop); L2 is flushed once before the timed region.
-* e2e — the same metric through the public API with HOST buffers: per step a
-  pinned-host -> device copy of the commands, ``step_batch``, a device ->
-  pinned-host copy of the next state (p, q, nu) and a host sync.
+* e2e — the same metric through the public API with HOST buffers:
+  ``step_batch(state, pinned_host_commands, pose_out=pinned_host_pose)`` per
+  step = async H2D of the commands, the step launch, one D2H of the next
+  state's p, q, nu rows and a host sync (the caller reads the result).
 * roofline — the step kernel's algorithmic bytes per launch / average launch
   duration vs the measured HBM copy bandwidth (MEASURED_PEAKS.json).
 * cpu_baseline — the CPU oracle (numpy restatement of the reference) on the
@@ -267,12 +268,9 @@ def run_b200(args, rank, world, local_rank):
     host_out = torch.empty((13, n), dtype=torch.float32).pin_memory()
     cur = torch.cuda.current_stream(dev)
 
-    pose_rows = st._soa[:13, :n]  # p, q, nu: one [13][N] span of the SoA block
-
     def e2e_step(t):
-        E.step_batch(st, host_cmds[t].to(dev, non_blocking=True))
-        host_out.copy_(pose_rows, non_blocking=True)
-        cur.synchronize()
+        # public API, host buffers: pinned commands in, pinned (13, N) pose rows out
+        E.step_batch(st, host_cmds[t], pose_out=host_out)
 
     for t in range(min(args.warmup, k_total)):
         e2e_step(t)

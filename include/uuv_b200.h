@@ -139,7 +139,11 @@ typedef struct {
   uint16_t* overlay_keys;  /* [ld] bit k set: key k present in the row's overlay, or NULL */
   int32_t n_slots;
   int32_t slot[UUV_OV_COUNT];
+  int32_t flags;           /* UUV_STATE_* */
 } uuv_state;
+
+/* uuv_state.flags */
+enum { UUV_STATE_PAYLOAD_AT_ORIGIN = 1 /* every env's payload_position (if any) is 0 */ };
 
 /* One draw of a DR key (randomization.py:48-117): uniform or piecewise. */
 enum { UUV_DIST_UNIFORM = 0, UUV_DIST_PIECEWISE = 1 };
@@ -234,6 +238,14 @@ void uuv_ctx_destroy(uuv_ctx* ctx);
  * clipped to [-1, 1] inside. */
 uuv_status uuv_step(uuv_ctx* ctx, const uuv_state* st, const void* commands, int64_t cmd_ld,
                     int32_t substeps, double dt, void* stream);
+
+/* Host-buffer variant of uuv_step for callers whose commands and results live in
+ * (pinned) host memory: async copy host_cmd (n_envs, cmd_ld) -> dev_cmd, uuv_step,
+ * then, if host_pose != NULL, one async copy of the pose rows p, q, nu into
+ * host_pose as a row-major (13, n_envs) array; sync != 0 waits for the stream. */
+uuv_status uuv_step_host(uuv_ctx* ctx, const uuv_state* st, const void* host_cmd, int64_t cmd_ld,
+                         void* dev_cmd, void* host_pose, int32_t substeps, double dt,
+                         void* stream, int32_t sync);
 
 /* Reset rows with mask[i] != 0 (mask NULL = all rows) from the declarative sampler. */
 uuv_status uuv_reset(uuv_ctx* ctx, const uuv_state* st, const uint8_t* mask,

@@ -40,6 +40,7 @@ START_IDENTITY, START_BOX = 0, 1
 CURRENT_NONE, CURRENT_RANDOM_HEADING, CURRENT_HEADING_DRAW = 0, 1, 2
 TASK_STATION, TASK_TRACKING, TASK_DOCKING = 0, 1, 2
 TRAJ_HELIX, TRAJ_LISSAJOUS = 0, 1
+STATE_PAYLOAD_AT_ORIGIN = 1
 TR_NAMES = ("reward", "position_error", "attitude_error", "metric", "time", "contact_distance",
             "contact_speed", "contact_attitude")
 TF_NAMES = ("terminated", "truncated", "finished", "failure", "success", "diverged", "contact")
@@ -76,7 +77,7 @@ class State(C.Structure):
         ("current_ned", C.c_void_p),
         ("steps", C.c_void_p), ("episodes", C.c_void_p), ("diverged", C.c_void_p),
         ("type_id", C.c_void_p), ("overlay", C.c_void_p), ("overlay_keys", C.c_void_p),
-        ("n_slots", C.c_int32), ("slot", C.c_int32 * OV_COUNT),
+        ("n_slots", C.c_int32), ("slot", C.c_int32 * OV_COUNT), ("flags", C.c_int32),
     ]
 
 
@@ -130,6 +131,8 @@ EXPORTS = {
     "uuv_ctx_destroy": (None, [C.c_void_p]),
     "uuv_step": (C.c_int, [C.c_void_p, C.POINTER(State), C.c_void_p, C.c_int64, C.c_int32,
                            C.c_double, C.c_void_p]),
+    "uuv_step_host": (C.c_int, [C.c_void_p, C.POINTER(State), C.c_void_p, C.c_int64, C.c_void_p,
+                                C.c_void_p, C.c_int32, C.c_double, C.c_void_p, C.c_int32]),
     "uuv_reset": (C.c_int, [C.c_void_p, C.POINTER(State), C.c_void_p, C.POINTER(Sampler),
                             C.c_uint64, C.c_void_p]),
     "uuv_task_step": (C.c_int, [C.c_void_p, C.POINTER(State), C.POINTER(Task), C.POINTER(Sampler),

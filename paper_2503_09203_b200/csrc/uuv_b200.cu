@@ -12,11 +12,14 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
+#include <cstdlib>
 #include <map>
 #include <string>
 #include <vector>
 
 #include "uuv_task.cuh"
+#include "uuv_bulk.cuh"
 
 using namespace uuv;
 
@@ -250,23 +253,23 @@ UUV_D void store_state(const StateView<R>& sv, int64_t i, int A, R px, R py, R p
 }
 
 // Physics of one control step for env i; returns the post-step diverged flag.
-template <typename R, bool DR, int AC>
-UUV_D bool physics(const Hull<R>& H, const StateView<R>& sv, int64_t i, int K, R dt, const R* u,
-                   R& px, R& py, R& pz, Q4<R>& q, R* nu, R* act) {
+// K substeps for one env.  The overlay record is read at (ov, ov_ld, ov_i) — global
+// memory or a shared-memory slab; jitter always comes from the global record.
+template <typename R, bool DR, int AC, bool DM>
+UUV_D bool physics_at(const Hull<R>& H, const StateView<R>& sv, int64_t i, const double* ov,
+                      int64_t ov_ld, int64_t ov_i, bool has_cur, V3<R> cur, int K, R dt,
+                      const R* u, R& px, R& py, R& pz, Q4<R>& q, R* nu, R* act) {
   Sub<R> s;
   const double* jit = nullptr;
   if (DR) {
     EnvD e;
-    derive_env(H.d, sv.ov, sv.ld, i, sv.slot, e);
-    sub_from_env<R>(H.r, e, s);
+    derive_env(H.d, ov, ov_ld, ov_i, sv.slot, e);
+    sub_from_env<R, DM>(H.r, e, s);
     if (sv.slot[UUV_OV_JITTER] >= 0) jit = sv.ov + sv.slot[UUV_OV_JITTER] * sv.ld + i;
   }
-  const bool has_cur = sv.cur != nullptr;
-  V3<R> cur{R(0), R(0), R(0)};
-  if (has_cur) cur = V3<R>{sv.cur[i], sv.cur[sv.ld + i], sv.cur[2 * sv.ld + i]};
   bool ok = true;
   for (int k = 0; k < K; ++k) {
-    if (!substep<R, DR, false, AC>(H.r, s, jit, sv.ld, px, py, pz, q, nu, act, u, has_cur, cur, dt,
+    if (!substep<R, DR, false, AC, DM>(H.r, s, jit, sv.ld, px, py, pz, q, nu, act, u, has_cur, cur, dt,
                                nullptr)) {
       ok = false;
       break;
@@ -275,32 +278,230 @@ UUV_D bool physics(const Hull<R>& H, const StateView<R>& sv, int64_t i, int K, R
   return !ok;
 }
 
-template <typename R, int NT, bool DR, int AC>
+template <typename R, bool DR, int AC, bool DM>
+UUV_D bool physics(const Hull<R>& H, const StateView<R>& sv, int64_t i, int K, R dt, const R* u,
+                   R& px, R& py, R& pz, Q4<R>& q, R* nu, R* act) {
+  const bool has_cur = sv.cur != nullptr;
+  V3<R> cur{R(0), R(0), R(0)};
+  if (has_cur) cur = V3<R>{sv.cur[i], sv.cur[sv.ld + i], sv.cur[2 * sv.ld + i]};
+  return physics_at<R, DR, AC, DM>(H, sv, i, sv.ov, sv.ld, i, has_cur, cur, K, dt, u, px, py, pz,
+                                   q, nu, act);
+}
+
+// ------------------------------------------------------------------ persistent TMA step
+// Per-warp software pipeline: every warp owns 32-env tiles (stride = all warps of
+// the grid) and a double buffer in shared memory.  For each tile, lane r issues
+// the bulk copy (TMA engine, cp.async.bulk) of the tile's slice of SoA row r
+// into the free buffer — state, steps, diverged, type id, DR record, commands —
+// with completion counted in bytes on the warp's mbarrier, while the warp
+// computes the previous tile from the other buffer; results are written back in
+// place and bulk-copied to global memory by the same lanes.  Threads touch only
+// their own shared-memory column (immediate-offset LDS/STS, no per-access
+// address arithmetic) and only __syncwarp is needed, so warps pipeline
+// independently and each keeps its next slab in flight while computing.
+constexpr int kTile = 32;
+constexpr int kWarps = kBlock / 32;
+constexpr int kMaxRows = 64;
+struct RowDesc {
+  const char* g;  // global address of env 0 of this row
+  uint32_t elem;  // bytes per env
+  uint32_t soff;  // byte offset inside a warp buffer
+};
+
+template <typename R, int NT> struct TmaArgs {
+  Hull<R> hull[NT];
+  StateView<R> sv;
+  const R* cmd;
+  int64_t cmd_ld;
+  int32_t K;
+  R dt;
+  int32_t early_trigger;
+  int32_t n_load, n_store;
+  int32_t cmd_row;        // index of the command slab in load[], -1 if loaded per lane
+  uint32_t buf_bytes;
+  uint32_t off_cur, off_steps, off_div, off_type, off_ov, off_cmd;  // 0xffffffff: absent
+  int64_t n_tiles;
+  RowDesc load[kMaxRows];
+  RowDesc store[kMaxRows];
+};
+
+UUV_D uint32_t round16(uint32_t b) { return (b + 15u) & ~15u; }
+
+template <typename R, int NT, bool DR, int AC, bool DM>
+__global__ void __launch_bounds__(kBlock, MinB<R>::value)
+    k_step_tma(const __grid_constant__ TmaArgs<R, NT> a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + 2 * warp;
+  unsigned char* bufs = smem + 128 + (size_t)warp * 2 * a.buf_bytes;
+  const StateView<R>& sv = a.sv;
+  if (a.early_trigger) pdl_trigger();
+  if (lane == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  pdl_wait();  // the previous step's writes are visible from here on
+
+  auto issue_load = [&](int64_t tile, int b) {
+    const int64_t row0 = tile * kTile;
+    const int rows = (int)min((int64_t)kTile, sv.n - row0);
+    const bool tail = rows < kTile;
+    unsigned char* buf = bufs + (size_t)b * a.buf_bytes;
+    uint32_t total = 0;
+    for (int r = 0; r < a.n_load; ++r)
+      if (!(r == a.cmd_row && tail)) total += round16((uint32_t)rows * a.load[r].elem);
+    if (lane == 0) mbar_arrive_expect_tx(&bars[b], total);
+    __syncwarp();
+    for (int r = lane; r < a.n_load; r += 32) {
+      if (r == a.cmd_row && tail) continue;
+      const RowDesc& d = a.load[r];
+      bulk_g2s(buf + d.soff, d.g + row0 * d.elem, round16((uint32_t)rows * d.elem), &bars[b]);
+    }
+  };
+
+  const int64_t stride = (int64_t)gridDim.x * kWarps;
+  int64_t tile = (int64_t)blockIdx.x * kWarps + warp;
+  if (tile < a.n_tiles) issue_load(tile, 0);
+  for (int k = 0; tile < a.n_tiles; ++k, tile += stride) {
+    const int b = k & 1;
+    const int64_t next = tile + stride;
+    if (next < a.n_tiles) {
+      bulk_wait_read_all();  // the other buffer's stores have finished reading it
+      __syncwarp();
+      issue_load(next, 1 - b);
+    }
+    mbar_wait(&bars[b], (uint32_t)((k >> 1) & 1));
+    unsigned char* buf = bufs + (size_t)b * a.buf_bytes;
+    const int64_t row0 = tile * kTile;
+    const int rows = (int)min((int64_t)kTile, sv.n - row0);
+    const unsigned t = lane;
+    if ((int)t < rows) {
+      const int64_t i = row0 + t;
+      R* S = reinterpret_cast<R*>(buf);  // state rows p q nu act, kTile each
+      int32_t* steps = reinterpret_cast<int32_t*>(buf + a.off_steps);
+      uint8_t* div = buf + a.off_div;
+      const int ty = NT > 1 ? (int)buf[a.off_type + t] : 0;
+      const Hull<R>& H = a.hull[ty];
+      const int A = AC > 0 ? AC : H.r.n_act;
+      constexpr int NA = AC > 0 ? AC : UUV_MAX_ACT;
+      if (!div[t]) {
+        R u[UUV_MAX_ACT];
+        const R* c = (a.cmd_row >= 0 && rows == kTile)
+                         ? reinterpret_cast<const R*>(buf + a.off_cmd) + t * a.cmd_ld
+                         : a.cmd + i * a.cmd_ld;
+#pragma unroll
+        for (int j = 0; j < UUV_MAX_ACT; ++j)
+          u[j] = (j < NA && j < A) ? clip_<R>(c[j], R(-1), R(1)) : R(0);
+        R px = S[t], py = S[kTile + t], pz = S[2 * kTile + t];
+        Q4<R> q{S[3 * kTile + t], S[4 * kTile + t], S[5 * kTile + t], S[6 * kTile + t]};
+        R nu[6], act[UUV_MAX_ACT];
+#pragma unroll
+        for (int k2 = 0; k2 < 6; ++k2) nu[k2] = S[(7 + k2) * kTile + t];
+#pragma unroll
+        for (int j = 0; j < UUV_MAX_ACT; ++j)
+          act[j] = (j < NA && j < A) ? S[(13 + j) * kTile + t] : R(0);
+        const bool has_cur = a.off_cur != 0xffffffffu;
+        V3<R> cur{R(0), R(0), R(0)};
+        if (has_cur) {
+          const R* Cc = reinterpret_cast<const R*>(buf + a.off_cur);
+          cur = V3<R>{Cc[t], Cc[kTile + t], Cc[2 * kTile + t]};
+        }
+        const double* ovs = DR ? reinterpret_cast<const double*>(buf + a.off_ov) : nullptr;
+        const bool d2 = physics_at<R, DR, AC, DM>(H, sv, i, ovs, kTile, t, has_cur, cur, a.K,
+                                                  a.dt, u, px, py, pz, q, nu, act);
+        S[t] = px; S[kTile + t] = py; S[2 * kTile + t] = pz;
+        S[3 * kTile + t] = q.w; S[4 * kTile + t] = q.x;
+        S[5 * kTile + t] = q.y; S[6 * kTile + t] = q.z;
+#pragma unroll
+        for (int k2 = 0; k2 < 6; ++k2) S[(7 + k2) * kTile + t] = nu[k2];
+#pragma unroll
+        for (int j = 0; j < NA; ++j)
+          if (j < A) S[(13 + j) * kTile + t] = act[j];
+        div[t] = d2 ? 1 : 0;
+      }
+      steps[t] += 1;
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    for (int r = lane; r < a.n_store; r += 32) {
+      const RowDesc& d = a.store[r];
+      bulk_s2g(const_cast<char*>(d.g) + row0 * d.elem, buf + d.soff,
+               round16((uint32_t)rows * d.elem));
+    }
+    bulk_commit();
+  }
+  bulk_wait_all();
+}
+
+// Inputs of one env's step, loaded ahead of use so that a persistent thread can
+// have env k+1's loads in flight while it computes env k.
+template <typename R> struct StepIn {
+  R px, py, pz;
+  Q4<R> q;
+  R nu[6], act[UUV_MAX_ACT], u[UUV_MAX_ACT];
+  int32_t steps;
+  uint8_t div, ty;
+};
+
+template <typename R, int NT, int AC>
+UUV_D void load_in(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in) {
+  const StateView<R>& sv = a.sv;
+  in.ty = NT > 1 ? sv.type_id[i] : 0;
+  const int A = AC > 0 ? AC : a.hull[in.ty].r.n_act;
+  constexpr int NA = AC > 0 ? AC : UUV_MAX_ACT;
+  in.steps = sv.steps[i];
+  in.div = sv.diverged[i];
+  const R* crow = a.cmd + i * a.cmd_ld;
+#pragma unroll
+  for (int j = 0; j < UUV_MAX_ACT; ++j)
+    in.u[j] = (j < NA && j < A) ? clip_<R>(crow[j], R(-1), R(1)) : R(0);
+  load_state(sv, i, A, in.px, in.py, in.pz, in.q, in.nu, in.act);
+}
+
+template <typename R, int NT, bool DR, int AC, bool DM>
+UUV_D void step_env(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in) {
+  const StateView<R>& sv = a.sv;
+  if (in.div) {  // frozen rows stay frozen (engine.py:411, 441-449)
+    sv.steps[i] = in.steps + 1;
+    return;
+  }
+  const Hull<R>& H = a.hull[in.ty];
+  const int A = AC > 0 ? AC : H.r.n_act;
+  const bool div = physics<R, DR, AC, DM>(H, sv, i, a.K, a.dt, in.u, in.px, in.py, in.pz, in.q,
+                                          in.nu, in.act);
+  store_state(sv, i, A, in.px, in.py, in.pz, in.q, in.nu, in.act);
+  sv.diverged[i] = div ? 1 : 0;
+  sv.steps[i] = in.steps + 1;
+}
+
+// One env per thread; when the grid is smaller than the batch (persistent mode)
+// each thread walks envs with stride gridDim * kBlock and prefetches the next
+// env's inputs into registers before computing the current one.
+template <typename R, int NT, bool DR, int AC, bool DM>
 __global__ void __launch_bounds__(kBlock, MinB<R>::value) k_step(const __grid_constant__ StepArgs<R, NT> a) {
   if (a.early_trigger) pdl_trigger();
   pdl_wait();
-  const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
-  const StateView<R>& sv = a.sv;
-  if (i >= sv.n) return;
-  const int t = NT > 1 ? (int)sv.type_id[i] : 0;
-  const Hull<R>& H = a.hull[t];
-  const int A = H.r.n_act;
-  const int32_t steps = sv.steps[i];
-  if (sv.diverged[i]) {  // frozen rows stay frozen (engine.py:411, 441-449)
-    sv.steps[i] = steps + 1;
-    return;
+  const int64_t stride = (int64_t)gridDim.x * kBlock;
+  int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+  const int64_t n = a.sv.n;
+  if (i >= n) return;
+  StepIn<R> cur;
+  load_in<R, NT, AC>(a, i, cur);
+  while (true) {
+    const int64_t nx = i + stride;
+    if (nx < n) {
+      StepIn<R> nxt;
+      load_in<R, NT, AC>(a, nx, nxt);
+      step_env<R, NT, DR, AC, DM>(a, i, cur);
+      cur = nxt;
+      i = nx;
+    } else {
+      step_env<R, NT, DR, AC, DM>(a, i, cur);
+      break;
+    }
   }
-  R u[UUV_MAX_ACT];
-  const R* crow = a.cmd + i * a.cmd_ld;
-#pragma unroll
-  for (int j = 0; j < UUV_MAX_ACT; ++j) u[j] = j < A ? clip_<R>(crow[j], R(-1), R(1)) : R(0);
-  R px, py, pz, nu[6], act[UUV_MAX_ACT];
-  Q4<R> q;
-  load_state(sv, i, A, px, py, pz, q, nu, act);
-  const bool div = physics<R, DR, AC>(H, sv, i, a.K, a.dt, u, px, py, pz, q, nu, act);
-  store_state(sv, i, A, px, py, pz, q, nu, act);
-  sv.diverged[i] = div ? 1 : 0;
-  sv.steps[i] = steps + 1;
 }
 
 // ------------------------------------------------------------------ task step
@@ -338,7 +539,7 @@ UUV_D void flush_obs(const R* s_obs, R* obs, int64_t obs_ld, int obs_dim, int64_
   }
 }
 
-template <typename R, bool DR, int AC>
+template <typename R, bool DR, int AC, bool DM>
 __global__ void __launch_bounds__(kBlock, MinB<R>::value) k_task_step(const __grid_constant__ TaskArgs<R> a) {
   __shared__ R s_obs[kBlock * kObsMax];
   __shared__ double s_red[kBlock / 32][UUV_ST_COUNT];
@@ -372,7 +573,7 @@ __global__ void __launch_bounds__(kBlock, MinB<R>::value) k_task_step(const __gr
     R px, py, pz, nu[6], act[UUV_MAX_ACT];
     Q4<R> q;
     load_state(sv, i, A, px, py, pz, q, nu, act);
-    if (!div) div = physics<R, DR, AC>(H, sv, i, a.K, a.dt_sub, u, px, py, pz, q, nu, act);
+    if (!div) div = physics<R, DR, AC, DM>(H, sv, i, a.K, a.dt_sub, u, px, py, pz, q, nu, act);
     steps += 1;
     R dev = a.dev_sum != nullptr ? a.dev_sum[i] : R(0);
     TaskOut<R> o;
@@ -593,7 +794,7 @@ template <typename R, int NT> struct TermsArgs {
   double* out;
 };
 
-template <typename R, int NT, bool DR, int AC>
+template <typename R, int NT, bool DR, int AC, bool DM>
 __global__ void __launch_bounds__(kBlock) k_terms(const __grid_constant__ TermsArgs<R, NT> a) {
   const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
   const StateView<R>& sv = a.sv;
@@ -611,14 +812,14 @@ __global__ void __launch_bounds__(kBlock) k_terms(const __grid_constant__ TermsA
   if (DR) {
     EnvD e;
     derive_env(H.d, sv.ov, sv.ld, i, sv.slot, e);
-    sub_from_env<R>(H.r, e, s);
+    sub_from_env<R, DM>(H.r, e, s);
     if (sv.slot[UUV_OV_JITTER] >= 0) jit = sv.ov + sv.slot[UUV_OV_JITTER] * sv.ld + i;
   }
   const bool has_cur = sv.cur != nullptr;
   V3<R> cur{R(0), R(0), R(0)};
   if (has_cur) cur = V3<R>{sv.cur[i], sv.cur[sv.ld + i], sv.cur[2 * sv.ld + i]};
   Terms<R> tm;
-  const bool ok = substep<R, DR, true, AC>(H.r, s, jit, sv.ld, px, py, pz, q, nu, act, u, has_cur, cur,
+  const bool ok = substep<R, DR, true, AC, DM>(H.r, s, jit, sv.ld, px, py, pz, q, nu, act, u, has_cur, cur,
                                        a.dt, &tm);
   double* o = a.out + i * 48;
   for (int k = 0; k < 6; ++k) {
@@ -667,6 +868,22 @@ int act_class(const uuv_ctx* ctx) {
   return h.n_act;
 }
 
+// Every env's composite mass matrix is diagonal: single diagonal hull with r_g = 0
+// and diagonal inertia, and no payload placed off the origin.
+bool diag_mass(const uuv_ctx* ctx, const uuv_state* st) {
+  if (ctx->hulls.size() != 1) return false;
+  const uuv_hull& h = ctx->hulls[0];
+  if (!(is_diag(h.M_A) && is_diag(h.D_lin) && is_diag(h.D_quad))) return false;
+  if (h.r_g[0] != 0.0 || h.r_g[1] != 0.0 || h.r_g[2] != 0.0) return false;
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c)
+      if (r != c && h.inertia[3 * r + c] != 0.0) return false;
+  if (st->overlay != nullptr && st->slot[UUV_OV_PAYLOAD_POS] >= 0 &&
+      !(st->flags & UUV_STATE_PAYLOAD_AT_ORIGIN))
+    return false;
+  return true;
+}
+
 template <typename R> const std::vector<Hull<R>>& hulls_of(const uuv_ctx* c);
 template <> const std::vector<Hull<float>>& hulls_of<float>(const uuv_ctx* c) { return c->hf; }
 template <> const std::vector<Hull<double>>& hulls_of<double>(const uuv_ctx* c) { return c->hd; }
@@ -680,9 +897,133 @@ void fill_hulls(const uuv_ctx* ctx, Hull<R>* dst, double dt_sub) {
   }
 }
 
-template <typename R, int NT, bool DR, int AC>
+// Persistent TMA-staged step: host-side slab layout + launch.
+uint32_t align128(uint32_t x) { return (x + 127u) & ~127u; }
+
+template <typename R, int NT, bool DR, int AC, bool DM>
+uuv_status launch_step_tma(const uuv_ctx* ctx, const uuv_state* st, const void* cmd,
+                           int64_t cmd_ld, int32_t K, double dt, cudaStream_t s) {
+  static TmaArgs<R, NT> a;  // large; built on the host once per call (not thread-safe to share)
+  const double dt_sub = dt / K;
+  fill_hulls<R, NT>(ctx, a.hull, dt_sub);
+  a.sv = make_view<R>(*st);
+  a.cmd = (const R*)cmd;
+  a.cmd_ld = cmd_ld;
+  a.K = K;
+  a.dt = (R)dt_sub;
+  a.early_trigger = 1;
+  const uint32_t es = sizeof(R), rowb = kTile * es;
+  const int64_t ld = st->ld;
+  int nl = 0, ns = 0;
+  uint32_t off = 0;
+  auto row_ptr = [&](int k) -> const char* {
+    if (k < 3) return (const char*)st->p + (size_t)k * ld * es;
+    if (k < 7) return (const char*)st->q + (size_t)(k - 3) * ld * es;
+    if (k < 13) return (const char*)st->nu + (size_t)(k - 7) * ld * es;
+    return (const char*)st->act + (size_t)(k - 13) * ld * es;
+  };
+  for (int k = 0; k < 13 + st->a_max; ++k) {
+    a.load[nl++] = RowDesc{row_ptr(k), es, off};
+    a.store[ns++] = RowDesc{row_ptr(k), es, off};
+    off += rowb;
+  }
+  a.off_cur = 0xffffffffu;
+  if (st->current_ned != nullptr) {
+    a.off_cur = off;
+    for (int k = 0; k < 3; ++k) {
+      a.load[nl++] = RowDesc{(const char*)st->current_ned + (size_t)k * ld * es, es, off};
+      off += rowb;
+    }
+  }
+  off = align128(off);
+  a.off_steps = off;
+  a.load[nl++] = RowDesc{(const char*)st->steps, 4, off};
+  a.store[ns++] = RowDesc{(const char*)st->steps, 4, off};
+  off += kTile * 4;
+  a.off_div = off;
+  a.load[nl++] = RowDesc{(const char*)st->diverged, 1, off};
+  a.store[ns++] = RowDesc{(const char*)st->diverged, 1, off};
+  off += kTile;
+  a.off_type = 0xffffffffu;
+  if (NT > 1) {
+    a.off_type = off;
+    a.load[nl++] = RowDesc{(const char*)st->type_id, 1, off};
+    off += kTile;
+  }
+  off = align128(off);
+  a.off_ov = 0xffffffffu;
+  if (DR) {
+    a.off_ov = off;
+    const int n_stage = st->slot[UUV_OV_JITTER] >= 0 ? st->slot[UUV_OV_JITTER] : st->n_slots;
+    for (int k = 0; k < n_stage; ++k) {
+      a.load[nl++] = RowDesc{(const char*)st->overlay + (size_t)k * ld * 8, 8, off};
+      off += kTile * 8;
+    }
+  }
+  a.cmd_row = -1;
+  a.off_cmd = 0xffffffffu;
+  if (((uintptr_t)cmd & 15u) == 0) {
+    off = align128(off);
+    a.off_cmd = off;
+    a.cmd_row = nl;
+    a.load[nl++] = RowDesc{(const char*)cmd, (uint32_t)(cmd_ld * es), off};
+    off += (uint32_t)(kTile * cmd_ld * es);
+  }
+  a.buf_bytes = align128(off);
+  a.n_load = nl;
+  a.n_store = ns;
+  a.n_tiles = (st->n_envs + kTile - 1) / kTile;
+  const size_t smem = 128 + (size_t)kWarps * 2 * a.buf_bytes;
+  auto kern = k_step_tma<R, NT, DR, AC, DM>;
+  static thread_local std::map<const void*, size_t> smem_set;
+  size_t& have = smem_set[(const void*)kern];
+  if (smem > have) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return fail(UUV_ERR_CUDA, "uuv_step smem: %s", cudaGetErrorString(e));
+    have = smem;
+  }
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem);
+  const int64_t grid = std::min<int64_t>((a.n_tiles + kWarps - 1) / kWarps,
+                                         (int64_t)sms * std::max(per_sm, 1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kBlock);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
+  if (e != cudaSuccess) return fail(UUV_ERR_CUDA, "uuv_step: %s", cudaGetErrorString(e));
+  return check_launch("uuv_step");
+}
+
+int64_t step_waves() {
+  static const int64_t w = [] {
+    const char* v = getenv("UUV_STEP_WAVES");
+    return v ? std::max<int64_t>(1, atoll(v)) : (int64_t)1;
+  }();
+  return w;
+}
+
+bool use_tma_step() {
+  static const bool on = [] {
+    const char* v = getenv("UUV_STEP_KERNEL");
+    return v && strcmp(v, "tma") == 0;
+  }();
+  return on;
+}
+
+template <typename R, int NT, bool DR, int AC, bool DM = false>
 uuv_status launch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd, int64_t cmd_ld,
                        int32_t K, double dt, cudaStream_t s) {
+  if (use_tma_step()) return launch_step_tma<R, NT, DR, AC, DM>(ctx, st, cmd, cmd_ld, K, dt, s);
   StepArgs<R, NT> a;
   const double dt_sub = dt / K;
   fill_hulls<R, NT>(ctx, a.hull, dt_sub);
@@ -691,9 +1032,12 @@ uuv_status launch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd,
   a.cmd_ld = cmd_ld;
   a.K = K;
   a.dt = (R)dt_sub;
-  const int64_t grid = grid_for(st->n_envs);
-  a.early_trigger = grid <= one_wave_ctas(k_step<R, NT, DR, AC>) ? 1 : 0;
-  cudaError_t e = launch_pdl(k_step<R, NT, DR, AC>, (unsigned)grid, s, a);
+  const int64_t need = grid_for(st->n_envs);
+  const int64_t wave = one_wave_ctas(k_step<R, NT, DR, AC, DM>);
+  // persistent (grid-stride + register prefetch) beyond one wave; UUV_STEP_WAVES overrides
+  const int64_t grid = std::min<int64_t>(need, wave * step_waves());
+  a.early_trigger = grid <= wave ? 1 : 0;
+  cudaError_t e = launch_pdl(k_step<R, NT, DR, AC, DM>, (unsigned)grid, s, a);
   if (e != cudaSuccess) return fail(UUV_ERR_CUDA, "uuv_step: %s", cudaGetErrorString(e));
   return check_launch("uuv_step");
 }
@@ -703,11 +1047,18 @@ uuv_status dispatch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cm
                          int32_t K, double dt, cudaStream_t s) {
   const bool dr = st->overlay != nullptr;
   if (ctx->hulls.size() == 1) {
+    const bool dm = diag_mass(ctx, st);
     switch (act_class(ctx)) {
       case 6:
+        if (dm)
+          return dr ? launch_step<R, 1, true, 6, true>(ctx, st, cmd, cmd_ld, K, dt, s)
+                    : launch_step<R, 1, false, 6, true>(ctx, st, cmd, cmd_ld, K, dt, s);
         return dr ? launch_step<R, 1, true, 6>(ctx, st, cmd, cmd_ld, K, dt, s)
                   : launch_step<R, 1, false, 6>(ctx, st, cmd, cmd_ld, K, dt, s);
       case 8:
+        if (dm)
+          return dr ? launch_step<R, 1, true, 8, true>(ctx, st, cmd, cmd_ld, K, dt, s)
+                    : launch_step<R, 1, false, 8, true>(ctx, st, cmd, cmd_ld, K, dt, s);
         return dr ? launch_step<R, 1, true, 8>(ctx, st, cmd, cmd_ld, K, dt, s)
                   : launch_step<R, 1, false, 8>(ctx, st, cmd, cmd_ld, K, dt, s);
       default:
@@ -761,17 +1112,22 @@ void fill_task_args(const uuv_ctx* ctx, const uuv_state* st, const uuv_task* tas
   a.cmd_ld = 0;
 }
 
+template <typename R, int AC, bool DM>
+void launch_task_dr(bool dr, unsigned g, cudaStream_t cs, const TaskArgs<R>& a) {
+  if (dr) k_task_step<R, true, AC, DM><<<g, kBlock, 0, cs>>>(a);
+  else k_task_step<R, false, AC, DM><<<g, kBlock, 0, cs>>>(a);
+}
+
 template <typename R>
-void launch_task_step(bool dr, int ac, unsigned g, cudaStream_t cs, const TaskArgs<R>& a) {
+void launch_task_step(bool dr, int ac, bool dm, unsigned g, cudaStream_t cs, const TaskArgs<R>& a) {
   if (ac == 6) {
-    if (dr) k_task_step<R, true, 6><<<g, kBlock, 0, cs>>>(a);
-    else k_task_step<R, false, 6><<<g, kBlock, 0, cs>>>(a);
+    if (dm) launch_task_dr<R, 6, true>(dr, g, cs, a);
+    else launch_task_dr<R, 6, false>(dr, g, cs, a);
   } else if (ac == 8) {
-    if (dr) k_task_step<R, true, 8><<<g, kBlock, 0, cs>>>(a);
-    else k_task_step<R, false, 8><<<g, kBlock, 0, cs>>>(a);
+    if (dm) launch_task_dr<R, 8, true>(dr, g, cs, a);
+    else launch_task_dr<R, 8, false>(dr, g, cs, a);
   } else {
-    if (dr) k_task_step<R, true, 0><<<g, kBlock, 0, cs>>>(a);
-    else k_task_step<R, false, 0><<<g, kBlock, 0, cs>>>(a);
+    launch_task_dr<R, 0, false>(dr, g, cs, a);
   }
 }
 
@@ -804,7 +1160,7 @@ static uuv_status derive_launch(const uuv_ctx* ctx, const uuv_state* st, double*
   return check_launch("uuv_derive_params");
 }
 
-template <typename R, int NT, bool DR, int AC>
+template <typename R, int NT, bool DR, int AC, bool DM = false>
 static uuv_status terms_launch(const uuv_ctx* ctx, const uuv_state* st, const void* cmd,
                                int64_t cmd_ld, double dt_sub, double* out, cudaStream_t cs) {
   TermsArgs<R, NT> a;
@@ -814,7 +1170,7 @@ static uuv_status terms_launch(const uuv_ctx* ctx, const uuv_state* st, const vo
   a.cmd_ld = cmd_ld;
   a.dt = (R)dt_sub;
   a.out = out;
-  k_terms<R, NT, DR, AC><<<(unsigned)grid_for(st->n_envs), kBlock, 0, cs>>>(a);
+  k_terms<R, NT, DR, AC, DM><<<(unsigned)grid_for(st->n_envs), kBlock, 0, cs>>>(a);
   return check_launch("uuv_substep_terms");
 }
 
@@ -825,11 +1181,18 @@ static uuv_status terms_dispatch(const uuv_ctx* ctx, const uuv_state* st, const 
   if (multi)
     return dr ? terms_launch<R, UUV_MAX_TYPES, true, 0>(ctx, st, cmd, cmd_ld, dt_sub, out, cs)
               : terms_launch<R, UUV_MAX_TYPES, false, 0>(ctx, st, cmd, cmd_ld, dt_sub, out, cs);
+  const bool dm = diag_mass(ctx, st);
   switch (act_class(ctx)) {
     case 6:
+      if (dm)
+        return dr ? terms_launch<R, 1, true, 6, true>(ctx, st, cmd, cmd_ld, dt_sub, out, cs)
+                  : terms_launch<R, 1, false, 6, true>(ctx, st, cmd, cmd_ld, dt_sub, out, cs);
       return dr ? terms_launch<R, 1, true, 6>(ctx, st, cmd, cmd_ld, dt_sub, out, cs)
                 : terms_launch<R, 1, false, 6>(ctx, st, cmd, cmd_ld, dt_sub, out, cs);
     case 8:
+      if (dm)
+        return dr ? terms_launch<R, 1, true, 8, true>(ctx, st, cmd, cmd_ld, dt_sub, out, cs)
+                  : terms_launch<R, 1, false, 8, true>(ctx, st, cmd, cmd_ld, dt_sub, out, cs);
       return dr ? terms_launch<R, 1, true, 8>(ctx, st, cmd, cmd_ld, dt_sub, out, cs)
                 : terms_launch<R, 1, false, 8>(ctx, st, cmd, cmd_ld, dt_sub, out, cs);
     default:
@@ -946,6 +1309,42 @@ uuv_status uuv_step(uuv_ctx* ctx, const uuv_state* st, const void* commands, int
                               : dispatch_step<double>(ctx, st, commands, cmd_ld, substeps, dt, cs);
 }
 
+uuv_status uuv_step_host(uuv_ctx* ctx, const uuv_state* st, const void* host_cmd, int64_t cmd_ld,
+                         void* dev_cmd, void* host_pose, int32_t substeps, double dt,
+                         void* stream, int32_t sync) {
+  uuv_status s = check_state(ctx, st);
+  if (s != UUV_OK) return s;
+  if (host_cmd == nullptr || dev_cmd == nullptr) return fail(UUV_ERR_ARG, "commands: null");
+  if (st->n_envs == 0) return UUV_OK;
+  cudaStream_t cs = (cudaStream_t)stream;
+  const size_t es = st->dtype == UUV_F32 ? sizeof(float) : sizeof(double);
+  cudaError_t e = cudaMemcpyAsync(dev_cmd, host_cmd, (size_t)st->n_envs * cmd_ld * es,
+                                  cudaMemcpyHostToDevice, cs);
+  if (e != cudaSuccess) return fail(UUV_ERR_CUDA, "commands H2D: %s", cudaGetErrorString(e));
+  if ((s = uuv_step(ctx, st, dev_cmd, cmd_ld, substeps, dt, stream)) != UUV_OK) return s;
+  if (host_pose != nullptr) {
+    const size_t row = (size_t)st->n_envs * es, pitch = (size_t)st->ld * es;
+    const char* p = (const char*)st->p;
+    if ((const char*)st->q == p + 3 * pitch && (const char*)st->nu == p + 7 * pitch) {
+      e = cudaMemcpy2DAsync(host_pose, row, p, pitch, row, 13, cudaMemcpyDeviceToHost, cs);
+    } else {
+      e = cudaMemcpy2DAsync(host_pose, row, st->p, pitch, row, 3, cudaMemcpyDeviceToHost, cs);
+      if (e == cudaSuccess)
+        e = cudaMemcpy2DAsync((char*)host_pose + 3 * row, row, st->q, pitch, row, 4,
+                              cudaMemcpyDeviceToHost, cs);
+      if (e == cudaSuccess)
+        e = cudaMemcpy2DAsync((char*)host_pose + 7 * row, row, st->nu, pitch, row, 6,
+                              cudaMemcpyDeviceToHost, cs);
+    }
+    if (e != cudaSuccess) return fail(UUV_ERR_CUDA, "pose D2H: %s", cudaGetErrorString(e));
+  }
+  if (sync) {
+    e = cudaStreamSynchronize(cs);
+    if (e != cudaSuccess) return fail(UUV_ERR_CUDA, "sync: %s", cudaGetErrorString(e));
+  }
+  return UUV_OK;
+}
+
 uuv_status uuv_reset(uuv_ctx* ctx, const uuv_state* st, const uint8_t* mask,
                      const uuv_sampler* sampler, uint64_t seed, void* stream) {
   uuv_status s = check_state(ctx, st);
@@ -984,13 +1383,13 @@ uuv_status uuv_task_step(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task
     fill_task_args<float>(ctx, st, task, sampler, seed, dt, substeps, io, a);
     a.cmd = (const float*)commands;
     a.cmd_ld = cmd_ld;
-    launch_task_step<float>(dr, act_class(ctx), g, cs, a);
+    launch_task_step<float>(dr, act_class(ctx), diag_mass(ctx, st), g, cs, a);
   } else {
     TaskArgs<double> a;
     fill_task_args<double>(ctx, st, task, sampler, seed, dt, substeps, io, a);
     a.cmd = (const double*)commands;
     a.cmd_ld = cmd_ld;
-    launch_task_step<double>(dr, act_class(ctx), g, cs, a);
+    launch_task_step<double>(dr, act_class(ctx), diag_mass(ctx, st), g, cs, a);
   }
   return check_launch("uuv_task_step");
 }

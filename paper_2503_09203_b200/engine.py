@@ -324,6 +324,9 @@ class BatchState:
             self._type[:n] = torch.from_numpy(ids).to(self.device)
         self._ov = None
         self._ov_keys = None
+        self._payload_offsets = False  # some env may carry a payload off the origin
+        self._pin = None  # pinned staging for host-side commands (step_batch host path)
+        self._dcmd = None
         self._slots = {}
         self._host_overlays = {}
         self._hulls = [pack_hull(v) for v in self.vehicles]
@@ -462,7 +465,20 @@ class BatchState:
             s.slot[k] = -1
         for name, s0 in self._slots.items():
             s.slot[N.OV_INDEX[name]] = s0
+        s.flags = 0 if self._payload_offsets else N.STATE_PAYLOAD_AT_ORIGIN
         return s
+
+    def _note_sampler(self, sampler: "DeviceSampler"):
+        """Record what a device sampler can write (slots, current, payload offsets)."""
+        keys = sampler.keys()
+        if keys:
+            self._ensure_slots(keys)
+        if sampler.current_spec:
+            self._enable_current()
+        p = (sampler.overlay_spec or {}).get("payload_position")
+        if p is not None and p.distribution.support() != (0.0, 0.0):
+            self._payload_offsets = True
+            self._cs = None
 
     def _assign_vehicle(self, i, cfg):
         if cfg.action_dim > self.a_max:
@@ -528,14 +544,70 @@ def _commands(state: BatchState, commands, width):
     return t
 
 
-def step_batch(state: BatchState, commands) -> BatchState:
-    """Advance every environment one control step (engine.py:465-484)."""
-    width = state.a_max if len(state.vehicles) > 1 or state._type is not None else \
+def _cmd_width(state: BatchState) -> int:
+    return state.a_max if len(state.vehicles) > 1 or state._type is not None else \
         state.vehicle.action_dim
+
+
+def step_batch(state: BatchState, commands, *, pose_out=None) -> BatchState:
+    """Advance every environment one control step (engine.py:465-484).
+
+    ``commands``: (N, A) CUDA tensor (one launch, no host sync), or host data — a CPU
+    tensor or numpy array, staged through a pinned buffer and copied asynchronously.
+    ``pose_out``: optional pinned CPU tensor (13, N) in the batch dtype; receives the
+    rows p (3), q (4), nu (6) after the step and the call waits for them.
+    """
+    width = _cmd_width(state)
+    host = not torch.is_tensor(commands) or commands.device.type == "cpu"
+    if host or pose_out is not None:
+        return _step_host(state, commands, width, pose_out)
     cmd = _commands(state, commands, width)
     N.check(N.load().uuv_step(state._ctx, C.byref(state._cstate()), cmd.data_ptr(),
                               cmd.stride(0), state.sim.substeps, state.sim.dt, state._stream()),
             EngineError)
+    return state
+
+
+def _step_host(state: BatchState, commands, width, pose_out):
+    n = state.n_envs
+    st = state
+    if st._pin is None:
+        st._pin = torch.empty((n, width), dtype=st.dtype).pin_memory()
+        st._dcmd = torch.empty((n, width), dtype=st.dtype, device=st.device)
+    if torch.is_tensor(commands):
+        if tuple(commands.shape) != (n, width):
+            raise EngineError(f"commands: expected shape {(n, width)}, got {tuple(commands.shape)}")
+        if commands.device.type == "cpu" and commands.is_pinned() and commands.dtype == st.dtype \
+                and commands.is_contiguous():
+            src = commands
+        elif commands.device.type == "cpu":
+            st._pin.copy_(commands)
+            src = st._pin
+        else:  # device commands with a host pose_out
+            src = None
+    else:
+        arr = np.asarray(commands)
+        if arr.shape != (n, width):
+            raise EngineError(f"commands: expected shape {(n, width)}, got {arr.shape}")
+        st._pin.numpy()[...] = arr
+        src = st._pin
+    if pose_out is not None:
+        if (tuple(pose_out.shape) != (13, n) or pose_out.dtype != st.dtype
+                or not pose_out.is_pinned() or not pose_out.is_contiguous()):
+            raise EngineError(f"pose_out: expected a pinned contiguous ({13}, {n}) {st.dtype} tensor")
+    lib = N.load()
+    if src is None:
+        cmd = _commands(state, commands, width)
+        N.check(lib.uuv_step(st._ctx, C.byref(st._cstate()), cmd.data_ptr(), cmd.stride(0),
+                             st.sim.substeps, st.sim.dt, st._stream()), EngineError)
+        torch.cuda.current_stream(st.device).synchronize()
+        pose_out.copy_(st._soa[:13, :n])
+        return state
+    N.check(lib.uuv_step_host(st._ctx, C.byref(st._cstate()), src.data_ptr(), width,
+                              st._dcmd.data_ptr(),
+                              pose_out.data_ptr() if pose_out is not None else None,
+                              st.sim.substeps, st.sim.dt, st._stream(),
+                              1 if pose_out is not None or src is st._pin else 0), EngineError)
     return state
 
 
@@ -570,11 +642,7 @@ def reset_envs(state: BatchState, mask, sampler: InitSampler = default_sampler) 
 
 
 def _device_reset(state: BatchState, m, sampler: DeviceSampler):
-    keys = sampler.keys()
-    if keys:
-        state._ensure_slots(keys)
-    if sampler.current_spec:
-        state._enable_current()
+    state._note_sampler(sampler)
     rows_mask = m.to(torch.uint8)
     packed = sampler.pack()
     if state._host_overlays:
@@ -633,6 +701,9 @@ def _host_reset(state: BatchState, m, sampler):
                 kbits[r] |= 1 << N.OV_INDEX[name]
                 if name == "payload_position":
                     block[s0:s0 + 3, r] = np.asarray(v, float)
+                    if np.any(block[s0:s0 + 3, r] != 0.0):
+                        state._payload_offsets = True
+                        state._cs = None
                 elif name == "mount_position_jitter":
                     jv = np.asarray(v, float)
                     jm = np.zeros((N.MAX_ACT, 3))

@@ -241,10 +241,7 @@ class VecTaskEnv:
         st = self.state
         self._sampler = spec_sampler(self._dr, start_box(task))
         self._sampler_c = self._sampler.pack()
-        if self._sampler.keys():
-            st._ensure_slots(self._sampler.keys())
-        if self._sampler.current_spec:
-            st._enable_current()
+        st._note_sampler(self._sampler)
         ld, dev = st._ld, st.device
         self._prev_u = torch.zeros((self.action_dim, ld), dtype=dtype, device=dev)
         self._dev_sum = torch.zeros(ld, dtype=dtype, device=dev) if task.task == TRACKING else None

@@ -68,7 +68,51 @@ def make_case(name, n):
     return st, width, bpf
 
 
+def measure_task(name, n, steps):
+    """Fused task step (physics + obs/reward/termination/auto-reset) per env.step call."""
+    from paper_2503_09203_b200.tasks import TaskConfig, make_env
+
+    dev = torch.device("cuda", 0)
+    if name == "task_cfg4":  # tracking with ocean current, 8 fused substeps
+        task = TaskConfig(task="tracking", vehicle="bluerov", level="disturbed")
+        env = make_env(task, E.SimConfig(batch_size=n, substeps=8), seed=0, device=dev)
+        a = 6
+    else:  # task_cfg5: docking, train-preset DR, auto-reset on
+        task = TaskConfig(task="docking", vehicle="bluerov_heavy", level="disturbed_dr")
+        env = make_env(task, E.SimConfig(batch_size=n), seed=0, device=dev)
+        a = 8
+    env.reset()
+    cmds = torch.rand((n, a), device=dev) * 2 - 1
+    s = torch.cuda.Stream(dev)
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            env.step(cmds)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(steps):
+                env.step(cmds)
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = None
+    for _ in range(3):
+        with torch.cuda.stream(s):
+            e0.record(s)
+            g.replay()
+            e1.record(s)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / 1e3 / steps
+        best = t if best is None else min(best, t)
+    stats = env.rollout_stats()
+    return {"case": name, "n": n, "us_per_step": best * 1e6, "frames_per_s": n / best,
+            "finished_per_frame": stats["finished"] / max(stats["frames"], 1)}
+
+
 def measure(name, n, steps):
+    if name.startswith("task_"):
+        return measure_task(name, n, steps)
     st, width, bpf = make_case(name, n)
     dev = st.device
     cmds = torch.rand((n, width), device=dev) * 2 - 1
