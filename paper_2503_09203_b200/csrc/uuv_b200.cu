@@ -13,6 +13,8 @@
 #include <cstdio>
 #include <cstring>
 #include <algorithm>
+#include <climits>
+#include <cstdint>
 #include <cstdlib>
 #include <map>
 #include <string>
@@ -178,6 +180,7 @@ struct uuv_ctx {
 
 template <typename R, int NT> struct StepArgs {
   Hull<R> hull[NT];
+  int8_t cls[NT];  // mixed fleets: per-type specialisation (see hull_class)
   StateView<R> sv;
   const R* cmd;
   int64_t cmd_ld;
@@ -476,6 +479,23 @@ UUV_D void step_env(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in) {
   sv.steps[i] = in.steps + 1;
 }
 
+// Mixed fleets: every env takes its vehicle type's specialised path (types are
+// contiguous env blocks, so the switch is warp-uniform except at block edges).
+template <typename R, int NT, bool DR, int AC, bool DM>
+UUV_D void step_any(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in) {
+  if constexpr (NT > 1) {
+    switch (a.cls[in.ty]) {
+      case 1: step_env<R, NT, DR, 6, true>(a, i, in); return;
+      case 2: step_env<R, NT, DR, 8, true>(a, i, in); return;
+      case 3: step_env<R, NT, DR, 6, false>(a, i, in); return;
+      case 4: step_env<R, NT, DR, 8, false>(a, i, in); return;
+      default: step_env<R, NT, DR, 0, false>(a, i, in); return;
+    }
+  } else {
+    step_env<R, NT, DR, AC, DM>(a, i, in);
+  }
+}
+
 // One env per thread; when the grid is smaller than the batch (persistent mode)
 // each thread walks envs with stride gridDim * kBlock and prefetches the next
 // env's inputs into registers before computing the current one.
@@ -489,19 +509,24 @@ __global__ void __launch_bounds__(kBlock, MinB<R>::value) k_step(const __grid_co
   if (i >= n) return;
   StepIn<R> cur;
   load_in<R, NT, AC>(a, i, cur);
+#if UUV_PERSISTENT_STEP
   while (true) {
     const int64_t nx = i + stride;
     if (nx < n) {
       StepIn<R> nxt;
       load_in<R, NT, AC>(a, nx, nxt);
-      step_env<R, NT, DR, AC, DM>(a, i, cur);
+      step_any<R, NT, DR, AC, DM>(a, i, cur);
       cur = nxt;
       i = nx;
     } else {
-      step_env<R, NT, DR, AC, DM>(a, i, cur);
+      step_any<R, NT, DR, AC, DM>(a, i, cur);
       break;
     }
   }
+#else
+  (void)stride;
+  step_any<R, NT, DR, AC, DM>(a, i, cur);
+#endif
 }
 
 // ------------------------------------------------------------------ task step
@@ -858,21 +883,21 @@ uuv_status check_state(const uuv_ctx* ctx, const uuv_state* st) {
   return UUV_OK;
 }
 
-// Actuator class of a single-vehicle batch (see substep): A first-order thrusters.
-int act_class(const uuv_ctx* ctx) {
-  if (ctx->hulls.size() != 1) return 0;
-  const uuv_hull& h = ctx->hulls[0];
+// Actuator class of a hull (see substep): A first-order thrusters, else 0.
+int hull_act_class(const uuv_hull& h) {
   if (h.n_act != 6 && h.n_act != 8) return 0;
   for (int j = 0; j < h.n_act; ++j)
     if (h.kind[j] == UUV_RUDDER || h.model[j] != UUV_FIRST_ORDER) return 0;
   return h.n_act;
 }
 
+int act_class(const uuv_ctx* ctx) {
+  return ctx->hulls.size() == 1 ? hull_act_class(ctx->hulls[0]) : 0;
+}
+
 // Every env's composite mass matrix is diagonal: single diagonal hull with r_g = 0
 // and diagonal inertia, and no payload placed off the origin.
-bool diag_mass(const uuv_ctx* ctx, const uuv_state* st) {
-  if (ctx->hulls.size() != 1) return false;
-  const uuv_hull& h = ctx->hulls[0];
+bool hull_diag_mass(const uuv_hull& h, const uuv_state* st) {
   if (!(is_diag(h.M_A) && is_diag(h.D_lin) && is_diag(h.D_quad))) return false;
   if (h.r_g[0] != 0.0 || h.r_g[1] != 0.0 || h.r_g[2] != 0.0) return false;
   for (int r = 0; r < 3; ++r)
@@ -882,6 +907,19 @@ bool diag_mass(const uuv_ctx* ctx, const uuv_state* st) {
       !(st->flags & UUV_STATE_PAYLOAD_AT_ORIGIN))
     return false;
   return true;
+}
+
+bool diag_mass(const uuv_ctx* ctx, const uuv_state* st) {
+  return ctx->hulls.size() == 1 && hull_diag_mass(ctx->hulls[0], st);
+}
+
+// Specialisation code of each type of a mixed fleet (step_any).
+int8_t hull_class(const uuv_hull& h, const uuv_state* st) {
+  const int ac = hull_act_class(h);
+  const bool dm = hull_diag_mass(h, st);
+  if (ac == 6) return dm ? 1 : 3;
+  if (ac == 8) return dm ? 2 : 4;
+  return 0;
 }
 
 template <typename R> const std::vector<Hull<R>>& hulls_of(const uuv_ctx* c);
@@ -1004,7 +1042,11 @@ uuv_status launch_step_tma(const uuv_ctx* ctx, const uuv_state* st, const void* 
   return check_launch("uuv_step");
 }
 
+#ifndef UUV_PERSISTENT_STEP
+#define UUV_PERSISTENT_STEP 0
+#endif
 int64_t step_waves() {
+  if (!UUV_PERSISTENT_STEP) return INT64_MAX / 4;  // one thread per env
   static const int64_t w = [] {
     const char* v = getenv("UUV_STEP_WAVES");
     return v ? std::max<int64_t>(1, atoll(v)) : (int64_t)1;
@@ -1027,6 +1069,8 @@ uuv_status launch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd,
   StepArgs<R, NT> a;
   const double dt_sub = dt / K;
   fill_hulls<R, NT>(ctx, a.hull, dt_sub);
+  for (int t = 0; t < NT; ++t)
+    a.cls[t] = t < (int)ctx->hulls.size() ? hull_class(ctx->hulls[t], st) : 0;
   a.sv = make_view<R>(*st);
   a.cmd = (const R*)cmd;
   a.cmd_ld = cmd_ld;
@@ -1035,7 +1079,8 @@ uuv_status launch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd,
   const int64_t need = grid_for(st->n_envs);
   const int64_t wave = one_wave_ctas(k_step<R, NT, DR, AC, DM>);
   // persistent (grid-stride + register prefetch) beyond one wave; UUV_STEP_WAVES overrides
-  const int64_t grid = std::min<int64_t>(need, wave * step_waves());
+  const int64_t waves = step_waves();
+  const int64_t grid = waves >= need ? need : std::min<int64_t>(need, wave * waves);
   a.early_trigger = grid <= wave ? 1 : 0;
   cudaError_t e = launch_pdl(k_step<R, NT, DR, AC, DM>, (unsigned)grid, s, a);
   if (e != cudaSuccess) return fail(UUV_ERR_CUDA, "uuv_step: %s", cudaGetErrorString(e));
@@ -1325,7 +1370,10 @@ uuv_status uuv_step_host(uuv_ctx* ctx, const uuv_state* st, const void* host_cmd
   if (host_pose != nullptr) {
     const size_t row = (size_t)st->n_envs * es, pitch = (size_t)st->ld * es;
     const char* p = (const char*)st->p;
-    if ((const char*)st->q == p + 3 * pitch && (const char*)st->nu == p + 7 * pitch) {
+    if ((const char*)st->q == p + 3 * pitch && (const char*)st->nu == p + 7 * pitch &&
+        row == pitch) {  // n == ld: the 13 pose rows are one contiguous span
+      e = cudaMemcpyAsync(host_pose, p, 13 * row, cudaMemcpyDeviceToHost, cs);
+    } else if ((const char*)st->q == p + 3 * pitch && (const char*)st->nu == p + 7 * pitch) {
       e = cudaMemcpy2DAsync(host_pose, row, p, pitch, row, 13, cudaMemcpyDeviceToHost, cs);
     } else {
       e = cudaMemcpy2DAsync(host_pose, row, st->p, pitch, row, 3, cudaMemcpyDeviceToHost, cs);
