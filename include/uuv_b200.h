@@ -168,11 +168,16 @@ enum { UUV_CURRENT_NONE = 0, UUV_CURRENT_RANDOM_HEADING = 1, UUV_CURRENT_HEADING
  *   start box: p = p_base + U(p_lo, p_hi) (3), euler = U(eul_lo, eul_hi) (3),
  *              nu = U(nu_lo, nu_hi) (6).
  */
+/* Per-(seed, env, episode) stream of a reset. */
+enum { UUV_RNG_PHILOX = 0,  /* Philox4x64-10, key [seed, env], counter [0, episode, 0, 0] */
+       UUV_RNG_PCG64 = 1 }; /* PCG64(SeedSequence(seed, spawn_key=(env, episode))): the
+                               unmodified reference's BatchState.env_rng (engine.py:291-295) */
+
 typedef struct {
   int32_t n_overlay;
   int32_t current_mode;
   int32_t start_mode;
-  int32_t pad_;
+  int32_t rng_mode;        /* UUV_RNG_* */
   uuv_draw overlay[UUV_MAX_DRAWS];
   uuv_draw current_speed, current_heading;
   double p_base[3], p_lo[3], p_hi[3];

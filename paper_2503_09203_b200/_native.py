@@ -41,6 +41,8 @@ CURRENT_NONE, CURRENT_RANDOM_HEADING, CURRENT_HEADING_DRAW = 0, 1, 2
 TASK_STATION, TASK_TRACKING, TASK_DOCKING = 0, 1, 2
 TRAJ_HELIX, TRAJ_LISSAJOUS = 0, 1
 STATE_PAYLOAD_AT_ORIGIN = 1
+RNG_PHILOX, RNG_PCG64 = 0, 1
+RNG_MODES = {"philox": RNG_PHILOX, "pcg64": RNG_PCG64}
 TR_NAMES = ("reward", "position_error", "attitude_error", "metric", "time", "contact_distance",
             "contact_speed", "contact_attitude")
 TF_NAMES = ("terminated", "truncated", "finished", "failure", "success", "diverged", "contact")
@@ -90,7 +92,7 @@ class Draw(C.Structure):
 class Sampler(C.Structure):
     _fields_ = [
         ("n_overlay", C.c_int32), ("current_mode", C.c_int32), ("start_mode", C.c_int32),
-        ("pad_", C.c_int32),
+        ("rng_mode", C.c_int32),
         ("overlay", Draw * MAX_DRAWS), ("current_speed", Draw), ("current_heading", Draw),
         ("p_base", C.c_double * 3), ("p_lo", C.c_double * 3), ("p_hi", C.c_double * 3),
         ("eul_lo", C.c_double * 3), ("eul_hi", C.c_double * 3),

@@ -197,6 +197,17 @@ template <typename R, int NT> struct StepArgs {
 UUV_D void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 UUV_D void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 
+// UUV_PDL: 0 off, 1 trigger dependents at kernel entry, 2 (default) trigger after the
+// stores.  Measured on B200 (cfg2, 4096 envs, graph of 100 steps): 2.57 / 3.29 / 2.34 us.
+int pdl_mode() {
+  static const int m = [] {
+    const char* v = getenv("UUV_PDL");
+    return v ? atoi(v) : 2;
+  }();
+  return m;
+}
+bool pdl_enabled() { return pdl_mode() != 0; }
+
 template <typename Kernel, typename Args>
 cudaError_t launch_pdl(Kernel k, unsigned grid, cudaStream_t s, const Args& a) {
   cudaLaunchConfig_t cfg = {};
@@ -208,7 +219,7 @@ cudaError_t launch_pdl(Kernel k, unsigned grid, cudaStream_t s, const Args& a) {
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, k, a);
 }
 
@@ -500,9 +511,16 @@ UUV_D void step_any(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in) {
 // each thread walks envs with stride gridDim * kBlock and prefetches the next
 // env's inputs into registers before computing the current one.
 template <typename R, int NT, bool DR, int AC, bool DM>
-__global__ void __launch_bounds__(kBlock, MinB<R>::value) k_step(const __grid_constant__ StepArgs<R, NT> a) {
-  if (a.early_trigger) pdl_trigger();
+__global__ void __launch_bounds__(kBlock, (NT > 1 && sizeof(R) == 4) ? 3 : MinB<R>::value)
+    k_step(const __grid_constant__ StepArgs<R, NT> a) {
+  if (a.early_trigger == 1) pdl_trigger();
   pdl_wait();
+  struct ExitTrigger {
+    bool on;
+    __device__ ~ExitTrigger() {
+      if (on) pdl_trigger();
+    }
+  } exit_trigger{a.early_trigger == 2};
   const int64_t stride = (int64_t)gridDim.x * kBlock;
   int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
   const int64_t n = a.sv.n;
@@ -1081,7 +1099,7 @@ uuv_status launch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd,
   // persistent (grid-stride + register prefetch) beyond one wave; UUV_STEP_WAVES overrides
   const int64_t waves = step_waves();
   const int64_t grid = waves >= need ? need : std::min<int64_t>(need, wave * waves);
-  a.early_trigger = grid <= wave ? 1 : 0;
+  a.early_trigger = pdl_mode() == 2 ? 2 : ((grid <= wave && pdl_enabled()) ? 1 : 0);
   cudaError_t e = launch_pdl(k_step<R, NT, DR, AC, DM>, (unsigned)grid, s, a);
   if (e != cudaSuccess) return fail(UUV_ERR_CUDA, "uuv_step: %s", cudaGetErrorString(e));
   return check_launch("uuv_step");

@@ -39,8 +39,8 @@ UUV_D void reset_env(const StateView<R>& sv, int64_t i, const uuv_sampler& smp, 
                      R& px, R& py, R& pz, Q4<R>& q, R* nu, V3<R>& cur) {
   const int32_t ep = sv.episodes[i] + 1;
   sv.episodes[i] = ep;
-  Philox g;
-  g.init(seed, (uint64_t)(sv.env_offset + i), (uint64_t)(int64_t)ep);
+  EnvRng g;
+  g.init(smp.rng_mode, seed, (uint64_t)(sv.env_offset + i), (uint64_t)(int64_t)ep);
   const int64_t ld = sv.ld;
   // identity record: ratios 1, cobm/payload/positions/jitter 0
   if (sv.ov != nullptr) {

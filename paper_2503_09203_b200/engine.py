@@ -40,6 +40,15 @@ from .vehicles import (
 M64 = (1 << 64) - 1
 _ALIGN = 32
 
+try:  # the raw cudaStream_t of the current stream without building a Stream object
+    _get_raw_stream = torch._C._cuda_getCurrentRawStream
+
+    def _raw_stream(index):
+        return _get_raw_stream(index)
+except AttributeError:  # pragma: no cover
+    def _raw_stream(index):
+        return torch.cuda.current_stream(index).cuda_stream
+
 
 class EngineError(ValueError):
     pass
@@ -90,10 +99,20 @@ def default_sampler(env_index: int, episode: int, rng) -> EnvInit:
 
 
 def philox_generator(seed: int, env_index: int, episode: int) -> np.random.Generator:
-    """Host twin of the device stream (same bits as the reset kernel)."""
+    """Host twin of the device Philox stream (same bits as the reset kernel)."""
     return np.random.Generator(np.random.Philox(
         key=np.array([int(seed) & M64, int(env_index) & M64], dtype=np.uint64),
         counter=np.array([0, int(episode) & M64, 0, 0], dtype=np.uint64)))
+
+
+def pcg64_generator(seed: int, env_index: int, episode: int) -> np.random.Generator:
+    """The reference's own stream, PCG64(SeedSequence(seed, spawn_key=(env, episode)))
+    (engine.py:291-295); the reset kernel restates it bit for bit (rng="pcg64")."""
+    return np.random.Generator(np.random.PCG64(
+        np.random.SeedSequence(int(seed) & M64, spawn_key=(int(env_index), int(episode)))))
+
+
+RNG_GENERATORS = {"philox": philox_generator, "pcg64": pcg64_generator}
 
 
 # ================================================================ hull packing
@@ -289,15 +308,19 @@ class BatchState:
     """N environments of one vehicle (or a mixed fleet) resident in HBM."""
 
     def __init__(self, vehicles, counts, sim: SimConfig, master_seed=0, device=None,
-                 dtype=torch.float32, env_offset=0):
+                 dtype=torch.float32, env_offset=0, rng="philox"):
         if dtype not in (torch.float32, torch.float64):
             raise EngineError("dtype must be torch.float32 or torch.float64")
+        if rng not in RNG_GENERATORS:
+            raise EngineError(f"rng must be one of {sorted(RNG_GENERATORS)}, got {rng!r}")
+        self.rng = rng
         self.sim = sim
         self.vehicles = list(vehicles)
         self.vehicle = self.vehicles[0]
         self.master_seed = int(master_seed)
         self.env_offset = int(env_offset)
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self._dev_index = self.device.index if self.device.index is not None else torch.cuda.current_device()
         self.dtype = dtype
         n = int(sum(counts))
         if n != sim.batch_size:
@@ -327,6 +350,7 @@ class BatchState:
         self._payload_offsets = False  # some env may carry a payload off the origin
         self._pin = None  # pinned staging for host-side commands (step_batch host path)
         self._dcmd = None
+        self._pinned_cache = {}
         self._slots = {}
         self._host_overlays = {}
         self._hulls = [pack_hull(v) for v in self.vehicles]
@@ -407,12 +431,12 @@ class BatchState:
 
     def env_rng(self, i: int) -> np.random.Generator:
         """The counter-based substream of env i's current episode (engine.py:291-295)."""
-        return philox_generator(self.master_seed, self.env_offset + int(i),
-                                int(self.episodes[int(i)].item()))
+        return RNG_GENERATORS[self.rng](self.master_seed, self.env_offset + int(i),
+                                        int(self.episodes[int(i)].item()))
 
     # ---------------------------------------------------------------- internals
     def _stream(self):
-        return torch.cuda.current_stream(self.device).cuda_stream
+        return _raw_stream(self._dev_index)
 
     def _enable_current(self):
         if self._cur is None:
@@ -513,17 +537,22 @@ class _Layout:
 
 
 def make_batch(vehicle: VehicleConfig, sim: SimConfig, master_seed: int = 0, *, device=None,
-               dtype=torch.float32, env_offset: int = 0) -> BatchState:
-    """Allocate a batch primed with the base vehicle; call reset_envs to start."""
-    return BatchState([vehicle], [sim.batch_size], sim, master_seed, device, dtype, env_offset)
+               dtype=torch.float32, env_offset: int = 0, rng: str = "philox") -> BatchState:
+    """Allocate a batch primed with the base vehicle; call reset_envs to start.
+
+    ``rng``: ``"philox"`` (default) or ``"pcg64"`` — the reference's own
+    PCG64/SeedSequence streams, for resets bit-identical to the unmodified reference.
+    """
+    return BatchState([vehicle], [sim.batch_size], sim, master_seed, device, dtype, env_offset,
+                      rng)
 
 
 def make_fleet_batch(vehicles, counts, sim: SimConfig, master_seed: int = 0, *, device=None,
-                     dtype=torch.float32, env_offset: int = 0) -> BatchState:
+                     dtype=torch.float32, env_offset: int = 0, rng: str = "philox") -> BatchState:
     """Mixed-vehicle batch: contiguous env blocks per vehicle type, commands padded to A_max."""
     if len(vehicles) != len(counts) or not 1 <= len(vehicles) <= N.MAX_TYPES:
         raise EngineError(f"need 1..{N.MAX_TYPES} vehicles with one count each")
-    return BatchState(vehicles, counts, sim, master_seed, device, dtype, env_offset)
+    return BatchState(vehicles, counts, sim, master_seed, device, dtype, env_offset, rng)
 
 
 def _commands(state: BatchState, commands, width):
@@ -558,14 +587,27 @@ def step_batch(state: BatchState, commands, *, pose_out=None) -> BatchState:
     rows p (3), q (4), nu (6) after the step and the call waits for them.
     """
     width = _cmd_width(state)
-    host = not torch.is_tensor(commands) or commands.device.type == "cpu"
-    if host or pose_out is not None:
+    if pose_out is not None or not isinstance(commands, torch.Tensor) or not commands.is_cuda:
         return _step_host(state, commands, width, pose_out)
     cmd = _commands(state, commands, width)
-    N.check(N.load().uuv_step(state._ctx, C.byref(state._cstate()), cmd.data_ptr(),
-                              cmd.stride(0), state.sim.substeps, state.sim.dt, state._stream()),
-            EngineError)
+    status = N.load().uuv_step(state._ctx, C.byref(state._cstate()), cmd.data_ptr(),
+                               cmd.stride(0), state.sim.substeps, state.sim.dt, state._stream())
+    if status:
+        N.check(status, EngineError)
     return state
+
+
+def _pinned_ok(state: BatchState, t, shape) -> bool:
+    """Pinned, contiguous, batch dtype and shape (cached per buffer address)."""
+    key = (t.data_ptr(), tuple(t.shape), t.dtype)
+    ok = state._pinned_cache.get(key)
+    if ok is None:
+        ok = (tuple(t.shape) == shape and t.dtype == state.dtype and t.is_contiguous()
+              and t.is_pinned())
+        if len(state._pinned_cache) > 64:
+            state._pinned_cache.clear()
+        state._pinned_cache[key] = ok
+    return ok
 
 
 def _step_host(state: BatchState, commands, width, pose_out):
@@ -574,40 +616,40 @@ def _step_host(state: BatchState, commands, width, pose_out):
     if st._pin is None:
         st._pin = torch.empty((n, width), dtype=st.dtype).pin_memory()
         st._dcmd = torch.empty((n, width), dtype=st.dtype, device=st.device)
-    if torch.is_tensor(commands):
-        if tuple(commands.shape) != (n, width):
-            raise EngineError(f"commands: expected shape {(n, width)}, got {tuple(commands.shape)}")
-        if commands.device.type == "cpu" and commands.is_pinned() and commands.dtype == st.dtype \
-                and commands.is_contiguous():
-            src = commands
-        elif commands.device.type == "cpu":
-            st._pin.copy_(commands)
-            src = st._pin
-        else:  # device commands with a host pose_out
-            src = None
+    src = None
+    if isinstance(commands, torch.Tensor):
+        if commands.device.type == "cpu":
+            if _pinned_ok(st, commands, (n, width)):
+                src = commands
+            else:
+                if tuple(commands.shape) != (n, width):
+                    raise EngineError(f"commands: expected shape {(n, width)}, "
+                                      f"got {tuple(commands.shape)}")
+                st._pin.copy_(commands)
+                src = st._pin
     else:
         arr = np.asarray(commands)
         if arr.shape != (n, width):
             raise EngineError(f"commands: expected shape {(n, width)}, got {arr.shape}")
         st._pin.numpy()[...] = arr
         src = st._pin
-    if pose_out is not None:
-        if (tuple(pose_out.shape) != (13, n) or pose_out.dtype != st.dtype
-                or not pose_out.is_pinned() or not pose_out.is_contiguous()):
-            raise EngineError(f"pose_out: expected a pinned contiguous ({13}, {n}) {st.dtype} tensor")
+    if pose_out is not None and not _pinned_ok(st, pose_out, (13, n)):
+        raise EngineError(f"pose_out: expected a pinned contiguous (13, {n}) {st.dtype} tensor")
     lib = N.load()
-    if src is None:
+    if src is None:  # device commands with a host pose_out
         cmd = _commands(state, commands, width)
         N.check(lib.uuv_step(st._ctx, C.byref(st._cstate()), cmd.data_ptr(), cmd.stride(0),
                              st.sim.substeps, st.sim.dt, st._stream()), EngineError)
         torch.cuda.current_stream(st.device).synchronize()
         pose_out.copy_(st._soa[:13, :n])
         return state
-    N.check(lib.uuv_step_host(st._ctx, C.byref(st._cstate()), src.data_ptr(), width,
-                              st._dcmd.data_ptr(),
-                              pose_out.data_ptr() if pose_out is not None else None,
-                              st.sim.substeps, st.sim.dt, st._stream(),
-                              1 if pose_out is not None or src is st._pin else 0), EngineError)
+    status = lib.uuv_step_host(st._ctx, C.byref(st._cstate()), src.data_ptr(), width,
+                               st._dcmd.data_ptr(),
+                               pose_out.data_ptr() if pose_out is not None else None,
+                               st.sim.substeps, st.sim.dt, st._stream(),
+                               1 if pose_out is not None or src is st._pin else 0)
+    if status:
+        N.check(status, EngineError)
     return state
 
 
@@ -645,6 +687,7 @@ def _device_reset(state: BatchState, m, sampler: DeviceSampler):
     state._note_sampler(sampler)
     rows_mask = m.to(torch.uint8)
     packed = sampler.pack()
+    packed.rng_mode = N.RNG_MODES[state.rng]
     if state._host_overlays:
         idx = torch.nonzero(m).flatten().cpu().tolist()
         for i in idx:
@@ -661,8 +704,8 @@ def _host_reset(state: BatchState, m, sampler):
     eps = state.episodes[torch.from_numpy(rows).to(state.device)].cpu().numpy().astype(np.int64) + 1
     inits = []
     for i, ep in zip(rows, eps):
-        init = sampler(int(i), int(ep), philox_generator(state.master_seed,
-                                                         state.env_offset + int(i), int(ep)))
+        init = sampler(int(i), int(ep), RNG_GENERATORS[state.rng](
+            state.master_seed, state.env_offset + int(i), int(ep)))
         ov = dict(init.overlay)
         if ov:
             validate_overlay(state.vehicles[0] if state._type is None else state.vehicle, ov)

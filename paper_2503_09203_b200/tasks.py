@@ -221,7 +221,7 @@ class VecTaskEnv:
     """Batched task environment over one engine batch (tasks/core.py:217-383)."""
 
     def __init__(self, task: TaskConfig, sim: SimConfig, dr=None, seed: int = 0, *,
-                 device=None, dtype=torch.float32, env_offset: int = 0):
+                 device=None, dtype=torch.float32, env_offset: int = 0, rng: str = "philox"):
         self.task = task
         self.sim = sim
         self.vehicle = load_vehicle(task.vehicle)
@@ -233,7 +233,8 @@ class VecTaskEnv:
                 raise TaskError(f"trajectory duration {task.trajectory.duration} s is shorter than "
                                 f"the episode horizon {horizon} s")
         self.state: BatchState = make_batch(self.vehicle, sim, master_seed=self.seed,
-                                            device=device, dtype=dtype, env_offset=env_offset)
+                                            device=device, dtype=dtype, env_offset=env_offset,
+                                            rng=rng)
         self.n_envs = sim.batch_size
         self.action_dim = self.vehicle.action_dim
         self.metric_name = _METRIC[task.task]
@@ -241,6 +242,7 @@ class VecTaskEnv:
         st = self.state
         self._sampler = spec_sampler(self._dr, start_box(task))
         self._sampler_c = self._sampler.pack()
+        self._sampler_c.rng_mode = _N.RNG_MODES[rng]
         st._note_sampler(self._sampler)
         ld, dev = st._ld, st.device
         self._prev_u = torch.zeros((self.action_dim, ld), dtype=dtype, device=dev)

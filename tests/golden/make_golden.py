@@ -40,7 +40,18 @@ def _philox_env_rng(self, i):
         counter=np.array([0, int(self.episodes[i]) & M64, 0, 0], dtype=np.uint64)))
 
 
+_REFERENCE_ENV_RNG = R_eng.BatchState.env_rng
 R_eng.BatchState.env_rng = _philox_env_rng  # the single hook
+
+
+class unhooked:
+    """Run the reference exactly as shipped (PCG64/SeedSequence streams)."""
+
+    def __enter__(self):
+        R_eng.BatchState.env_rng = _REFERENCE_ENV_RNG
+
+    def __exit__(self, *exc):
+        R_eng.BatchState.env_rng = _philox_env_rng
 
 
 def vehicle(name):
@@ -212,6 +223,14 @@ def main():
     save("task_station_fail", task_fixture(
         "station_keeping", "bluerov", "disturbed", n=6, steps=80, episode_length=60,
         cmd_fn=full_thrust, nu_max=0.4, bounds=3.0))
+    # the unmodified reference (no hook): PCG64(SeedSequence(seed, spawn_key=(i, ep)))
+    with unhooked():
+        save("engine_bluerov_pcg64", engine_fixture("bluerov"))
+        save("task_station_keeping_standard_pcg64",
+             task_fixture("station_keeping", "bluerov", "standard"))
+        save("task_tracking_disturbed_pcg64", task_fixture("tracking", "lauv", "disturbed"))
+        save("task_docking_disturbed_dr_pcg64",
+             task_fixture("docking", "bluerov_heavy", "disturbed_dr"))
     save("task_docking_contact", task_fixture(
         "docking", "bluerov_heavy", "standard", n=4, steps=160, episode_length=400,
         cmd_fn=descend, dock=DockSpec(centre=(0.0, 0.0, 3.0), radius=5.0)))

@@ -64,11 +64,11 @@ def prod_sampler(fn):
     return s
 
 
-def fixture_batch(g, name, dtype, sampler=samplers.rich):
+def fixture_batch(g, name, dtype, sampler=samplers.rich, rng="philox"):
     meta = json.loads(str(g["meta"]))
     veh = product_vehicle(name)
     st = E.make_batch(veh, E.SimConfig(batch_size=meta["n"], substeps=meta["substeps"]),
-                      master_seed=meta["seed"], dtype=dtype)
+                      master_seed=meta["seed"], dtype=dtype, rng=rng)
     E.reset_envs(st, np.ones(meta["n"], bool), prod_sampler(sampler))
     return st, meta
 
@@ -145,6 +145,44 @@ def test_engine_fixture_float32(name):
         prev = tuple(g[f"traj_{k}"][t] for k in ("p", "q", "nu", "act"))
 
 
+def test_unhooked_reference_engine_fixture_pcg64():
+    """rng="pcg64": host-sampler resets draw the unmodified reference's streams."""
+    g = golden("engine_bluerov_pcg64")
+    st, meta = fixture_batch(g, "bluerov", torch.float64, rng="pcg64")
+    for k, arr in (("p0", st.p), ("q0", st.q), ("nu0", st.nu), ("current0", st.current_ned)):
+        assert np.array_equal(host(arr), g[k]), k
+    prev = (g["p0"], g["q0"], g["nu0"], g["act0"])
+    for t in range(g["cmds"].shape[0]):
+        set_state(st, *prev)
+        E.step_batch(st, g["cmds"][t])
+        ok, err = rowwise_close(host(st.nu), g["traj_nu"][t], F64_RTOL, atol=1e-300)
+        assert ok, (t, err)
+        prev = tuple(g[f"traj_{k}"][t] for k in ("p", "q", "nu", "act"))
+
+
+def test_device_pcg64_reset_matches_reference_streams():
+    """The device PCG64/SeedSequence restatement == numpy's, draw for draw."""
+    from paper_2503_09203_b200.tasks import disturbed_spec
+
+    task = TaskConfig(task="station_keeping", vehicle="bluerov", level="disturbed_dr")
+    n = 300
+    env = make_env(task, E.SimConfig(batch_size=n), seed=2**40 + 17, dtype=torch.float64,
+                   rng="pcg64")
+    env.reset()
+    oe = O.TaskEnv(task, product_vehicle("bluerov"), n, seed=2**40 + 17,
+                   disturbed_spec=disturbed_spec(), train_spec=preset("train"), rng="pcg64")
+    oe.reset()
+    assert np.array_equal(host(env.state.p), oe.batch.p)
+    assert np.array_equal(host(env.state.nu), oe.batch.nu)
+    assert env.state.overlays == oe.batch.overlays
+    for _ in range(3):  # later episodes (spawn_key episode > 0)
+        mask = np.random.default_rng(0).random(n) < 0.5
+        env.reset(mask)
+        oe.reset(mask)
+        assert np.array_equal(host(env.state.p), oe.batch.p)
+        assert env.state.overlays == oe.batch.overlays
+
+
 def test_mount_jitter_matrix_float64():
     g = golden("engine_jitter_hauv")
     veh = product_vehicle("hauv")
@@ -216,10 +254,16 @@ def test_neutral_vehicle_holds_station(dtype):
 
 TASK_FIXTURES = [f"task_{k}_{lv}" for k in ("station_keeping", "tracking", "docking")
                  for lv in ("standard", "disturbed", "disturbed_dr")] + [
-    "task_tracking_k8_hauv", "task_station_iauv_dr", "task_station_fail", "task_docking_contact"]
+    "task_tracking_k8_hauv", "task_station_iauv_dr", "task_station_fail", "task_docking_contact",
+    "task_station_keeping_standard_pcg64", "task_tracking_disturbed_pcg64",
+    "task_docking_disturbed_dr_pcg64"]
 
 
-def product_env(meta, dtype):
+def fixture_rng(name):
+    return "pcg64" if name.endswith("_pcg64") else "philox"
+
+
+def product_env(meta, dtype, rng="philox"):
     kw = dict(meta["task_kw"])
     if "dock" in kw:
         c = kw["dock"]
@@ -227,7 +271,7 @@ def product_env(meta, dtype):
     task = TaskConfig(task=meta["kind"], vehicle=meta["vehicle"], level=meta["level"],
                       episode_length=meta["episode_length"], **kw)
     return make_env(task, E.SimConfig(batch_size=meta["n"], substeps=meta["substeps"]),
-                    seed=meta["seed"], dtype=dtype)
+                    seed=meta["seed"], dtype=dtype, rng=rng)
 
 
 FLAG_KEYS = ("terminated", "truncated", "finished", "failure", "success", "diverged", "contact")
@@ -237,7 +281,7 @@ FLAG_KEYS = ("terminated", "truncated", "finished", "failure", "success", "diver
 def test_task_fixture_float64(name):
     g = golden(name)
     meta = json.loads(str(g["meta"]))
-    env = product_env(meta, torch.float64)
+    env = product_env(meta, torch.float64, fixture_rng(name))
     obs = env.reset()
     ok, err = rowwise_close(host(obs), g["obs0"], F64_RTOL, 1e-15)
     assert ok, ("obs0", err)
@@ -278,7 +322,7 @@ def test_task_fixture_float32_flags(name):
     """float32 build: termination/truncation/reset indices equal the reference's."""
     g = golden(name)
     meta = json.loads(str(g["meta"]))
-    env = product_env(meta, torch.float32)
+    env = product_env(meta, torch.float32, fixture_rng(name))
     env.reset()
     for t in range(g["cmds"].shape[0]):
         o, r, te, tr, info = env.step(g["cmds"][t])
