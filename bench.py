@@ -55,6 +55,16 @@ def dr_spec():
     return {k: DRParameter(k, Uniform(0.8, 1.2)) for k in DR_KEYS}
 
 
+def load_traffic():
+    """DRAM bytes per launch of the step kernel from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json")) as f:
+            t = json.load(f)
+        return t["dram_bytes_read"] + t["dram_bytes_write"]
+    except Exception:
+        return None
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -300,7 +310,9 @@ def run_b200(args, rank, world, local_rank):
             "e2e": {"value": world * n * k_total / e2e_el, "unit": "env-frames/s",
                     "h2d_bytes_per_step": n * A_BLUEROV * 4, "d2h_bytes_per_step": n * 13 * 4},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak,
+                         "traffic": load_traffic(),
+                         "traffic_note": "ncu dram bytes per launch (cold cache), profiles/r01",
                          "peak_source": peak_kind,
                          "bytes_per_frame": bpf, "kernel": "k_step<float,1,DR=true>"},
             "gpu_launches": k_total,
