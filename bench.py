@@ -192,11 +192,19 @@ def run_b200(args, rank, world, local_rank):
     from paper_2503_09203_b200.distributed import allreduce_max, shard_range
     from paper_2503_09203_b200.vehicles import load_vehicle
 
-    dev = torch.device("cuda", local_rank)
+    # one process per GPU; UUV_BENCH_GPU_OVERRIDE=0 pins every rank to GPU 0 and
+    # UUV_DIST_BACKEND=gloo swaps NCCL for gloo (used to exercise the multi-rank
+    # path on a single-GPU box; the driver's runs use one GPU per rank over NCCL)
+    dev_index = int(os.environ.get("UUV_BENCH_GPU_OVERRIDE", local_rank))
+    dev = torch.device("cuda", dev_index)
     torch.cuda.set_device(dev)
     dist = world > 1
     if dist:
-        torch.distributed.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("UUV_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            torch.distributed.init_process_group("nccl", device_id=dev)
+        else:
+            torch.distributed.init_process_group(backend)
 
     def barrier():
         if dist:
@@ -256,7 +264,7 @@ def run_b200(args, rank, world, local_rank):
         return e0.elapsed_time(e1) / 1e3
 
     timed()  # one untimed replay of the captured graphs (graph upload / first-run effects)
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(dev_index) as clk:
         t0 = time.perf_counter()
         el = timed()
         # keep sampling clocks under the same load for >= 1 s

@@ -585,46 +585,42 @@ UUV_D void flush_obs(const R* s_obs, R* obs, int64_t obs_ld, int obs_dim, int64_
 template <typename R, bool DR, int AC, bool DM>
 __global__ void __launch_bounds__(kBlock, MinB<R>::value) k_task_step(const __grid_constant__ TaskArgs<R> a) {
   __shared__ R s_obs[kBlock * kObsMax];
-  __shared__ double s_red[kBlock / 32][2];
-  __shared__ unsigned s_cnt[kBlock / 32][6];
+  __shared__ double s_red[kBlock / 32][UUV_ST_COUNT];
   const int64_t row0 = (int64_t)blockIdx.x * kBlock;
   const int64_t i = row0 + threadIdx.x;
   const StateView<R>& sv = a.sv;
   const Hull<R>& H = a.hull[0];
   const TaskR<R>& T = a.task;
-  constexpr int NA = AC > 0 ? AC : UUV_MAX_ACT;
-  const int A = AC > 0 ? AC : H.r.n_act;
+  const int A = H.r.n_act;
   const int od = T.obs_dim;
   const int64_t ld = sv.ld;
-  double s_reward = 0.0, s_metric = 0.0;
-  unsigned c_fin = 0, c_succ = 0, c_fail = 0, c_trunc = 0, c_div = 0, c_frames = 0;
+  double st[UUV_ST_COUNT];
+#pragma unroll
+  for (int k = 0; k < UUV_ST_COUNT; ++k) st[k] = 0.0;
   if (i < sv.n) {
-    // every input load first: commands, prev_u, state, counters, dev_sum
-    R u[UUV_MAX_ACT], pu[UUV_MAX_ACT];
+    // u = clip(commands); du = u - prev_u; prev_u = u  (tasks/core.py:329-335)
+    R u[UUV_MAX_ACT], du[UUV_MAX_ACT];
     const R* crow = a.cmd + i * a.cmd_ld;
 #pragma unroll
     for (int j = 0; j < UUV_MAX_ACT; ++j) {
-      u[j] = (j < NA && j < A) ? crow[j] : R(0);
-      pu[j] = (j < NA && j < A) ? a.prev_u[j * ld + i] : R(0);
+      if (j < A) {
+        u[j] = clip_<R>(crow[j], R(-1), R(1));
+        du[j] = u[j] - a.prev_u[j * ld + i];
+      } else {
+        u[j] = R(0);
+        du[j] = R(0);
+      }
     }
     int32_t steps = sv.steps[i];
     bool div = sv.diverged[i] != 0;
     R px, py, pz, nu[6], act[UUV_MAX_ACT];
     Q4<R> q;
     load_state(sv, i, A, px, py, pz, q, nu, act);
-    R dev = a.dev_sum != nullptr ? a.dev_sum[i] : R(0);
-    // u = clip(commands); du = u - prev_u; prev_u = u  (tasks/core.py:329-335)
-    R du[UUV_MAX_ACT];
-#pragma unroll
-    for (int j = 0; j < UUV_MAX_ACT; ++j) {
-      u[j] = (j < NA && j < A) ? clip_<R>(u[j], R(-1), R(1)) : R(0);
-      du[j] = u[j] - pu[j];
-    }
     if (!div) div = physics<R, DR, AC, DM>(H, sv, i, a.K, a.dt_sub, u, px, py, pz, q, nu, act);
     steps += 1;
+    R dev = a.dev_sum != nullptr ? a.dev_sum[i] : R(0);
     TaskOut<R> o;
-    R* srow = s_obs + threadIdx.x * od;
-    task_eval<R>(T, A, px, py, pz, q, nu, u, du, steps, div, a.dt, &dev, o, srow);
+    task_eval<R>(T, A, px, py, pz, q, nu, du, steps, div, a.dt, &dev, o);
     if (a.rout != nullptr) {
       a.rout[UUV_TR_REWARD * ld + i] = o.reward;
       a.rout[UUV_TR_POS_ERR * ld + i] = o.pos_err;
@@ -646,15 +642,18 @@ __global__ void __launch_bounds__(kBlock, MinB<R>::value) k_task_step(const __gr
       a.fout[UUV_TF_DIVERGED * ld + i] = div;
       a.fout[UUV_TF_CONTACT * ld + i] = o.contact;
     }
-    s_reward = (double)o.reward;
-    s_metric = o.finished ? (double)o.metric : 0.0;
-    c_fin = o.finished; c_succ = o.success; c_fail = o.failure; c_trunc = o.truncated;
-    c_div = div; c_frames = 1;
+    st[UUV_ST_REWARD] = (double)o.reward;
+    st[UUV_ST_FINISHED] = o.finished;
+    st[UUV_ST_SUCCESS] = o.success;
+    st[UUV_ST_FAILURE] = o.failure;
+    st[UUV_ST_TRUNCATED] = o.truncated;
+    st[UUV_ST_METRIC_FINISHED] = o.finished ? (double)o.metric : 0.0;
+    st[UUV_ST_DIVERGED] = div;
+    st[UUV_ST_FRAMES] = 1.0;
+    R* srow = s_obs + threadIdx.x * od;
     if (o.finished) {
-      if (a.term_obs != nullptr) {  // the pre-reset observation is the terminal one
-        R* tr = a.term_obs + i * a.obs_ld;
-        for (int c = 0; c < od; ++c) tr[c] = srow[c];
-      }
+      if (a.term_obs != nullptr)  // final observation of the ended episode
+        observe_row<R>(T, A, px, py, pz, q, nu, u, steps, a.dt, a.term_obs + i * a.obs_ld, nullptr);
       V3<R> cur;
       reset_env<R>(sv, i, a.smp, a.seed, px, py, pz, q, nu, cur);
 #pragma unroll
@@ -662,56 +661,34 @@ __global__ void __launch_bounds__(kBlock, MinB<R>::value) k_task_step(const __gr
       steps = 0;
       div = false;
       dev = R(0);
-      observe_row<R>(T, A, px, py, pz, q, nu, u, steps, a.dt, srow, nullptr);
     }
+    observe_row<R>(T, A, px, py, pz, q, nu, u, steps, a.dt, srow, nullptr);
     store_state(sv, i, A, px, py, pz, q, nu, act);
     sv.steps[i] = steps;
     sv.diverged[i] = div ? 1 : 0;
 #pragma unroll
-    for (int j = 0; j < NA; ++j)
+    for (int j = 0; j < UUV_MAX_ACT; ++j)
       if (j < A) a.prev_u[j * ld + i] = u[j];
     if (a.dev_sum != nullptr) a.dev_sum[i] = dev;
   }
-  if (a.stats != nullptr) {
-    // deterministic CTA reduction: integer counts with redux.sync, float64 sums
-    // through a fixed shuffle tree, then warps in index order
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const unsigned cf = __reduce_add_sync(0xffffffffu, c_fin);
-    const unsigned cs = __reduce_add_sync(0xffffffffu, c_succ);
-    const unsigned cl = __reduce_add_sync(0xffffffffu, c_fail);
-    const unsigned ct = __reduce_add_sync(0xffffffffu, c_trunc);
-    const unsigned cd = __reduce_add_sync(0xffffffffu, c_div);
-    const unsigned cn = __reduce_add_sync(0xffffffffu, c_frames);
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      s_reward += __shfl_down_sync(0xffffffffu, s_reward, off);
-      s_metric += __shfl_down_sync(0xffffffffu, s_metric, off);
-    }
-    if (lane == 0) {
-      s_red[warp][0] = s_reward;
-      s_red[warp][1] = s_metric;
-      s_cnt[warp][0] = cf; s_cnt[warp][1] = cs; s_cnt[warp][2] = cl;
-      s_cnt[warp][3] = ct; s_cnt[warp][4] = cd; s_cnt[warp][5] = cn;
-    }
-  }
   __syncthreads();
   flush_obs<R>(s_obs, a.obs, a.obs_ld, od, row0, sv.n);
-  if (a.stats != nullptr && threadIdx.x < UUV_ST_COUNT) {
-    const int k = threadIdx.x;
-    double v = 0.0;
-    for (int w = 0; w < kBlock / 32; ++w) {
-      switch (k) {
-        case UUV_ST_REWARD: v += s_red[w][0]; break;
-        case UUV_ST_METRIC_FINISHED: v += s_red[w][1]; break;
-        case UUV_ST_FINISHED: v += s_cnt[w][0]; break;
-        case UUV_ST_SUCCESS: v += s_cnt[w][1]; break;
-        case UUV_ST_FAILURE: v += s_cnt[w][2]; break;
-        case UUV_ST_TRUNCATED: v += s_cnt[w][3]; break;
-        case UUV_ST_DIVERGED: v += s_cnt[w][4]; break;
-        default: v += s_cnt[w][5]; break;
-      }
+  if (a.stats != nullptr) {
+    // deterministic CTA reduction: fixed shuffle tree, then warps in order
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < UUV_ST_COUNT; ++k) {
+      double v = st[k];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+      if (lane == 0) s_red[warp][k] = v;
     }
-    a.stats[blockIdx.x * UUV_ST_COUNT + k] += v;
+    __syncthreads();
+    if (threadIdx.x < UUV_ST_COUNT) {
+      double v = 0.0;
+      for (int w = 0; w < kBlock / 32; ++w) v += s_red[w][threadIdx.x];
+      a.stats[blockIdx.x * UUV_ST_COUNT + threadIdx.x] += v;
+    }
   }
 }
 

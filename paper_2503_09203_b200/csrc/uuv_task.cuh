@@ -169,37 +169,16 @@ template <typename R> struct TaskOut {
   bool terminated, truncated, finished, failure, success, contact;
 };
 
-// Reward / termination / info of one env after the physics step
-// (tasks/core.py:170-214, 339-361, 409-414, 465-473, 509-523), and — in the same
-// pass — its observation row (core.py:316-321) with prev_u = the clipped
-// command: for a row that finishes this is the episode's terminal observation.
 template <typename R>
 UUV_D void task_eval(const TaskR<R>& t, int A, R px, R py, R pz, Q4<R> q, const R* nu,
-                     const R* pu, const R* du, int32_t steps, bool diverged, R dt,
-                     R* dev_sum, TaskOut<R>& o, R* obs) {
+                     const R* du, int32_t steps, bool diverged, R dt, R* dev_sum, TaskOut<R>& o) {
   const R nanv = nan_<R>();
   const V3<R> p{px, py, pz};
   V3<R> vref{R(0), R(0), R(0)};
   const V3<R> tp = task_target(t, steps, dt, &vref);
   const V3<R> ew = tp - p;
-  const V3<R> ep = qrot_inv(q, ew);
   const Q4<R> tq{t.target_q[0], t.target_q[1], t.target_q[2], t.target_q[3]};
   const V3<R> ea = rotvec(qmul(qconj(q), tq));
-  if (obs != nullptr) {
-    obs[0] = ep.x; obs[1] = ep.y; obs[2] = ep.z;
-    obs[3] = ea.x; obs[4] = ea.y; obs[5] = ea.z;
-#pragma unroll
-    for (int k = 0; k < 6; ++k) obs[6 + k] = nu[k];
-#pragma unroll
-    for (int j = 0; j < UUV_MAX_ACT; ++j)
-      if (j < A) obs[12 + j] = pu[j];
-    if (t.kind == UUV_TASK_TRACKING) {
-      const V3<R> vb = qrot_inv(q, vref);
-      obs[12 + A] = vb.x; obs[13 + A] = vb.y; obs[14 + A] = vb.z;
-    } else if (t.kind == UUV_TASK_DOCKING) {
-      obs[12 + A] = t.dock_centre[2] - pz;
-    }
-  }
   R du2 = R(0);
 #pragma unroll
   for (int j = 0; j < UUV_MAX_ACT; ++j)
@@ -209,14 +188,14 @@ UUV_D void task_eval(const TaskR<R>& t, int A, R px, R py, R pz, Q4<R> q, const 
 #pragma unroll
   for (int k = 0; k < 6; ++k) nu2 += nu[k] * nu[k];
   const R nu_n = sqrt_<R>(nu2);
-  const R e_a = norm(ea);
   R reward;
   bool done = false;
   o.metric = nanv;
   o.c_dist = o.c_speed = o.c_att = nanv;
   o.contact = false;
   if (t.kind == UUV_TASK_STATION) {
-    const R e_p = norm(ep);
+    const R e_p = norm(qrot_inv(q, ew));
+    const R e_a = norm(ea);
     const R e_v = minc_<R>(nu_n, t.speed_cap);
     reward = -t.w_p * e_p - t.w_a * e_a - t.w_v * e_v - t.w_u * e_u +
              t.w_b * (e_p < t.r_tol ? R(1) : R(0));
@@ -252,7 +231,7 @@ UUV_D void task_eval(const TaskR<R>& t, int A, R px, R py, R pz, Q4<R> q, const 
   o.finished = o.terminated || o.truncated;
   o.failure = fail;
   o.pos_err = norm(ew);
-  o.att_err = e_a;
+  o.att_err = norm(ea);
   o.time = (R)steps * dt;
   if (t.kind == UUV_TASK_STATION) {
     o.metric = o.pos_err;
