@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define UUV_ABI_VERSION 1
+#define UUV_ABI_VERSION 2
 #define UUV_MAX_ACT 8        /* actuator columns per vehicle type             */
 #define UUV_MAX_TYPES 6      /* vehicle types in one batch (mixed fleets)     */
 #define UUV_MLP_MAX_PARAMS 128 /* packed weights+biases of one rotor network  */
@@ -145,8 +145,10 @@ typedef struct {
 /* uuv_state.flags */
 enum { UUV_STATE_PAYLOAD_AT_ORIGIN = 1 /* every env's payload_position (if any) is 0 */ };
 
-/* One draw of a DR key (randomization.py:48-117): uniform or piecewise. */
-enum { UUV_DIST_UNIFORM = 0, UUV_DIST_PIECEWISE = 1 };
+/* One draw of a DR key (randomization.py:48-117).  Gaussian draws are
+ * clip(mu + sigma * z, lo, hi) with z from numpy's random_standard_normal
+ * ziggurat, restated bit for bit (csrc/uuv_ziggurat.cuh). */
+enum { UUV_DIST_UNIFORM = 0, UUV_DIST_PIECEWISE = 1, UUV_DIST_GAUSSIAN = 2 };
 typedef struct {
   int32_t key;             /* UUV_OV_* (overlay draws) */
   int32_t dist;
@@ -154,7 +156,8 @@ typedef struct {
   int32_t pw_bins;         /* piecewise: K bins        */
   int32_t pw_offset;       /* into pw_table: K+1 breakpoints then K cdf values */
   int32_t pad_;
-  double lo, hi;
+  double lo, hi;           /* uniform bounds; gaussian clip interval */
+  double mu, sigma;        /* gaussian                               */
 } uuv_draw;
 
 enum { UUV_START_IDENTITY = 0, UUV_START_BOX = 1 };

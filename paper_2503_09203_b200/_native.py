@@ -35,7 +35,8 @@ OV_WIDTH["payload_position"] = 3
 OV_WIDTH["mount_position_jitter"] = 3 * MAX_ACT
 OV_IDENTITY = {k: (1.0 if i <= OV_INDEX["thrust_coeff*"] else 0.0) for i, k in enumerate(OV_KEYS)}
 
-DIST_UNIFORM, DIST_PIECEWISE = 0, 1
+ABI_VERSION = 2
+DIST_UNIFORM, DIST_PIECEWISE, DIST_GAUSSIAN = 0, 1, 2
 START_IDENTITY, START_BOX = 0, 1
 CURRENT_NONE, CURRENT_RANDOM_HEADING, CURRENT_HEADING_DRAW = 0, 1, 2
 TASK_STATION, TASK_TRACKING, TASK_DOCKING = 0, 1, 2
@@ -86,7 +87,7 @@ class State(C.Structure):
 class Draw(C.Structure):
     _fields_ = [("key", C.c_int32), ("dist", C.c_int32), ("n_draws", C.c_int32),
                 ("pw_bins", C.c_int32), ("pw_offset", C.c_int32), ("pad_", C.c_int32),
-                ("lo", C.c_double), ("hi", C.c_double)]
+                ("lo", C.c_double), ("hi", C.c_double), ("mu", C.c_double), ("sigma", C.c_double)]
 
 
 class Sampler(C.Structure):
@@ -173,6 +174,9 @@ def load():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    if lib.uuv_abi_version() != ABI_VERSION:
+        raise NativeError(f"ABI mismatch: library version {lib.uuv_abi_version()} != "
+                          f"binding {ABI_VERSION}; rebuild with `make`")
     sizes = (C.c_int64 * 5)()
     lib.uuv_abi_sizes(sizes)
     want = [C.sizeof(Hull), C.sizeof(State), C.sizeof(Sampler), C.sizeof(Task), C.sizeof(TaskIO)]

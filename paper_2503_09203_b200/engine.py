@@ -31,7 +31,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .randomization import CURRENT_KEYS, Piecewise, Uniform
+from .randomization import CURRENT_KEYS, Gaussian, Piecewise, Uniform
 from .vehicles import (
     DATA_DRIVEN, FIRST_ORDER, KIND_CODE, MODEL_CODE, RUDDER, TILTROTOR, VehicleConfig,
     fin_basis, tilt_rotation, validate_overlay,
@@ -217,6 +217,9 @@ class DeviceSampler:
                 d.pw_bins = dist.densities.size
                 d.pw_offset = len(pw)
                 pw.extend(list(dist.breakpoints) + list(dist._cdf))
+            elif isinstance(dist, Gaussian):
+                d.dist, d.mu, d.sigma = N.DIST_GAUSSIAN, dist.mu, dist.sigma
+                d.lo, d.hi = dist.clip
             else:
                 raise EngineError(f"{type(dist).__name__} distributions are sampled by the "
                                   "host reset path, not the device sampler")

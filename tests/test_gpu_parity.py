@@ -447,3 +447,63 @@ def test_large_fleet_properties():
         assert torch.equal(getattr(a, k), getattr(b, k)), k
     qn = a.q.double().norm(dim=1)
     assert (qn - 1).abs().max().item() < 1e-6
+
+
+def _gaussian_spec():
+    from paper_2503_09203_b200.randomization import DRParameter, Gaussian, Uniform
+
+    G = lambda k, mu, s, lo, hi: DRParameter(k, Gaussian(mu, s, (lo, hi)))  # noqa: E731
+    return {"mass*": G("mass*", 1.0, 0.1, 0.2, 1.8),       # wide clip: tail draws survive
+            "damping*": G("damping*", 1.0, 0.3, 0.9, 1.1),  # narrow clip: clipping exercised
+            "volume*": DRParameter("volume*", Uniform(0.95, 1.05)),
+            "added_mass*": G("added_mass*", 1.0, 0.0, 0.5, 1.5),  # sigma 0 still draws
+            "payload_mass*": G("payload_mass*", 0.5, 0.2, 0.0, 1.0),
+            "payload_position": G("payload_position", 0.0, 0.05, -0.1, 0.1),  # vector key
+            "current_velocity": G("current_velocity", 0.3, 0.1, 0.0, 0.6),
+            "current_direction": G("current_direction", 0.0, 1.0, -3.0, 3.0)}
+
+
+@pytest.mark.parametrize("rng", ["philox", "pcg64"])
+def test_device_gaussian_dr_matches_numpy_draws(rng):
+    """Gaussian keys on the device == clip(rng.normal(...)) on numpy's stream, bit for bit."""
+    spec = _gaussian_spec()
+    dyn = {k: v for k, v in spec.items() if not k.startswith("current")}
+    cur = {k: v for k, v in spec.items() if k.startswith("current")}
+    n = 50_000 if rng == "philox" else 4_000
+    veh = product_vehicle("bluerov_heavy")
+    st = E.make_batch(veh, E.SimConfig(batch_size=n), master_seed=31, dtype=torch.float64, rng=rng)
+    E.reset_envs(st, np.ones(n, bool), E.spec_sampler(spec))
+    got = st.overlays
+    cur_dev = host(st.current_ned)
+    stream = O.STREAMS[rng]
+    for i in range(n):
+        g = stream(31, i, 0)
+        want = O.draw_overlay(dyn, g)
+        c = O.draw_current(cur, g)
+        assert set(got[i]) == set(want), i
+        for k, v in want.items():
+            assert np.array_equal(np.asarray(got[i][k]).view(np.uint64),
+                                  np.asarray(v).view(np.uint64)), (i, k, got[i][k], v)
+        ok, err = rowwise_close(cur_dev[i:i + 1], c[None], 1e-15, 1e-17)
+        assert ok, (i, err)
+    # derived rows follow the reference's overlay math on the drawn values
+    if rng == "pcg64":
+        ob = O.Batch(veh, 64, seed=31, rng=rng)
+        ob.reset(np.ones(64, bool), lambda i, ep, r: O.Init(overlay=O.draw_overlay(dyn, r)))
+        for k in ("mass", "volume", "r_g"):
+            assert np.array_equal(host(getattr(st.params, k))[:64], ob.P[k]), k
+        ok, err = rowwise_close(host(st.params.M_inv)[:64], ob.P["M_inv"], F64_RTOL)
+        assert ok, err
+
+
+def test_gaussian_dr_task_env_runs_fp32():
+    """make_env with a Gaussian DR spec resets and steps on the device (float32)."""
+    spec = _gaussian_spec()
+    task = TaskConfig(task="docking", vehicle="bluerov_heavy", level="disturbed_dr")
+    env = make_env(task, E.SimConfig(batch_size=8192), dr=spec, seed=4)
+    obs = env.reset()
+    for _ in range(20):
+        obs, rew, term, trunc, info = env.step(torch.rand((8192, 8), device="cuda") * 2 - 1)
+    assert torch.isfinite(obs).all() and torch.isfinite(rew).all()
+    m = np.array([o["mass*"] for o in env.state.overlays[:2000]])
+    assert m.min() >= 0.2 and m.max() <= 1.8 and abs(m.mean() - 1.0) < 0.02
