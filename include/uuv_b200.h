@@ -227,7 +227,17 @@ typedef struct {
   void* real_out;          /* [UUV_TR_COUNT][ld] or NULL (reset/observe)      */
   uint8_t* flag_out;       /* [UUV_TF_COUNT][ld] or NULL                      */
   double* stats;           /* [n_blocks][UUV_ST_COUNT] running sums or NULL   */
+  void* trace;             /* [UUV_TRACE_COUNT + a_max][trace_ld] or NULL     */
+  int64_t trace_ld;
 } uuv_task_io;
+
+/* Per-step trajectory record written by uuv_task_step when uuv_task_io.trace
+ * is set (batch dtype, SoA rows): the post-step, post-auto-reset pose and
+ * velocity, the reward, t = steps * dt and the raw (unclipped) command -- the
+ * fields of the reference's rollout records (cli.py:261-303).  Rows
+ * UUV_TRACE_CMD .. UUV_TRACE_CMD + a_max - 1 hold the command. */
+enum { UUV_TRACE_P = 0, UUV_TRACE_Q = 3, UUV_TRACE_NU = 7, UUV_TRACE_REWARD = 13,
+       UUV_TRACE_T = 14, UUV_TRACE_CMD = 15, UUV_TRACE_COUNT = 15 };
 
 typedef struct uuv_ctx uuv_ctx;
 

@@ -46,6 +46,8 @@ RNG_PHILOX, RNG_PCG64 = 0, 1
 RNG_MODES = {"philox": RNG_PHILOX, "pcg64": RNG_PCG64}
 TR_NAMES = ("reward", "position_error", "attitude_error", "metric", "time", "contact_distance",
             "contact_speed", "contact_attitude")
+# uuv_task_io.trace rows (UUV_TRACE_*): p(3) q(4) nu(6) reward t, then the command
+TRACE_P, TRACE_Q, TRACE_NU, TRACE_REWARD, TRACE_T, TRACE_CMD = 0, 3, 7, 13, 14, 15
 TF_NAMES = ("terminated", "truncated", "finished", "failure", "success", "diverged", "contact")
 ST_NAMES = ("reward_sum", "finished", "success", "failure", "truncated", "metric_sum_finished",
             "diverged", "frames")
@@ -122,7 +124,8 @@ class Task(C.Structure):
 class TaskIO(C.Structure):
     _fields_ = [("prev_u", C.c_void_p), ("dev_sum", C.c_void_p), ("obs", C.c_void_p),
                 ("obs_ld", C.c_int64), ("term_obs", C.c_void_p), ("real_out", C.c_void_p),
-                ("flag_out", C.c_void_p), ("stats", C.c_void_p)]
+                ("flag_out", C.c_void_p), ("stats", C.c_void_p), ("trace", C.c_void_p),
+                ("trace_ld", C.c_int64)]
 
 
 EXPORTS = {

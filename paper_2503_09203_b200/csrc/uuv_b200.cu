@@ -559,6 +559,7 @@ template <typename R> struct TaskArgs {
   int32_t K;
   R dt_sub;
   R dt;  // control dt (time / tracking reference)
+  double dt64;
   R* prev_u;
   R* dev_sum;
   R* obs;
@@ -567,6 +568,8 @@ template <typename R> struct TaskArgs {
   R* rout;
   uint8_t* fout;
   double* stats;
+  R* trace;
+  int64_t trace_ld;
   const uint8_t* mask;  // task reset only
   int32_t mode;         // task reset kernel: 0 observe only, 1 reset masked then observe
 };
@@ -670,6 +673,22 @@ __global__ void __launch_bounds__(kBlock, MinB<R>::value) k_task_step(const __gr
     for (int j = 0; j < UUV_MAX_ACT; ++j)
       if (j < A) a.prev_u[j * ld + i] = u[j];
     if (a.dev_sum != nullptr) a.dev_sum[i] = dev;
+    if (a.trace != nullptr) {  // rollout record (cli.py:277-287), coalesced SoA rows
+      R* tr = a.trace + i;
+      const int64_t tl = a.trace_ld;
+      tr[(UUV_TRACE_P + 0) * tl] = px;
+      tr[(UUV_TRACE_P + 1) * tl] = py;
+      tr[(UUV_TRACE_P + 2) * tl] = pz;
+      tr[(UUV_TRACE_Q + 0) * tl] = q.w;
+      tr[(UUV_TRACE_Q + 1) * tl] = q.x;
+      tr[(UUV_TRACE_Q + 2) * tl] = q.y;
+      tr[(UUV_TRACE_Q + 3) * tl] = q.z;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) tr[(UUV_TRACE_NU + k) * tl] = nu[k];
+      tr[UUV_TRACE_REWARD * tl] = o.reward;
+      tr[UUV_TRACE_T * tl] = (R)(__dmul_rn((double)steps, a.dt64));
+      for (int j = 0; j < A; ++j) tr[(UUV_TRACE_CMD + j) * tl] = crow[j];
+    }
   }
   __syncthreads();
   flush_obs<R>(s_obs, a.obs, a.obs_ld, od, row0, sv.n);
@@ -1141,6 +1160,10 @@ uuv_status check_sampler(const uuv_sampler* smp) {
     const uuv_draw& dr = smp->overlay[d];
     if (dr.key < 0 || dr.key >= UUV_OV_COUNT) return fail(UUV_ERR_ARG, "sampler: bad key");
     if (dr.n_draws != 1 && dr.n_draws != 3) return fail(UUV_ERR_ARG, "sampler: bad n_draws");
+    if (dr.dist < UUV_DIST_UNIFORM || dr.dist > UUV_DIST_GAUSSIAN)
+      return fail(UUV_ERR_ARG, "sampler: bad distribution");
+    if (dr.dist == UUV_DIST_GAUSSIAN && !(dr.sigma >= 0.0 && dr.lo <= dr.hi))
+      return fail(UUV_ERR_ARG, "sampler: gaussian needs sigma >= 0 and lo <= hi");
     if (dr.dist == UUV_DIST_PIECEWISE &&
         (dr.pw_bins < 1 || dr.pw_offset < 0 || dr.pw_offset + 2 * dr.pw_bins + 1 > UUV_PW_MAX))
       return fail(UUV_ERR_ARG, "sampler: piecewise table out of range");
@@ -1161,6 +1184,7 @@ void fill_task_args(const uuv_ctx* ctx, const uuv_state* st, const uuv_task* tas
   a.K = K;
   a.dt_sub = (R)(dt / K);
   a.dt = (R)dt;
+  a.dt64 = dt;
   a.prev_u = (R*)io->prev_u;
   a.dev_sum = (R*)io->dev_sum;
   a.obs = (R*)io->obs;
@@ -1169,6 +1193,8 @@ void fill_task_args(const uuv_ctx* ctx, const uuv_state* st, const uuv_task* tas
   a.rout = (R*)io->real_out;
   a.fout = io->flag_out;
   a.stats = io->stats;
+  a.trace = (R*)io->trace;
+  a.trace_ld = io->trace_ld;
   a.mask = nullptr;
   a.mode = 0;
   a.cmd = nullptr;

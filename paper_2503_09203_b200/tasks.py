@@ -250,6 +250,7 @@ class VecTaskEnv:
         self._stats = torch.zeros((_N.load().uuv_stats_blocks(self.n_envs), len(_N.ST_NAMES)),
                                   dtype=torch.float64, device=dev)
         self._task_c = self._pack_task()
+        self._recorder = None
 
     # -------------------------------------------------------------- layout
     @property
@@ -327,6 +328,8 @@ class VecTaskEnv:
         io.real_out = rout.data_ptr() if rout is not None else None
         io.flag_out = fout.data_ptr() if fout is not None else None
         io.stats = self._stats.data_ptr() if stats else None
+        if rout is not None and self._recorder is not None:
+            io.trace, io.trace_ld = self._recorder._next_slot()
         return io
 
     def _new_obs(self):
@@ -355,6 +358,31 @@ class VecTaskEnv:
                                     _C.byref(self._io(obs, stats=False)), st._stream()),
                  TaskError)
         return obs
+
+    @property
+    def dr(self):
+        """The DR spec later resets draw from (None at level 'standard')."""
+        return self._dr
+
+    def set_dr(self, dr) -> None:
+        """Swap the DR spec drawn by every later reset and auto-reset.
+
+        For curriculum schedules (randomization.py:238-287): call
+        ``env.set_dr(set_progress(schedule, t))`` between rollouts instead of
+        rebuilding the env.  Later episodes are then exactly those of
+        ``make_env(task, sim, dr=spec, seed=seed)`` (same streams, same
+        episode counters).  Steps captured in a CUDA graph before the call keep
+        the old spec: re-capture after it.
+        """
+        if self.task.level != LEVEL_DISTURBED_DR:
+            raise TaskError("a DR spec requires level 'disturbed_dr'")
+        mode = self._sampler_c.rng_mode
+        self._dr = dict(dr)
+        self._sampler = spec_sampler(self._dr, start_box(self.task))
+        packed = self._sampler.pack()
+        packed.rng_mode = mode
+        self.state._note_sampler(self._sampler)
+        self._sampler_c = packed
 
     def observe(self):
         st = self.state

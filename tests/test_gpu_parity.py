@@ -507,3 +507,47 @@ def test_gaussian_dr_task_env_runs_fp32():
     assert torch.isfinite(obs).all() and torch.isfinite(rew).all()
     m = np.array([o["mass*"] for o in env.state.overlays[:2000]])
     assert m.min() >= 0.2 and m.max() <= 1.8 and abs(m.mean() - 1.0) < 0.02
+
+
+def test_set_dr_schedule_between_rollouts_matches_fresh_spec():
+    """env.set_dr(set_progress(schedule, t)): later episodes draw the new spec exactly."""
+    from paper_2503_09203_b200.randomization import (BoundsSchedule, DRParameter, DRSchedule,
+                                                     Gaussian, set_progress)
+    from paper_2503_09203_b200.tasks import disturbed_spec
+
+    base = dict(preset("train"))
+    base["thrust_coeff*"] = DRParameter("thrust_coeff*", Gaussian(1.0, 0.05, (0.9, 1.1)))
+    sch = DRSchedule(base, [BoundsSchedule("mass*", [(0.0, 1.0, 1.0), (1.0, 0.6, 1.4)]),
+                            BoundsSchedule("current_velocity", [(0.0, 0.0, 0.0), (1.0, 0.0, 1.0)])])
+    task = TaskConfig(task="station_keeping", vehicle="bluerov", level="disturbed_dr")
+    n = 256
+    env = make_env(task, E.SimConfig(batch_size=n), seed=9, dtype=torch.float64)
+    oe = O.TaskEnv(task, product_vehicle("bluerov"), n, seed=9,
+                   disturbed_spec=disturbed_spec(), train_spec=preset("train"))
+    env.reset()
+    oe.reset()
+    rng = np.random.default_rng(3)
+    for prog in (0.0, 0.5, 1.0):
+        spec = set_progress(sch, prog)
+        env.set_dr(spec)
+        oe.dr = spec
+        oe.dyn = {k: v for k, v in spec.items() if not k.startswith("current")}
+        mask = rng.random(n) < 0.5
+        env.reset(mask)
+        oe.reset(mask)
+        got = env.state.overlays
+        for i in np.nonzero(mask)[0]:
+            assert got[i] == oe.batch.overlays[i], (prog, i)
+        assert np.array_equal(host(env.state.p)[mask], oe.batch.p[mask])  # fresh draws
+        ok, err = rowwise_close(host(env.state.p), oe.batch.p, 1e-10, 1e-12)
+        assert ok, err
+        for _ in range(5):
+            u = rng.uniform(-1, 1, (n, env.action_dim))
+            obs, rew, term, trunc, info = env.step(torch.from_numpy(u).cuda())
+            o_obs, o_rew, o_term, o_trunc, _ = oe.step(u)
+            assert np.array_equal(host(term).astype(bool), o_term)
+            ok, err = rowwise_close(host(obs), o_obs, 1e-10, 1e-12)
+            assert ok, (prog, err)
+    with pytest.raises(Exception):
+        make_env(TaskConfig(task="station_keeping", vehicle="bluerov"),
+                 E.SimConfig(batch_size=8)).set_dr(base)
