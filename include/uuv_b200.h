@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define UUV_ABI_VERSION 2
+#define UUV_ABI_VERSION 3
 #define UUV_MAX_ACT 8        /* actuator columns per vehicle type             */
 #define UUV_MAX_TYPES 6      /* vehicle types in one batch (mixed fleets)     */
 #define UUV_MLP_MAX_PARAMS 128 /* packed weights+biases of one rotor network  */
@@ -239,12 +239,40 @@ typedef struct {
 enum { UUV_TRACE_P = 0, UUV_TRACE_Q = 3, UUV_TRACE_NU = 7, UUV_TRACE_REWARD = 13,
        UUV_TRACE_T = 14, UUV_TRACE_CMD = 15, UUV_TRACE_COUNT = 15 };
 
+/*
+ * Population of affine-tanh policies evaluated inside the task step
+ * (baseline.py:37-84, 109-192): row i acts with member m = i / slot,
+ *   u_i = tanh(W_m obs_i + b_m)  for m < members,  0 otherwise,
+ * where obs_i is the observation the previous step (or reset) returned.
+ * theta rows are [members][theta_ld] in the batch dtype: W (action_dim x
+ * obs_dim, row-major) then b (action_dim) -- the reference's Policy.theta().
+ * With `ret` set, the launch also runs one iteration of _rollout_returns
+ * (baseline.py:109-127): pending rows accumulate the reward, a row's first
+ * finish records metric/success and clears pending, and live[t] counts rows
+ * still pending after step t.  Step t (1-based) is a no-op when live[t-1] is 0,
+ * so a whole episode loop can be enqueued (or graph-captured) without host syncs
+ * and stops exactly where the reference's `if not pending.any(): break` does.
+ */
+typedef struct {
+  const void* theta;
+  int64_t theta_ld;
+  int32_t members;
+  int32_t slot;
+  double* ret;             /* [ld] or NULL (no episode bookkeeping) */
+  void* metric;            /* [ld] batch dtype                      */
+  uint8_t* success;        /* [ld]                                  */
+  uint8_t* pending;        /* [ld] 1 until the row's first finish   */
+  int32_t* live;           /* [>= t + 1], live[0] = initial pending */
+  int32_t t;               /* this launch's step index, >= 1        */
+  int32_t pad_;
+} uuv_policy;
+
 typedef struct uuv_ctx uuv_ctx;
 
 const char* uuv_last_error(void);
 int32_t uuv_abi_version(void);
 /* sizeof of the ABI structs, for binding self-checks: hull, state, sampler, task, task_io. */
-void uuv_abi_sizes(int64_t out[5]);
+void uuv_abi_sizes(int64_t out[6]);  /* sizeof hull, state, sampler, task, task_io, policy */
 
 /* Context: owns the hull list of one batch (host copy; travels by value in each launch). */
 uuv_status uuv_ctx_create(const uuv_hull* hulls, int32_t n_types, uuv_ctx** out);
@@ -276,6 +304,13 @@ uuv_status uuv_task_step(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task
                          void* stream);
 
 /* Reset masked rows (prev_u and dev_sum zeroed too), then observe all rows. */
+/* uuv_task_step with the commands computed on the device by a policy
+ * population (uuv_policy); io->obs may be NULL (the observation is recomputed
+ * in-kernel from the state).  Replaces the act_fn(obs) -> env.step round trip
+ * of baseline._rollout_returns / evaluate / cem_train. */
+uuv_status uuv_policy_step(uuv_ctx* ctx, const uuv_state* state, const uuv_task* task,
+                           const uuv_sampler* sampler, uint64_t seed, const uuv_policy* policy,
+                           int32_t substeps, double dt, const uuv_task_io* io, void* stream);
 uuv_status uuv_task_reset(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task,
                           const uuv_sampler* sampler, uint64_t seed, const uint8_t* mask,
                           double dt, const uuv_task_io* io, void* stream);

@@ -35,7 +35,7 @@ OV_WIDTH["payload_position"] = 3
 OV_WIDTH["mount_position_jitter"] = 3 * MAX_ACT
 OV_IDENTITY = {k: (1.0 if i <= OV_INDEX["thrust_coeff*"] else 0.0) for i, k in enumerate(OV_KEYS)}
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 DIST_UNIFORM, DIST_PIECEWISE, DIST_GAUSSIAN = 0, 1, 2
 START_IDENTITY, START_BOX = 0, 1
 CURRENT_NONE, CURRENT_RANDOM_HEADING, CURRENT_HEADING_DRAW = 0, 1, 2
@@ -128,6 +128,13 @@ class TaskIO(C.Structure):
                 ("trace_ld", C.c_int64)]
 
 
+class Policy(C.Structure):
+    _fields_ = [("theta", C.c_void_p), ("theta_ld", C.c_int64), ("members", C.c_int32),
+                ("slot", C.c_int32), ("ret", C.c_void_p), ("metric", C.c_void_p),
+                ("success", C.c_void_p), ("pending", C.c_void_p), ("live", C.c_void_p),
+                ("t", C.c_int32), ("pad_", C.c_int32)]
+
+
 EXPORTS = {
     "uuv_last_error": (C.c_char_p, []),
     "uuv_abi_version": (C.c_int32, []),
@@ -144,6 +151,9 @@ EXPORTS = {
     "uuv_task_step": (C.c_int, [C.c_void_p, C.POINTER(State), C.POINTER(Task), C.POINTER(Sampler),
                                 C.c_uint64, C.c_void_p, C.c_int64, C.c_int32, C.c_double,
                                 C.POINTER(TaskIO), C.c_void_p]),
+    "uuv_policy_step": (C.c_int, [C.c_void_p, C.POINTER(State), C.POINTER(Task),
+                                  C.POINTER(Sampler), C.c_uint64, C.POINTER(Policy), C.c_int32,
+                                  C.c_double, C.POINTER(TaskIO), C.c_void_p]),
     "uuv_task_reset": (C.c_int, [C.c_void_p, C.POINTER(State), C.POINTER(Task), C.POINTER(Sampler),
                                  C.c_uint64, C.c_void_p, C.c_double, C.POINTER(TaskIO),
                                  C.c_void_p]),
@@ -180,9 +190,10 @@ def load():
     if lib.uuv_abi_version() != ABI_VERSION:
         raise NativeError(f"ABI mismatch: library version {lib.uuv_abi_version()} != "
                           f"binding {ABI_VERSION}; rebuild with `make`")
-    sizes = (C.c_int64 * 5)()
+    sizes = (C.c_int64 * 6)()
     lib.uuv_abi_sizes(sizes)
-    want = [C.sizeof(Hull), C.sizeof(State), C.sizeof(Sampler), C.sizeof(Task), C.sizeof(TaskIO)]
+    want = [C.sizeof(Hull), C.sizeof(State), C.sizeof(Sampler), C.sizeof(Task), C.sizeof(TaskIO),
+            C.sizeof(Policy)]
     if list(sizes) != want:
         raise NativeError(f"ABI mismatch: library struct sizes {list(sizes)} != binding {want}")
     _lib = lib

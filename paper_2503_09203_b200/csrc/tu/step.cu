@@ -1,0 +1,3 @@
+// Translation unit step of libuuvb200.so (see UUV_TU in ../uuv_b200.cu).
+#define UUV_TU 2
+#include "../uuv_b200.cu"

@@ -17,6 +17,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <map>
+#include <type_traits>
 #include <string>
 #include <vector>
 
@@ -24,6 +25,22 @@
 #include "uuv_bulk.cuh"
 
 using namespace uuv;
+
+// Translation-unit split: the Makefile compiles this file once per UUV_TU so
+// the kernel families build in parallel (1 = C ABI + reset/statistics/
+// inspection kernels, 2 = physics step kernels, 3 = task step kernels,
+// 4 = policy step kernels).  UUV_TU 0 (default) builds everything in one TU.
+#ifndef UUV_TU
+#define UUV_TU 0
+#endif
+#define UUV_TU_MAIN (UUV_TU == 0 || UUV_TU == 1)
+#define UUV_TU_STEP (UUV_TU == 0 || UUV_TU == 2)
+#define UUV_TU_TASK (UUV_TU == 0 || UUV_TU == 3)
+#define UUV_TU_POLICY (UUV_TU == 0 || UUV_TU == 4)
+
+namespace uuv_tu {
+extern thread_local std::string g_err;  // uuv_last_error's message (defined in TU 1)
+}
 
 namespace {
 
@@ -41,8 +58,6 @@ template <> struct MinB<float> { static constexpr int value = UUV_MINB_F32; };
 template <> struct MinB<double> { static constexpr int value = UUV_MINB_F64; };
 constexpr int kObsMax = 12 + UUV_MAX_ACT + 3;
 
-thread_local std::string g_err;
-
 uuv_status fail(uuv_status s, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
 uuv_status fail(uuv_status s, const char* fmt, ...) {
   char buf[512];
@@ -50,7 +65,7 @@ uuv_status fail(uuv_status s, const char* fmt, ...) {
   va_start(ap, fmt);
   vsnprintf(buf, sizeof buf, fmt, ap);
   va_end(ap);
-  g_err = buf;
+  uuv_tu::g_err = buf;
   return s;
 }
 
@@ -199,14 +214,14 @@ UUV_D void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::)
 
 // UUV_PDL: 0 off, 1 trigger dependents at kernel entry, 2 (default) trigger after the
 // stores.  Measured on B200 (cfg2, 4096 envs, graph of 100 steps): 2.57 / 3.29 / 2.34 us.
-int pdl_mode() {
+static int pdl_mode() {
   static const int m = [] {
     const char* v = getenv("UUV_PDL");
     return v ? atoi(v) : 2;
   }();
   return m;
 }
-bool pdl_enabled() { return pdl_mode() != 0; }
+static bool pdl_enabled() { return pdl_mode() != 0; }
 
 template <typename Kernel, typename Args>
 cudaError_t launch_pdl(Kernel k, unsigned grid, cudaStream_t s, const Args& a) {
@@ -570,6 +585,16 @@ template <typename R> struct TaskArgs {
   double* stats;
   R* trace;
   int64_t trace_ld;
+  // policy population + episode bookkeeping (uuv_policy_step only)
+  const R* pol_theta;
+  int64_t pol_ld;
+  int32_t pol_members, pol_slot;
+  double* ep_ret;
+  R* ep_metric;
+  uint8_t* ep_success;
+  uint8_t* ep_pending;
+  int32_t* ep_live;
+  int32_t ep_t;
   const uint8_t* mask;  // task reset only
   int32_t mode;         // task reset kernel: 0 observe only, 1 reset masked then observe
 };
@@ -585,10 +610,32 @@ UUV_D void flush_obs(const R* s_obs, R* obs, int64_t obs_ld, int obs_dim, int64_
   }
 }
 
-template <typename R, bool DR, int AC, bool DM>
+// u = tanh(W_m obs + b_m) for the row's population member (baseline.py:62-64,
+// 164-169): products summed in obs order without contraction, then + b.
+template <typename R>
+UUV_D void policy_command(const TaskArgs<R>& a, int A, int od, int64_t i, const R* obs, R* raw) {
+  const int64_t m = i / a.pol_slot;
+#pragma unroll
+  for (int j = 0; j < UUV_MAX_ACT; ++j) raw[j] = R(0);
+  if (m >= a.pol_members) return;  // rows past members * slot act with 0
+  const R* th = a.pol_theta + m * a.pol_ld;
+#pragma unroll
+  for (int j = 0; j < UUV_MAX_ACT; ++j) {
+    if (j < A) {
+      const R* w = th + j * od;
+      R acc = R(0);
+      for (int k = 0; k < od; ++k) acc = add_rn(acc, mul_rn(__ldg(w + k), obs[k]));
+      raw[j] = tanh(add_rn(acc, __ldg(th + A * od + j)));
+    }
+  }
+}
+
+template <typename R, bool DR, int AC, bool DM, bool POL = false>
 __global__ void __launch_bounds__(kBlock, MinB<R>::value) k_task_step(const __grid_constant__ TaskArgs<R> a) {
   __shared__ R s_obs[kBlock * kObsMax];
   __shared__ double s_red[kBlock / 32][UUV_ST_COUNT];
+  if (POL && a.ep_live != nullptr && a.ep_live[a.ep_t - 1] == 0) return;  // the episode loop broke
+  bool live = false;
   const int64_t row0 = (int64_t)blockIdx.x * kBlock;
   const int64_t i = row0 + threadIdx.x;
   const StateView<R>& sv = a.sv;
@@ -601,24 +648,36 @@ __global__ void __launch_bounds__(kBlock, MinB<R>::value) k_task_step(const __gr
 #pragma unroll
   for (int k = 0; k < UUV_ST_COUNT; ++k) st[k] = 0.0;
   if (i < sv.n) {
+    int32_t steps = sv.steps[i];
+    bool div = sv.diverged[i] != 0;
+    R px, py, pz, nu[6], act[UUV_MAX_ACT];
+    Q4<R> q;
+    load_state(sv, i, A, px, py, pz, q, nu, act);
     // u = clip(commands); du = u - prev_u; prev_u = u  (tasks/core.py:329-335)
-    R u[UUV_MAX_ACT], du[UUV_MAX_ACT];
-    const R* crow = a.cmd + i * a.cmd_ld;
+    R u[UUV_MAX_ACT], du[UUV_MAX_ACT], raw[UUV_MAX_ACT];
+    if constexpr (POL) {
+      // the observation the last step returned, recomputed from the stored state
+      R pu[UUV_MAX_ACT];
+#pragma unroll
+      for (int j = 0; j < UUV_MAX_ACT; ++j) pu[j] = j < A ? a.prev_u[j * ld + i] : R(0);
+      R* orow = s_obs + threadIdx.x * od;
+      observe_row<R>(T, A, px, py, pz, q, nu, pu, steps, a.dt, orow, nullptr);
+      policy_command<R>(a, A, od, i, orow, raw);
+    } else {
+      const R* crow = a.cmd + i * a.cmd_ld;
+#pragma unroll
+      for (int j = 0; j < UUV_MAX_ACT; ++j) raw[j] = j < A ? crow[j] : R(0);
+    }
 #pragma unroll
     for (int j = 0; j < UUV_MAX_ACT; ++j) {
       if (j < A) {
-        u[j] = clip_<R>(crow[j], R(-1), R(1));
+        u[j] = clip_<R>(raw[j], R(-1), R(1));
         du[j] = u[j] - a.prev_u[j * ld + i];
       } else {
         u[j] = R(0);
         du[j] = R(0);
       }
     }
-    int32_t steps = sv.steps[i];
-    bool div = sv.diverged[i] != 0;
-    R px, py, pz, nu[6], act[UUV_MAX_ACT];
-    Q4<R> q;
-    load_state(sv, i, A, px, py, pz, q, nu, act);
     if (!div) div = physics<R, DR, AC, DM>(H, sv, i, a.K, a.dt_sub, u, px, py, pz, q, nu, act);
     steps += 1;
     R dev = a.dev_sum != nullptr ? a.dev_sum[i] : R(0);
@@ -644,6 +703,18 @@ __global__ void __launch_bounds__(kBlock, MinB<R>::value) k_task_step(const __gr
       a.fout[UUV_TF_SUCCESS * ld + i] = o.success;
       a.fout[UUV_TF_DIVERGED * ld + i] = div;
       a.fout[UUV_TF_CONTACT * ld + i] = o.contact;
+    }
+    if constexpr (POL) {
+      if (a.ep_ret != nullptr && a.ep_pending[i]) {  // _rollout_returns (baseline.py:116-123)
+        a.ep_ret[i] += (double)o.reward;
+        if (o.finished) {
+          a.ep_metric[i] = o.metric;
+          a.ep_success[i] = o.success;
+          a.ep_pending[i] = 0;
+        } else {
+          live = true;
+        }
+      }
     }
     st[UUV_ST_REWARD] = (double)o.reward;
     st[UUV_ST_FINISHED] = o.finished;
@@ -687,11 +758,17 @@ __global__ void __launch_bounds__(kBlock, MinB<R>::value) k_task_step(const __gr
       for (int k = 0; k < 6; ++k) tr[(UUV_TRACE_NU + k) * tl] = nu[k];
       tr[UUV_TRACE_REWARD * tl] = o.reward;
       tr[UUV_TRACE_T * tl] = (R)(__dmul_rn((double)steps, a.dt64));
-      for (int j = 0; j < A; ++j) tr[(UUV_TRACE_CMD + j) * tl] = crow[j];
+      for (int j = 0; j < A; ++j) tr[(UUV_TRACE_CMD + j) * tl] = raw[j];
+    }
+  }
+  if constexpr (POL) {
+    if (a.ep_live != nullptr) {
+      const int cnt = __syncthreads_count(live);
+      if (threadIdx.x == 0 && cnt != 0) atomicAdd(a.ep_live + a.ep_t, cnt);
     }
   }
   __syncthreads();
-  flush_obs<R>(s_obs, a.obs, a.obs_ld, od, row0, sv.n);
+  if (a.obs != nullptr) flush_obs<R>(s_obs, a.obs, a.obs_ld, od, row0, sv.n);
   if (a.stats != nullptr) {
     // deterministic CTA reduction: fixed shuffle tree, then warps in order
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -776,7 +853,8 @@ __global__ void __launch_bounds__(kBlock) k_reset(const __grid_constant__ ResetA
 }
 
 // ------------------------------------------------------------------ statistics
-__global__ void k_stats(const double* stats, int64_t n_blocks, double* out, int32_t reset,
+#if UUV_TU_MAIN
+static __global__ void k_stats(const double* stats, int64_t n_blocks, double* out, int32_t reset,
                         double* stats_rw) {
   // one CTA; thread k sums statistic k over blocks in index order (deterministic)
   const int k = threadIdx.x;
@@ -787,6 +865,7 @@ __global__ void k_stats(const double* stats, int64_t n_blocks, double* out, int3
   if (reset)
     for (int64_t b = 0; b < n_blocks; ++b) stats_rw[b * UUV_ST_COUNT + k] = 0.0;
 }
+#endif
 
 // ------------------------------------------------------------------ inspection kernels
 template <typename R, int NT> struct DeriveArgs {
@@ -1195,33 +1274,41 @@ void fill_task_args(const uuv_ctx* ctx, const uuv_state* st, const uuv_task* tas
   a.stats = io->stats;
   a.trace = (R*)io->trace;
   a.trace_ld = io->trace_ld;
+  a.pol_theta = nullptr;
+  a.pol_ld = 0;
+  a.pol_members = a.pol_slot = 0;
+  a.ep_ret = nullptr;
+  a.ep_metric = nullptr;
+  a.ep_success = a.ep_pending = nullptr;
+  a.ep_live = nullptr;
+  a.ep_t = 0;
   a.mask = nullptr;
   a.mode = 0;
   a.cmd = nullptr;
   a.cmd_ld = 0;
 }
 
-template <typename R, int AC, bool DM>
+template <typename R, int AC, bool DM, bool POL>
 void launch_task_dr(bool dr, unsigned g, cudaStream_t cs, const TaskArgs<R>& a) {
-  if (dr) k_task_step<R, true, AC, DM><<<g, kBlock, 0, cs>>>(a);
-  else k_task_step<R, false, AC, DM><<<g, kBlock, 0, cs>>>(a);
+  if (dr) k_task_step<R, true, AC, DM, POL><<<g, kBlock, 0, cs>>>(a);
+  else k_task_step<R, false, AC, DM, POL><<<g, kBlock, 0, cs>>>(a);
 }
 
-template <typename R>
+template <typename R, bool POL = false>
 void launch_task_step(bool dr, int ac, bool dm, unsigned g, cudaStream_t cs, const TaskArgs<R>& a) {
   if (ac == 6) {
-    if (dm) launch_task_dr<R, 6, true>(dr, g, cs, a);
-    else launch_task_dr<R, 6, false>(dr, g, cs, a);
+    if (dm) launch_task_dr<R, 6, true, POL>(dr, g, cs, a);
+    else launch_task_dr<R, 6, false, POL>(dr, g, cs, a);
   } else if (ac == 8) {
-    if (dm) launch_task_dr<R, 8, true>(dr, g, cs, a);
-    else launch_task_dr<R, 8, false>(dr, g, cs, a);
+    if (dm) launch_task_dr<R, 8, true, POL>(dr, g, cs, a);
+    else launch_task_dr<R, 8, false, POL>(dr, g, cs, a);
   } else {
-    launch_task_dr<R, 0, false>(dr, g, cs, a);
+    launch_task_dr<R, 0, false, POL>(dr, g, cs, a);
   }
 }
 
 uuv_status check_task(const uuv_ctx* ctx, const uuv_state* st, const uuv_task* task,
-                      const uuv_task_io* io) {
+                      const uuv_task_io* io, bool obs_optional = false) {
   if (task == nullptr || io == nullptr) return fail(UUV_ERR_ARG, "null task or io");
   if (ctx->hulls.size() != 1) return fail(UUV_ERR_UNSUPPORTED, "tasks need a single-vehicle batch");
   const int A = ctx->hulls[0].n_act;
@@ -1229,7 +1316,8 @@ uuv_status check_task(const uuv_ctx* ctx, const uuv_state* st, const uuv_task* t
   if (task->obs_dim != 12 + A + extra)
     return fail(UUV_ERR_SHAPE, "task: obs_dim %d != 12 + A + extra = %d", task->obs_dim,
                 12 + A + extra);
-  if (io->obs == nullptr || io->prev_u == nullptr || io->obs_ld < task->obs_dim)
+  if ((io->obs == nullptr && !obs_optional) || io->prev_u == nullptr ||
+      (io->obs != nullptr && io->obs_ld < task->obs_dim))
     return fail(UUV_ERR_ARG, "task io: obs / prev_u missing or obs_ld too small");
   if (task->kind == UUV_TASK_TRACKING && io->dev_sum == nullptr)
     return fail(UUV_ERR_ARG, "task io: tracking needs dev_sum");
@@ -1237,6 +1325,45 @@ uuv_status check_task(const uuv_ctx* ctx, const uuv_state* st, const uuv_task* t
 }
 
 }  // namespace
+
+namespace uuv_tu {
+template <typename R>
+uuv_status step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd, int64_t cmd_ld,
+                int32_t K, double dt, cudaStream_t s);
+template <typename R, bool POL>
+void task(bool dr, int ac, bool dm, unsigned g, cudaStream_t cs, const TaskArgs<R>& a);
+
+#if UUV_TU_STEP
+template <typename R>
+uuv_status step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd, int64_t cmd_ld,
+                int32_t K, double dt, cudaStream_t s) {
+  return dispatch_step<R>(ctx, st, cmd, cmd_ld, K, dt, s);
+}
+template uuv_status step<float>(const uuv_ctx*, const uuv_state*, const void*, int64_t, int32_t,
+                                double, cudaStream_t);
+template uuv_status step<double>(const uuv_ctx*, const uuv_state*, const void*, int64_t, int32_t,
+                                 double, cudaStream_t);
+#endif
+#if UUV_TU_TASK || UUV_TU_POLICY
+template <typename R, bool POL>
+void task(bool dr, int ac, bool dm, unsigned g, cudaStream_t cs, const TaskArgs<R>& a) {
+  launch_task_step<R, POL>(dr, ac, dm, g, cs, a);
+}
+#endif
+#if UUV_TU_TASK
+template void task<float, false>(bool, int, bool, unsigned, cudaStream_t, const TaskArgs<float>&);
+template void task<double, false>(bool, int, bool, unsigned, cudaStream_t, const TaskArgs<double>&);
+#endif
+#if UUV_TU_POLICY
+template void task<float, true>(bool, int, bool, unsigned, cudaStream_t, const TaskArgs<float>&);
+template void task<double, true>(bool, int, bool, unsigned, cudaStream_t, const TaskArgs<double>&);
+#endif
+}  // namespace uuv_tu
+
+#if UUV_TU_MAIN
+namespace uuv_tu {
+thread_local std::string g_err;
+}
 
 template <typename R, int NT>
 static uuv_status derive_launch(const uuv_ctx* ctx, const uuv_state* st, double* o12, double* minv,
@@ -1319,14 +1446,15 @@ static uuv_status task_reset_impl(uuv_ctx* ctx, const uuv_state* st, const uuv_t
 // ================================================================== C ABI
 extern "C" {
 
-const char* uuv_last_error(void) { return g_err.c_str(); }
+const char* uuv_last_error(void) { return uuv_tu::g_err.c_str(); }
 int32_t uuv_abi_version(void) { return UUV_ABI_VERSION; }
-void uuv_abi_sizes(int64_t out[5]) {
+void uuv_abi_sizes(int64_t out[6]) {
   out[0] = sizeof(uuv_hull);
   out[1] = sizeof(uuv_state);
   out[2] = sizeof(uuv_sampler);
   out[3] = sizeof(uuv_task);
   out[4] = sizeof(uuv_task_io);
+  out[5] = sizeof(uuv_policy);
 }
 
 uuv_status uuv_ctx_set_hulls(uuv_ctx* ctx, const uuv_hull* hulls, int32_t n_types) {
@@ -1394,8 +1522,8 @@ uuv_status uuv_step(uuv_ctx* ctx, const uuv_state* st, const void* commands, int
   if (!(dt > 0)) return fail(UUV_ERR_ARG, "dt must be > 0");
   if (st->n_envs == 0) return UUV_OK;
   cudaStream_t cs = (cudaStream_t)stream;
-  return st->dtype == UUV_F32 ? dispatch_step<float>(ctx, st, commands, cmd_ld, substeps, dt, cs)
-                              : dispatch_step<double>(ctx, st, commands, cmd_ld, substeps, dt, cs);
+  return st->dtype == UUV_F32 ? uuv_tu::step<float>(ctx, st, commands, cmd_ld, substeps, dt, cs)
+                              : uuv_tu::step<double>(ctx, st, commands, cmd_ld, substeps, dt, cs);
 }
 
 uuv_status uuv_step_host(uuv_ctx* ctx, const uuv_state* st, const void* host_cmd, int64_t cmd_ld,
@@ -1475,15 +1603,64 @@ uuv_status uuv_task_step(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task
     fill_task_args<float>(ctx, st, task, sampler, seed, dt, substeps, io, a);
     a.cmd = (const float*)commands;
     a.cmd_ld = cmd_ld;
-    launch_task_step<float>(dr, act_class(ctx), diag_mass(ctx, st), g, cs, a);
+    uuv_tu::task<float, false>(dr, act_class(ctx), diag_mass(ctx, st), g, cs, a);
   } else {
     TaskArgs<double> a;
     fill_task_args<double>(ctx, st, task, sampler, seed, dt, substeps, io, a);
     a.cmd = (const double*)commands;
     a.cmd_ld = cmd_ld;
-    launch_task_step<double>(dr, act_class(ctx), diag_mass(ctx, st), g, cs, a);
+    uuv_tu::task<double, false>(dr, act_class(ctx), diag_mass(ctx, st), g, cs, a);
   }
   return check_launch("uuv_task_step");
+}
+
+uuv_status uuv_policy_step(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task,
+                           const uuv_sampler* sampler, uint64_t seed, const uuv_policy* pol,
+                           int32_t substeps, double dt, const uuv_task_io* io, void* stream) {
+  uuv_status s = check_state(ctx, st);
+  if (s != UUV_OK) return s;
+  if ((s = check_task(ctx, st, task, io, true)) != UUV_OK) return s;
+  if ((s = check_sampler(sampler)) != UUV_OK) return s;
+  if (pol == nullptr || pol->theta == nullptr) return fail(UUV_ERR_ARG, "policy: null theta");
+  const int A = ctx->hulls[0].n_act;
+  if (pol->members < 1 || pol->slot < 1)
+    return fail(UUV_ERR_ARG, "policy: members and slot must be >= 1");
+  if (pol->theta_ld < (int64_t)A * task->obs_dim + A)
+    return fail(UUV_ERR_SHAPE, "policy: theta row stride < action_dim * obs_dim + action_dim");
+  if (pol->ret != nullptr &&
+      (pol->metric == nullptr || pol->success == nullptr || pol->pending == nullptr ||
+       pol->live == nullptr || pol->t < 1))
+    return fail(UUV_ERR_ARG, "policy: episode buffers incomplete or t < 1");
+  if (substeps < 1 || !(dt > 0)) return fail(UUV_ERR_ARG, "substeps >= 1 and dt > 0 required");
+  if (st->n_envs == 0) return UUV_OK;
+  cudaStream_t cs = (cudaStream_t)stream;
+  const unsigned g = (unsigned)grid_for(st->n_envs);
+  const bool dr = st->overlay != nullptr;
+  auto fill_pol = [&](auto& a, auto* theta) {
+    using RT = std::remove_const_t<std::remove_pointer_t<decltype(theta)>>;
+    a.pol_theta = theta;
+    a.pol_ld = pol->theta_ld;
+    a.pol_members = pol->members;
+    a.pol_slot = pol->slot;
+    a.ep_ret = pol->ret;
+    a.ep_metric = (RT*)pol->metric;
+    a.ep_success = pol->success;
+    a.ep_pending = pol->pending;
+    a.ep_live = pol->ret != nullptr ? pol->live : nullptr;
+    a.ep_t = pol->t;
+  };
+  if (st->dtype == UUV_F32) {
+    TaskArgs<float> a;
+    fill_task_args<float>(ctx, st, task, sampler, seed, dt, substeps, io, a);
+    fill_pol(a, (const float*)pol->theta);
+    uuv_tu::task<float, true>(dr, act_class(ctx), diag_mass(ctx, st), g, cs, a);
+  } else {
+    TaskArgs<double> a;
+    fill_task_args<double>(ctx, st, task, sampler, seed, dt, substeps, io, a);
+    fill_pol(a, (const double*)pol->theta);
+    uuv_tu::task<double, true>(dr, act_class(ctx), diag_mass(ctx, st), g, cs, a);
+  }
+  return check_launch("uuv_policy_step");
 }
 
 uuv_status uuv_task_reset(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task,
@@ -1533,3 +1710,5 @@ uuv_status uuv_substep_terms(uuv_ctx* ctx, const uuv_state* st, const void* comm
 }
 
 }  // extern "C"
+
+#endif  // UUV_TU_MAIN

@@ -322,8 +322,8 @@ class VecTaskEnv:
         io = _N.TaskIO()
         io.prev_u = self._prev_u.data_ptr()
         io.dev_sum = self._dev_sum.data_ptr() if self._dev_sum is not None else None
-        io.obs = obs.data_ptr()
-        io.obs_ld = obs.stride(0)
+        io.obs = obs.data_ptr() if obs is not None else None
+        io.obs_ld = obs.stride(0) if obs is not None else 0
         io.term_obs = term.data_ptr() if term is not None else None
         io.real_out = rout.data_ptr() if rout is not None else None
         io.flag_out = fout.data_ptr() if fout is not None else None

@@ -1,0 +1,125 @@
+"""Device episode loop (uuv_policy_step) vs the reference's cem_train / evaluate."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2503_09203_b200 import baseline as B
+from paper_2503_09203_b200.engine import SimConfig
+from paper_2503_09203_b200.tasks import TaskConfig, make_env
+
+pytestmark = pytest.mark.gpu
+GOLD = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                                   "baseline_reference.json")))
+# float64 closed-loop episodes; the policy's dot product and the physics agree
+# with the reference to ~1e-15 per step, compounded over <= 80 steps
+RTOL = 1e-9
+
+
+def small_env(seed=5, batch=40, **kw):
+    task = TaskConfig(task="station_keeping", vehicle="bluerov", episode_length=60)
+    return make_env(task, SimConfig(batch_size=batch), seed=seed, **kw)
+
+
+def dock_env(seed=3, batch=43, **kw):
+    task = TaskConfig(task="docking", vehicle="bluerov_heavy", level="disturbed_dr",
+                      episode_length=80)
+    return make_env(task, SimConfig(batch_size=batch), seed=seed, **kw)
+
+
+REF = dict(dtype=torch.float64, rng="pcg64")
+
+
+@pytest.mark.parametrize("case,mk", [("cem_station", small_env), ("cem_dock_padded", dock_env)])
+def test_cem_matches_reference(case, mk):
+    g = GOLD[case]
+    env = mk(**REF)
+    res = B.cem_train(env, **g["kw"])
+    for mine, ref in zip(res.curve, g["curve"]):
+        assert mine["iteration"] == ref["iteration"]
+        for k in ("mean_return", "elite_return", "best_return"):
+            np.testing.assert_allclose(mine[k], ref[k], rtol=RTOL, err_msg=k)
+    np.testing.assert_allclose(res.policy.theta(), g["theta"], rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(res.best_return, g["best_return"], rtol=RTOL)
+    # same loop lengths and auto-resets: episode counters equal after all iterations
+    assert env.state.episodes.cpu().tolist() == g["episodes"]
+
+
+def test_evaluate_matches_reference():
+    g = GOLD["eval_zero"]
+    env = small_env(seed=9, batch=25, **REF)
+    cell = B.evaluate(B.Policy.zeros(env.obs_dim, env.action_dim), env, n_trials=50)
+    assert (cell.label, cell.n_trials) == (g["label"], g["n_trials"])
+    np.testing.assert_allclose([cell.mean_error, cell.std_error],
+                               [g["mean_error"], g["std_error"]], rtol=RTOL)
+    assert cell.success_rate == g["success_rate"]
+    assert env.state.episodes.cpu().tolist() == g["episodes"]
+    g = GOLD["eval_trained"]
+    env = small_env(seed=7, batch=30, **REF)
+    pol = B.Policy.from_theta(np.asarray(GOLD["cem_station"]["theta"]), env.obs_dim,
+                              env.action_dim)
+    cell = B.evaluate(pol, env, n_trials=45, label="trained")
+    np.testing.assert_allclose([cell.mean_error, cell.std_error],
+                               [g["mean_error"], g["std_error"]], rtol=RTOL)
+    assert cell.success_rate == g["success_rate"]
+
+
+def test_device_loop_matches_host_loop_and_graph_replay():
+    """Fused policy launches == env.step with the same policy on the host side of the ABI."""
+    pol = B.Policy(weights=np.random.default_rng(0).uniform(-0.2, 0.2, (8, 21)),
+                   bias=np.array([0.1, -0.1, 0.0, 0.2, -0.5, -0.5, -0.5, -0.5]))
+    outs = []
+    for mode in ("callable", "eager", "graph"):
+        env = dock_env(batch=64, dtype=torch.float64)
+        if mode == "callable":
+            outs.append(B._rollout_returns(env, lambda o: pol(o)))
+        else:
+            r = B.EpisodeRunner(env, 1, 64, graph=(mode == "graph"))
+            outs.append(r.run(pol.theta()[None]))
+            outs.append(r.run(pol.theta()[None]))  # second episode (fresh reset)
+        outs[-1] = outs[-1] + (env.state.episodes.cpu().tolist(),)
+    cb, e1, e2, g1, g2 = outs
+    for a, b in ((e1, g1), (e2, g2)):  # graph replay == eager launches, bit for bit
+        for x, y in zip(a, b):
+            assert np.array_equal(np.asarray(x), np.asarray(y))
+    np.testing.assert_allclose(cb[0], e1[0], rtol=1e-9)
+    np.testing.assert_allclose(cb[1], e1[1], rtol=1e-9, atol=1e-12)
+    assert np.array_equal(cb[2], e1[2])
+
+
+def test_cem_deterministic_monotone_and_zero_variance():
+    curves = [B.cem_train(small_env(), population=10, iterations=3, seed=5).curve
+              for _ in range(2)]
+    assert curves[0] == curves[1]
+    res = B.cem_train(small_env(seed=6), population=10, iterations=5, seed=6)
+    best = [c["best_return"] for c in res.curve]
+    assert all(b2 >= b1 for b1, b2 in zip(best, best[1:])) and res.best_return == best[-1]
+    env = small_env()
+    p0 = B.Policy.zeros(env.obs_dim, env.action_dim)
+    res = B.cem_train(env, population=10, iterations=3, seed=5, init_std=0.0, init_policy=p0)
+    assert res.policy.theta().tobytes() == p0.theta().tobytes()
+
+
+def test_validation():
+    env = small_env()
+    with pytest.raises(B.BaselineError, match="population"):
+        B.cem_train(env, population=5, iterations=1)
+    with pytest.raises(B.BaselineError, match="elite_frac"):
+        B.cem_train(env, population=10, elite_frac=1.5, iterations=1)
+    tiny = make_env(TaskConfig(task="station_keeping", episode_length=10),
+                    SimConfig(batch_size=4), seed=0)
+    with pytest.raises(B.BaselineError, match="batch"):
+        B.cem_train(tiny, population=10, iterations=1)
+    with pytest.raises(B.BaselineError, match="shapes"):
+        B.cem_train(env, population=10, iterations=1,
+                    init_policy=B.Policy.zeros(env.obs_dim + 1, env.action_dim))
+    pol = B.Policy.zeros(env.obs_dim, env.action_dim)
+    with pytest.raises(B.BaselineError, match="n_trials"):
+        B.evaluate(pol, env, n_trials=0)
+    with pytest.raises(B.BaselineError, match="match"):
+        B.evaluate(B.Policy.zeros(env.obs_dim + 2, env.action_dim), env, n_trials=1)
+    cell = B.evaluate(pol, small_env(seed=7, batch=30), n_trials=45, label="hold")
+    assert cell.label == "hold" and cell.n_trials == 45 and 0.0 <= cell.success_rate <= 1.0

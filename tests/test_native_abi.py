@@ -33,11 +33,11 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_struct_sizes_and_version():
     lib = N.load()
-    assert lib.uuv_abi_version() == N.ABI_VERSION == 2
-    sizes = (C.c_int64 * 5)()
+    assert lib.uuv_abi_version() == N.ABI_VERSION == 3
+    sizes = (C.c_int64 * 6)()
     lib.uuv_abi_sizes(sizes)
     assert list(sizes) == [C.sizeof(N.Hull), C.sizeof(N.State), C.sizeof(N.Sampler),
-                           C.sizeof(N.Task), C.sizeof(N.TaskIO)]
+                           C.sizeof(N.Task), C.sizeof(N.TaskIO), C.sizeof(N.Policy)]
 
 
 def test_ctx_create_validates_hulls():
