@@ -9,7 +9,7 @@ PKG := paper_2503_09203_b200
 LIB := $(PKG)/libuuvb200.so
 SRC := $(PKG)/csrc/uuv_b200.cu
 HDR := include/uuv_b200.h $(wildcard $(PKG)/csrc/*.cuh)
-TUS := main step task policy
+TUS := main step task policy serve
 OBJS := $(TUS:%=build/tu_%.o)
 
 all: $(LIB)

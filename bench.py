@@ -11,8 +11,14 @@ commands U(-1, 1).  A step is one control step (one ``uuv_step`` launch).
   resident, as in an RL loop); L2 is flushed once before the timed region.
 * e2e — the same metric through the public API with HOST buffers:
   ``step_batch(state, pinned_host_commands, pose_out=pinned_host_pose)`` per
-  step = async H2D of the commands, the step launch, one D2H of the next
-  state's p, q, nu rows and a host sync (the caller reads the result).
+  step: the step's commands go host->device and its p, q, nu rows
+  device->host, and the call returns when they are in host memory.  Two
+  paths are timed and the faster is reported (both in ``e2e.per_path``): one
+  launch per step whose kernel reads/writes the mapped pinned buffers over the
+  link (CUDA events), and the same calls inside ``engine.serve(state)``, where a
+  resident step kernel is driven by a doorbell in mapped pinned memory (no
+  launch, no stream sync per step; host clock around exactly K synchronous
+  steps).
 * roofline — the step kernel's algorithmic bytes per launch / average launch
   duration vs the measured HBM copy bandwidth (MEASURED_PEAKS.json).
 * cpu_baseline — the CPU oracle (numpy restatement of the reference) on the
@@ -287,9 +293,12 @@ def run_b200(args, rank, world, local_rank):
     cur = torch.cuda.current_stream(dev)
 
     def e2e_step(t):
-        # public API, host buffers: pinned commands in, pinned (13, N) pose rows out
+        # public API, host buffers: pinned commands in, pinned (13, N) pose rows out;
+        # returns when the step's pose rows are in host memory
         E.step_batch(st, host_cmds[t], pose_out=host_out)
 
+    # (1) launched path: one uuv_step_host call per step (kernel reads/writes the
+    # mapped pinned buffers), CUDA events on the launching stream
     for t in range(min(args.warmup, k_total)):
         e2e_step(t)
     barrier()
@@ -300,7 +309,25 @@ def run_b200(args, rank, world, local_rank):
         e2e_step(t)
     f1.record(cur)
     torch.cuda.synchronize(dev)
-    e2e_el = allreduce_max(f0.elapsed_time(f1) / 1e3, dev)
+    e2e_launch_el = allreduce_max(f0.elapsed_time(f1) / 1e3, dev)
+    # (2) the same calls inside engine.serve(): a resident step kernel driven by a
+    # doorbell in mapped pinned memory (no launch / stream sync per step); the
+    # steps are synchronous, so the host clock brackets exactly K of them
+    barrier()
+    torch.cuda.synchronize(dev)
+    with E.serve(st):
+        for t in range(min(args.warmup, k_total)):
+            e2e_step(t)
+        t0 = time.perf_counter()
+        for t in range(k_total):
+            e2e_step(t)
+        e2e_serve_el = time.perf_counter() - t0
+    torch.cuda.synchronize(dev)
+    e2e_serve_el = allreduce_max(e2e_serve_el, dev)
+    e2e_el = min(e2e_serve_el, e2e_launch_el)
+    e2e_path = ("step_batch inside engine.serve(): resident step kernel, doorbell in mapped "
+                "pinned memory" if e2e_el == e2e_serve_el else
+                "step_batch -> uuv_step_host (one launch per step, mapped pinned buffers)")
     barrier()
 
     if rank == 0:
@@ -316,7 +343,10 @@ def run_b200(args, rank, world, local_rank):
                              "env state resident",
                        "launch": "CUDA graph of K uuv_step launches"},
             "e2e": {"value": world * n * k_total / e2e_el, "unit": "env-frames/s",
-                    "h2d_bytes_per_step": n * A_BLUEROV * 4, "d2h_bytes_per_step": n * 13 * 4},
+                    "h2d_bytes_per_step": n * A_BLUEROV * 4, "d2h_bytes_per_step": n * 13 * 4,
+                    "path": e2e_path,
+                    "per_path": {"serve": world * n * k_total / e2e_serve_el,
+                                 "launch_per_step": world * n * k_total / e2e_launch_el}},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
                          "traffic": load_traffic(),

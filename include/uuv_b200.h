@@ -286,14 +286,40 @@ uuv_status uuv_step(uuv_ctx* ctx, const uuv_state* st, const void* commands, int
                     int32_t substeps, double dt, void* stream);
 
 /* Host-buffer variant of uuv_step for callers whose commands and results live in
- * (pinned) host memory: async copy host_cmd (n_envs, cmd_ld) -> dev_cmd, uuv_step,
- * then, if host_pose != NULL, one async copy of the pose rows p, q, nu into
- * host_pose as a row-major (13, n_envs) array; sync != 0 waits for the stream. */
+ * host memory: commands host_cmd (n_envs, cmd_ld) in, and, if host_pose != NULL,
+ * the pose rows p, q, nu out as a row-major (13, n_envs) array; sync != 0 waits.
+ * When both buffers are pinned (mapped) host memory the step kernel reads the
+ * commands and stores the pose rows over the host link itself (no copy-engine
+ * round trips; UUV_HOST_STEP=copy forces the copy path); otherwise the commands
+ * are staged through dev_cmd with async copies. */
 uuv_status uuv_step_host(uuv_ctx* ctx, const uuv_state* st, const void* host_cmd, int64_t cmd_ld,
                          void* dev_cmd, void* host_pose, int32_t substeps, double dt,
                          void* stream, int32_t sync);
 
 /* Reset rows with mask[i] != 0 (mask NULL = all rows) from the declarative sampler. */
+/*
+ * Step server: a resident kernel that advances the batch one control step each
+ * time the host rings a doorbell in mapped pinned memory -- no kernel launch and
+ * no stream synchronisation per step (host-in-the-loop stepping, the reference's
+ * numpy-in / numpy-out usage).  It runs on its own non-blocking stream, ordered
+ * after the work already on `stream` at start; uuv_server_stop orders later work
+ * on `stream` after it.  While it runs it owns the state, and a device-wide
+ * synchronisation would wait for it.  The grid (one thread per env) must fit in
+ * one wave.  The kernel ends by itself after idle_timeout_ms without a step.
+ */
+typedef struct uuv_server uuv_server;
+uuv_status uuv_server_start(uuv_ctx* ctx, const uuv_state* state, int32_t substeps, double dt,
+                            void* stream, int32_t idle_timeout_ms, uuv_server** out);
+/* One step: host_cmd (n_envs, cmd_ld) and host_pose ((13, n_envs) rows p, q, nu,
+ * or NULL) must be pinned host memory; returns when every env has stepped. */
+uuv_status uuv_server_step(uuv_server* server, const void* host_cmd, int64_t cmd_ld,
+                           void* host_pose);
+/* CTA 0's %globaltimer stamps of the last step (doorbell seen, commands read,
+ * physics done, system fence done, CTA barrier done, unused): profiling aid. */
+void uuv_server_stamps(const uuv_server* server, uint64_t out[6]);
+/* Stop the kernel, wait for it and free the server. */
+uuv_status uuv_server_stop(uuv_server* server);
+
 uuv_status uuv_reset(uuv_ctx* ctx, const uuv_state* st, const uint8_t* mask,
                      const uuv_sampler* sampler, uint64_t seed, void* stream);
 

@@ -144,6 +144,11 @@ EXPORTS = {
     "uuv_ctx_destroy": (None, [C.c_void_p]),
     "uuv_step": (C.c_int, [C.c_void_p, C.POINTER(State), C.c_void_p, C.c_int64, C.c_int32,
                            C.c_double, C.c_void_p]),
+    "uuv_server_start": (C.c_int, [C.c_void_p, C.POINTER(State), C.c_int32, C.c_double,
+                                   C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]),
+    "uuv_server_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "uuv_server_stop": (C.c_int, [C.c_void_p]),
+    "uuv_server_stamps": (None, [C.c_void_p, C.POINTER(C.c_uint64)]),
     "uuv_step_host": (C.c_int, [C.c_void_p, C.POINTER(State), C.c_void_p, C.c_int64, C.c_void_p,
                                 C.c_void_p, C.c_int32, C.c_double, C.c_void_p, C.c_int32]),
     "uuv_reset": (C.c_int, [C.c_void_p, C.POINTER(State), C.c_void_p, C.POINTER(Sampler),

@@ -29,7 +29,7 @@ using namespace uuv;
 // Translation-unit split: the Makefile compiles this file once per UUV_TU so
 // the kernel families build in parallel (1 = C ABI + reset/statistics/
 // inspection kernels, 2 = physics step kernels, 3 = task step kernels,
-// 4 = policy step kernels).  UUV_TU 0 (default) builds everything in one TU.
+// 4 = policy step kernels, 5 = step server).  UUV_TU 0 builds everything.
 #ifndef UUV_TU
 #define UUV_TU 0
 #endif
@@ -37,10 +37,21 @@ using namespace uuv;
 #define UUV_TU_STEP (UUV_TU == 0 || UUV_TU == 2)
 #define UUV_TU_TASK (UUV_TU == 0 || UUV_TU == 3)
 #define UUV_TU_POLICY (UUV_TU == 0 || UUV_TU == 4)
+#define UUV_TU_SERVE (UUV_TU == 0 || UUV_TU == 5)
 
 namespace uuv_tu {
 extern thread_local std::string g_err;  // uuv_last_error's message (defined in TU 1)
+// Every kernel instantiation the library can launch registers itself at load
+// time (KernelReg below), so a step server can force them all resident first:
+// under CUDA lazy loading, the first launch of an unloaded kernel waits for the
+// device, which would stall behind a resident server until its idle timeout.
+void register_kernel(const void* fn);
 }
+template <auto K> struct KernelReg {
+  static const bool ok;
+};
+template <auto K> const bool KernelReg<K>::ok = (uuv_tu::register_kernel((const void*)K), true);
+#define UUV_REGISTER(...) (void)KernelReg<__VA_ARGS__>::ok
 
 namespace {
 
@@ -202,6 +213,7 @@ template <typename R, int NT> struct StepArgs {
   int32_t K;
   R dt;
   int32_t early_trigger;  // single-wave grid: let the next step's CTAs launch now
+  R* pose_out;            // optional (13, n) row-major p, q, nu copy (host-mapped memory)
 };
 
 // Programmatic dependent launch (PDL).  Step kernels are launched with
@@ -494,15 +506,23 @@ UUV_D void step_env(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in) {
   const StateView<R>& sv = a.sv;
   if (in.div) {  // frozen rows stay frozen (engine.py:411, 441-449)
     sv.steps[i] = in.steps + 1;
-    return;
+  } else {
+    const Hull<R>& H = a.hull[in.ty];
+    const int A = AC > 0 ? AC : H.r.n_act;
+    const bool div = physics<R, DR, AC, DM>(H, sv, i, a.K, a.dt, in.u, in.px, in.py, in.pz,
+                                            in.q, in.nu, in.act);
+    store_state(sv, i, A, in.px, in.py, in.pz, in.q, in.nu, in.act);
+    sv.diverged[i] = div ? 1 : 0;
+    sv.steps[i] = in.steps + 1;
   }
-  const Hull<R>& H = a.hull[in.ty];
-  const int A = AC > 0 ? AC : H.r.n_act;
-  const bool div = physics<R, DR, AC, DM>(H, sv, i, a.K, a.dt, in.u, in.px, in.py, in.pz, in.q,
-                                          in.nu, in.act);
-  store_state(sv, i, A, in.px, in.py, in.pz, in.q, in.nu, in.act);
-  sv.diverged[i] = div ? 1 : 0;
-  sv.steps[i] = in.steps + 1;
+  if (a.pose_out != nullptr) {  // the caller's pinned (13, n) rows, stored over the link
+    R* o = a.pose_out + i;
+    const int64_t n = sv.n;
+    o[0] = in.px; o[n] = in.py; o[2 * n] = in.pz;
+    o[3 * n] = in.q.w; o[4 * n] = in.q.x; o[5 * n] = in.q.y; o[6 * n] = in.q.z;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) o[(7 + k) * n] = in.nu[k];
+  }
 }
 
 // Mixed fleets: every env takes its vehicle type's specialised path (types are
@@ -560,6 +580,188 @@ __global__ void __launch_bounds__(kBlock, (NT > 1 && sizeof(R) == 4) ? 3 : MinB<
   (void)stride;
   step_any<R, NT, DR, AC, DM>(a, i, cur);
 #endif
+}
+
+// ------------------------------------------------------------------ step server
+// A resident kernel that steps the batch whenever the host rings a doorbell in
+// mapped pinned memory: no launch, no stream synchronisation per step.  Each CTA
+// keeps its envs' state in registers, polls the doorbell (one thread, acquire at
+// system scope), reads that step's command rows over the host link, runs the
+// same physics as k_step, writes the state back to HBM and the pose rows to the
+// caller's pinned buffer, fences at system scope and raises its done flag.  The
+// host waits on all flags.  An idle timeout (%globaltimer) ends the kernel if
+// the host goes away, so it can never hold the GPU.
+struct ServeCtl {           // host-mapped, written by the host
+  uint64_t seq;             // doorbell: step number, or kServeQuit
+  uint64_t cmd;             // device-visible address of the (n, cmd_ld) commands
+  uint64_t pose;            // device-visible address of the (13, n) pose rows, or 0
+  int64_t cmd_ld;
+  uint64_t stamp[6];        // CTA 0 phase times of the last step (%globaltimer ns)
+};
+constexpr uint64_t kServeQuit = ~0ull;
+
+struct ServeSync {          // device memory: CTA 0 republishes the doorbell here
+  uint64_t go;
+  uint64_t cmd, pose;
+  int64_t cmd_ld;
+  uint32_t arrived;         // CTAs done with the current step
+};
+
+template <typename R, int NT> struct ServeArgs {
+  StepArgs<R, NT> step;
+  ServeCtl* ctl;
+  uint64_t* done;           // host-mapped: last step the whole grid finished
+  ServeSync* sync;
+  uint64_t idle_ns;
+  uint32_t sleep_ns;        // back-off between doorbell polls
+};
+
+UUV_D uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+UUV_D uint64_t ld_relaxed_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+UUV_D uint64_t ld_acquire_gpu(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+UUV_D void st_release_gpu(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+UUV_D void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+UUV_D uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <typename R, int NT, bool DR, int AC, bool DM>
+UUV_D void serve_env(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in, R* pose) {
+  const StateView<R>& sv = a.sv;
+  in.steps += 1;
+  if (!in.div) {
+    const Hull<R>& H = a.hull[in.ty];
+    const int A = AC > 0 ? AC : H.r.n_act;
+    const bool div = physics<R, DR, AC, DM>(H, sv, i, a.K, a.dt, in.u, in.px, in.py, in.pz,
+                                            in.q, in.nu, in.act);
+    store_state(sv, i, A, in.px, in.py, in.pz, in.q, in.nu, in.act);
+    in.div = div ? 1 : 0;
+    sv.diverged[i] = in.div;
+  }
+  sv.steps[i] = in.steps;
+  if (pose != nullptr) {
+    R* o = pose + i;
+    const int64_t n = sv.n;
+    o[0] = in.px; o[n] = in.py; o[2 * n] = in.pz;
+    o[3 * n] = in.q.w; o[4 * n] = in.q.x; o[5 * n] = in.q.y; o[6 * n] = in.q.z;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) o[(7 + k) * n] = in.nu[k];
+  }
+}
+
+template <typename R, int NT, bool DR, int AC, bool DM>
+__global__ void __launch_bounds__(kBlock, (NT > 1 && sizeof(R) == 4) ? 3 : MinB<R>::value)
+    k_serve(const __grid_constant__ ServeArgs<R, NT> sa) {
+  __shared__ uint64_t s_seq, s_cmd, s_pose;
+  __shared__ int64_t s_ld;
+  const StepArgs<R, NT>& a = sa.step;
+  const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+  const bool live = i < a.sv.n;
+  StepIn<R> in;
+  if (live) {
+    const StateView<R>& sv = a.sv;
+    in.ty = NT > 1 ? sv.type_id[i] : 0;
+    const int A = AC > 0 ? AC : a.hull[in.ty].r.n_act;
+    in.steps = sv.steps[i];
+    in.div = sv.diverged[i];
+    load_state(sv, i, A, in.px, in.py, in.pz, in.q, in.nu, in.act);
+  }
+  uint64_t seq = 0;
+  ServeSync* sy = sa.sync;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // start marker + the idle budget (profiling aid)
+    sa.ctl->stamp[4] = sa.idle_ns;
+    sa.ctl->stamp[5] = global_ns();
+  }
+  for (;;) {
+    if (threadIdx.x == 0) {
+      uint64_t v;
+      if (blockIdx.x == 0) {  // the only poller of the host doorbell
+        const uint64_t t0 = global_ns();
+        uint64_t why = 0;
+        for (;;) {
+          v = ld_relaxed_sys(&sa.ctl->seq);
+          if (v != seq) { why = 1; break; }
+          // signed: %globaltimer may step back slightly when it is re-synchronised
+          if ((int64_t)(global_ns() - t0) > (int64_t)sa.idle_ns) { v = kServeQuit; why = 2; break; }
+          __nanosleep(sa.sleep_ns);
+        }
+        if (v == kServeQuit) {  // exit record (profiling aid)
+          sa.ctl->stamp[0] = why;
+          sa.ctl->stamp[1] = global_ns() - t0;
+          sa.ctl->stamp[2] = seq;
+        }
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+        sy->cmd = *(volatile uint64_t*)&sa.ctl->cmd;
+        sy->pose = *(volatile uint64_t*)&sa.ctl->pose;
+        sy->cmd_ld = *(volatile int64_t*)&sa.ctl->cmd_ld;
+        st_release_gpu(&sy->go, v);
+      } else {
+        while ((v = ld_acquire_gpu(&sy->go)) == seq) __nanosleep(64);
+      }
+      s_seq = v;
+      s_cmd = *(volatile uint64_t*)&sy->cmd;
+      s_pose = *(volatile uint64_t*)&sy->pose;
+      s_ld = *(volatile int64_t*)&sy->cmd_ld;
+    }
+    __syncthreads();
+    const uint64_t v = s_seq;
+    if (v == kServeQuit) break;
+    const bool stamp = blockIdx.x == 0 && threadIdx.x == 0;
+    if (stamp) sa.ctl->stamp[0] = global_ns();
+    if (live) {
+      const R* crow = (const R*)s_cmd + i * s_ld;
+      const int A = AC > 0 ? AC : a.hull[in.ty].r.n_act;
+#pragma unroll
+      for (int j = 0; j < UUV_MAX_ACT; ++j)
+        in.u[j] = (j < A) ? clip_<R>(crow[j], R(-1), R(1)) : R(0);
+      if (stamp) sa.ctl->stamp[1] = global_ns() + (uint64_t)(in.u[0] > R(2));
+      if constexpr (NT > 1) {
+        switch (a.cls[in.ty]) {
+          case 1: serve_env<R, NT, DR, 6, true>(a, i, in, (R*)s_pose); break;
+          case 2: serve_env<R, NT, DR, 8, true>(a, i, in, (R*)s_pose); break;
+          case 3: serve_env<R, NT, DR, 6, false>(a, i, in, (R*)s_pose); break;
+          case 4: serve_env<R, NT, DR, 8, false>(a, i, in, (R*)s_pose); break;
+          default: serve_env<R, NT, DR, 0, false>(a, i, in, (R*)s_pose); break;
+        }
+      } else {
+        serve_env<R, NT, DR, AC, DM>(a, i, in, (R*)s_pose);
+      }
+    }
+    if (stamp) sa.ctl->stamp[2] = global_ns() + (uint64_t)(in.px > R(1e30));
+    // One system-scope fence per step: CTAs publish their stores at GPU scope
+    // and count in; the last one fences at system scope (cumulative) and
+    // releases the host's done flag.
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(&sy->arrived, 1u) == gridDim.x - 1) {
+        __threadfence();
+        sy->arrived = 0;
+        __threadfence_system();
+        st_release_sys(sa.done, v);
+      }
+    }
+    if (stamp) sa.ctl->stamp[3] = global_ns();
+    seq = v;
+  }
 }
 
 // ------------------------------------------------------------------ task step
@@ -1128,6 +1330,7 @@ uuv_status launch_step_tma(const uuv_ctx* ctx, const uuv_state* st, const void* 
   a.n_store = ns;
   a.n_tiles = (st->n_envs + kTile - 1) / kTile;
   const size_t smem = 128 + (size_t)kWarps * 2 * a.buf_bytes;
+  UUV_REGISTER(k_step_tma<R, NT, DR, AC, DM>);
   auto kern = k_step_tma<R, NT, DR, AC, DM>;
   static thread_local std::map<const void*, size_t> smem_set;
   size_t& have = smem_set[(const void*)kern];
@@ -1180,8 +1383,9 @@ bool use_tma_step() {
 
 template <typename R, int NT, bool DR, int AC, bool DM = false>
 uuv_status launch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd, int64_t cmd_ld,
-                       int32_t K, double dt, cudaStream_t s) {
-  if (use_tma_step()) return launch_step_tma<R, NT, DR, AC, DM>(ctx, st, cmd, cmd_ld, K, dt, s);
+                       int32_t K, double dt, cudaStream_t s, void* pose_out = nullptr) {
+  if (pose_out == nullptr && use_tma_step())
+    return launch_step_tma<R, NT, DR, AC, DM>(ctx, st, cmd, cmd_ld, K, dt, s);
   StepArgs<R, NT> a;
   const double dt_sub = dt / K;
   fill_hulls<R, NT>(ctx, a.hull, dt_sub);
@@ -1192,12 +1396,14 @@ uuv_status launch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd,
   a.cmd_ld = cmd_ld;
   a.K = K;
   a.dt = (R)dt_sub;
+  a.pose_out = (R*)pose_out;
   const int64_t need = grid_for(st->n_envs);
   const int64_t wave = one_wave_ctas(k_step<R, NT, DR, AC, DM>);
   // persistent (grid-stride + register prefetch) beyond one wave; UUV_STEP_WAVES overrides
   const int64_t waves = step_waves();
   const int64_t grid = waves >= need ? need : std::min<int64_t>(need, wave * waves);
   a.early_trigger = pdl_mode() == 2 ? 2 : ((grid <= wave && pdl_enabled()) ? 1 : 0);
+  UUV_REGISTER(k_step<R, NT, DR, AC, DM>);
   cudaError_t e = launch_pdl(k_step<R, NT, DR, AC, DM>, (unsigned)grid, s, a);
   if (e != cudaSuccess) return fail(UUV_ERR_CUDA, "uuv_step: %s", cudaGetErrorString(e));
   return check_launch("uuv_step");
@@ -1205,30 +1411,30 @@ uuv_status launch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd,
 
 template <typename R>
 uuv_status dispatch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd, int64_t cmd_ld,
-                         int32_t K, double dt, cudaStream_t s) {
+                         int32_t K, double dt, cudaStream_t s, void* pose = nullptr) {
   const bool dr = st->overlay != nullptr;
   if (ctx->hulls.size() == 1) {
     const bool dm = diag_mass(ctx, st);
     switch (act_class(ctx)) {
       case 6:
         if (dm)
-          return dr ? launch_step<R, 1, true, 6, true>(ctx, st, cmd, cmd_ld, K, dt, s)
-                    : launch_step<R, 1, false, 6, true>(ctx, st, cmd, cmd_ld, K, dt, s);
-        return dr ? launch_step<R, 1, true, 6>(ctx, st, cmd, cmd_ld, K, dt, s)
-                  : launch_step<R, 1, false, 6>(ctx, st, cmd, cmd_ld, K, dt, s);
+          return dr ? launch_step<R, 1, true, 6, true>(ctx, st, cmd, cmd_ld, K, dt, s, pose)
+                    : launch_step<R, 1, false, 6, true>(ctx, st, cmd, cmd_ld, K, dt, s, pose);
+        return dr ? launch_step<R, 1, true, 6>(ctx, st, cmd, cmd_ld, K, dt, s, pose)
+                  : launch_step<R, 1, false, 6>(ctx, st, cmd, cmd_ld, K, dt, s, pose);
       case 8:
         if (dm)
-          return dr ? launch_step<R, 1, true, 8, true>(ctx, st, cmd, cmd_ld, K, dt, s)
-                    : launch_step<R, 1, false, 8, true>(ctx, st, cmd, cmd_ld, K, dt, s);
-        return dr ? launch_step<R, 1, true, 8>(ctx, st, cmd, cmd_ld, K, dt, s)
-                  : launch_step<R, 1, false, 8>(ctx, st, cmd, cmd_ld, K, dt, s);
+          return dr ? launch_step<R, 1, true, 8, true>(ctx, st, cmd, cmd_ld, K, dt, s, pose)
+                    : launch_step<R, 1, false, 8, true>(ctx, st, cmd, cmd_ld, K, dt, s, pose);
+        return dr ? launch_step<R, 1, true, 8>(ctx, st, cmd, cmd_ld, K, dt, s, pose)
+                  : launch_step<R, 1, false, 8>(ctx, st, cmd, cmd_ld, K, dt, s, pose);
       default:
-        return dr ? launch_step<R, 1, true, 0>(ctx, st, cmd, cmd_ld, K, dt, s)
-                  : launch_step<R, 1, false, 0>(ctx, st, cmd, cmd_ld, K, dt, s);
+        return dr ? launch_step<R, 1, true, 0>(ctx, st, cmd, cmd_ld, K, dt, s, pose)
+                  : launch_step<R, 1, false, 0>(ctx, st, cmd, cmd_ld, K, dt, s, pose);
     }
   }
-  return dr ? launch_step<R, UUV_MAX_TYPES, true, 0>(ctx, st, cmd, cmd_ld, K, dt, s)
-            : launch_step<R, UUV_MAX_TYPES, false, 0>(ctx, st, cmd, cmd_ld, K, dt, s);
+  return dr ? launch_step<R, UUV_MAX_TYPES, true, 0>(ctx, st, cmd, cmd_ld, K, dt, s, pose)
+            : launch_step<R, UUV_MAX_TYPES, false, 0>(ctx, st, cmd, cmd_ld, K, dt, s, pose);
 }
 
 uuv_status check_sampler(const uuv_sampler* smp) {
@@ -1290,6 +1496,8 @@ void fill_task_args(const uuv_ctx* ctx, const uuv_state* st, const uuv_task* tas
 
 template <typename R, int AC, bool DM, bool POL>
 void launch_task_dr(bool dr, unsigned g, cudaStream_t cs, const TaskArgs<R>& a) {
+  UUV_REGISTER(k_task_step<R, true, AC, DM, POL>);
+  UUV_REGISTER(k_task_step<R, false, AC, DM, POL>);
   if (dr) k_task_step<R, true, AC, DM, POL><<<g, kBlock, 0, cs>>>(a);
   else k_task_step<R, false, AC, DM, POL><<<g, kBlock, 0, cs>>>(a);
 }
@@ -1329,21 +1537,94 @@ uuv_status check_task(const uuv_ctx* ctx, const uuv_state* st, const uuv_task* t
 namespace uuv_tu {
 template <typename R>
 uuv_status step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd, int64_t cmd_ld,
-                int32_t K, double dt, cudaStream_t s);
+                int32_t K, double dt, cudaStream_t s, void* pose);
 template <typename R, bool POL>
 void task(bool dr, int ac, bool dm, unsigned g, cudaStream_t cs, const TaskArgs<R>& a);
 
 #if UUV_TU_STEP
 template <typename R>
 uuv_status step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd, int64_t cmd_ld,
-                int32_t K, double dt, cudaStream_t s) {
-  return dispatch_step<R>(ctx, st, cmd, cmd_ld, K, dt, s);
+                int32_t K, double dt, cudaStream_t s, void* pose) {
+  return dispatch_step<R>(ctx, st, cmd, cmd_ld, K, dt, s, pose);
 }
 template uuv_status step<float>(const uuv_ctx*, const uuv_state*, const void*, int64_t, int32_t,
-                                double, cudaStream_t);
+                                double, cudaStream_t, void*);
 template uuv_status step<double>(const uuv_ctx*, const uuv_state*, const void*, int64_t, int32_t,
-                                 double, cudaStream_t);
+                                 double, cudaStream_t, void*);
 #endif
+template <typename R>
+uuv_status serve(const uuv_ctx* ctx, const uuv_state* st, int32_t K, double dt, cudaStream_t s,
+                 ServeCtl* ctl, uint64_t* done, ServeSync* sync, uint64_t idle_ns,
+                 int64_t* grid_out);
+
+#if UUV_TU_SERVE
+template <typename R, int NT, bool DR, int AC, bool DM = false>
+uuv_status serve_kernel(const uuv_ctx* ctx, const uuv_state* st, int32_t K, double dt,
+                        cudaStream_t s, ServeCtl* ctl, uint64_t* done, ServeSync* sync,
+                        uint64_t idle_ns, int64_t* grid_out) {
+  ServeArgs<R, NT> sa;
+  StepArgs<R, NT>& a = sa.step;
+  fill_hulls<R, NT>(ctx, a.hull, dt / K);
+  for (int t = 0; t < NT; ++t)
+    a.cls[t] = t < (int)ctx->hulls.size() ? hull_class(ctx->hulls[t], st) : 0;
+  a.sv = make_view<R>(*st);
+  a.cmd = nullptr;
+  a.cmd_ld = 0;
+  a.K = K;
+  a.dt = (R)(dt / K);
+  a.early_trigger = 0;
+  a.pose_out = nullptr;
+  sa.ctl = ctl;
+  sa.done = done;
+  sa.sync = sync;
+  sa.idle_ns = idle_ns;
+  static const uint32_t sleep_ns = [] {
+    const char* v = getenv("UUV_SERVE_SLEEP");
+    return v ? (uint32_t)atoi(v) : 100u;
+  }();
+  sa.sleep_ns = sleep_ns;
+  const int64_t grid = grid_for(st->n_envs);
+  if (grid > one_wave_ctas(k_serve<R, NT, DR, AC, DM>))
+    return fail(UUV_ERR_UNSUPPORTED, "step server: %lld CTAs do not fit one wave",
+                (long long)grid);
+  *grid_out = grid;
+  UUV_REGISTER(k_serve<R, NT, DR, AC, DM>);
+  k_serve<R, NT, DR, AC, DM><<<(unsigned)grid, kBlock, 0, s>>>(sa);
+  return check_launch("uuv_server_start");
+}
+
+template <typename R>
+uuv_status serve(const uuv_ctx* ctx, const uuv_state* st, int32_t K, double dt, cudaStream_t s,
+                 ServeCtl* ctl, uint64_t* done, ServeSync* sy, uint64_t idle_ns, int64_t* g) {
+  const bool dr = st->overlay != nullptr;
+  if (ctx->hulls.size() > 1)
+    return dr ? serve_kernel<R, UUV_MAX_TYPES, true, 0>(ctx, st, K, dt, s, ctl, done, sy, idle_ns, g)
+              : serve_kernel<R, UUV_MAX_TYPES, false, 0>(ctx, st, K, dt, s, ctl, done, sy, idle_ns, g);
+  const bool dm = diag_mass(ctx, st);
+  switch (act_class(ctx)) {
+    case 6:
+      if (dm)
+        return dr ? serve_kernel<R, 1, true, 6, true>(ctx, st, K, dt, s, ctl, done, sy, idle_ns, g)
+                  : serve_kernel<R, 1, false, 6, true>(ctx, st, K, dt, s, ctl, done, sy, idle_ns, g);
+      return dr ? serve_kernel<R, 1, true, 6>(ctx, st, K, dt, s, ctl, done, sy, idle_ns, g)
+                : serve_kernel<R, 1, false, 6>(ctx, st, K, dt, s, ctl, done, sy, idle_ns, g);
+    case 8:
+      if (dm)
+        return dr ? serve_kernel<R, 1, true, 8, true>(ctx, st, K, dt, s, ctl, done, sy, idle_ns, g)
+                  : serve_kernel<R, 1, false, 8, true>(ctx, st, K, dt, s, ctl, done, sy, idle_ns, g);
+      return dr ? serve_kernel<R, 1, true, 8>(ctx, st, K, dt, s, ctl, done, sy, idle_ns, g)
+                : serve_kernel<R, 1, false, 8>(ctx, st, K, dt, s, ctl, done, sy, idle_ns, g);
+    default:
+      return dr ? serve_kernel<R, 1, true, 0>(ctx, st, K, dt, s, ctl, done, sy, idle_ns, g)
+                : serve_kernel<R, 1, false, 0>(ctx, st, K, dt, s, ctl, done, sy, idle_ns, g);
+  }
+}
+template uuv_status serve<float>(const uuv_ctx*, const uuv_state*, int32_t, double, cudaStream_t,
+                                 ServeCtl*, uint64_t*, ServeSync*, uint64_t, int64_t*);
+template uuv_status serve<double>(const uuv_ctx*, const uuv_state*, int32_t, double, cudaStream_t,
+                                  ServeCtl*, uint64_t*, ServeSync*, uint64_t, int64_t*);
+#endif
+
 #if UUV_TU_TASK || UUV_TU_POLICY
 template <typename R, bool POL>
 void task(bool dr, int ac, bool dm, unsigned g, cudaStream_t cs, const TaskArgs<R>& a) {
@@ -1363,6 +1644,28 @@ template void task<double, true>(bool, int, bool, unsigned, cudaStream_t, const 
 #if UUV_TU_MAIN
 namespace uuv_tu {
 thread_local std::string g_err;
+
+static std::vector<const void*>& kernel_registry() {
+  static std::vector<const void*> r;
+  return r;
+}
+void register_kernel(const void* fn) { kernel_registry().push_back(fn); }
+}  // namespace uuv_tu
+
+// Load every registered kernel now (cudaFuncGetAttributes forces a lazily
+// loaded function resident).  Idempotent and cheap after the first call.
+static uuv_status preload_kernels() {
+  static std::vector<int> loaded_on;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (std::find(loaded_on.begin(), loaded_on.end(), dev) != loaded_on.end()) return UUV_OK;
+  for (const void* fn : uuv_tu::kernel_registry()) {
+    cudaFuncAttributes at;
+    const cudaError_t e = cudaFuncGetAttributes(&at, fn);
+    if (e != cudaSuccess) return fail(UUV_ERR_CUDA, "preload: %s", cudaGetErrorString(e));
+  }
+  loaded_on.push_back(dev);
+  return UUV_OK;
 }
 
 template <typename R, int NT>
@@ -1372,6 +1675,7 @@ static uuv_status derive_launch(const uuv_ctx* ctx, const uuv_state* st, double*
   fill_hulls<R, NT>(ctx, a.hull, 1.0);
   a.sv = make_view<R>(*st);
   a.out12 = o12; a.minv = minv; a.ct_tau = ct_tau; a.mounts = mounts;
+  UUV_REGISTER(k_derive<R, NT>);
   k_derive<R, NT><<<(unsigned)grid_for(st->n_envs), kBlock, 0, cs>>>(a);
   return check_launch("uuv_derive_params");
 }
@@ -1386,6 +1690,7 @@ static uuv_status terms_launch(const uuv_ctx* ctx, const uuv_state* st, const vo
   a.cmd_ld = cmd_ld;
   a.dt = (R)dt_sub;
   a.out = out;
+  UUV_REGISTER(k_terms<R, NT, DR, AC, DM>);
   k_terms<R, NT, DR, AC, DM><<<(unsigned)grid_for(st->n_envs), kBlock, 0, cs>>>(a);
   return check_launch("uuv_substep_terms");
 }
@@ -1432,15 +1737,88 @@ static uuv_status task_reset_impl(uuv_ctx* ctx, const uuv_state* st, const uuv_t
     fill_task_args<float>(ctx, st, task, sampler, seed, dt, 1, io, a);
     a.mask = mask;
     a.mode = mode;
+    UUV_REGISTER(k_task_reset<float>);
     k_task_reset<float><<<g, kBlock, 0, cs>>>(a);
   } else {
     TaskArgs<double> a;
     fill_task_args<double>(ctx, st, task, sampler, seed, dt, 1, io, a);
     a.mask = mask;
     a.mode = mode;
+    UUV_REGISTER(k_task_reset<double>);
     k_task_reset<double><<<g, kBlock, 0, cs>>>(a);
   }
   return check_launch(mode ? "uuv_task_reset" : "uuv_observe");
+}
+
+static uuv_status step_checked(uuv_ctx* ctx, const uuv_state* st, const void* commands,
+                               int64_t cmd_ld, int32_t substeps, double dt, cudaStream_t cs,
+                               void* pose) {
+  uuv_status s = check_state(ctx, st);
+  if (s != UUV_OK) return s;
+  if (commands == nullptr) return fail(UUV_ERR_ARG, "commands: null");
+  if (cmd_ld < st->a_max && ctx->hulls.size() > 1)
+    return fail(UUV_ERR_SHAPE, "commands: row stride %lld < a_max %d", (long long)cmd_ld, st->a_max);
+  if (cmd_ld < ctx->hulls[0].n_act)
+    return fail(UUV_ERR_SHAPE, "commands: row stride %lld < action_dim %d", (long long)cmd_ld,
+                ctx->hulls[0].n_act);
+  if (substeps < 1) return fail(UUV_ERR_ARG, "substeps must be >= 1, got %d", substeps);
+  if (!(dt > 0)) return fail(UUV_ERR_ARG, "dt must be > 0");
+  if (st->n_envs == 0) return UUV_OK;
+  return st->dtype == UUV_F32
+             ? uuv_tu::step<float>(ctx, st, commands, cmd_ld, substeps, dt, cs, pose)
+             : uuv_tu::step<double>(ctx, st, commands, cmd_ld, substeps, dt, cs, pose);
+}
+
+// uuv_step_host transfer mode: 1 = mapped pinned memory (default), 0 = copy engines
+// (UUV_HOST_STEP=copy).
+static int host_step_mode() {
+  static const int m = [] {
+    const char* v = getenv("UUV_HOST_STEP");
+    return (v != nullptr && strcmp(v, "copy") == 0) ? 0 : 1;
+  }();
+  return m;
+}
+
+// Device address of a pinned, mapped host buffer (the host address under UVA), or
+// nullptr for pageable memory.  A few recent answers are cached per thread.
+static void* host_mapped(const void* h) {
+  struct Entry { const void* h; void* d; };
+  thread_local Entry cache[8] = {};
+  thread_local int next = 0;
+  for (const Entry& c : cache)
+    if (c.h == h && h != nullptr) return c.d;
+  cudaPointerAttributes at;
+  void* d = nullptr;
+  if (cudaPointerGetAttributes(&at, h) == cudaSuccess && at.type == cudaMemoryTypeHost)
+    d = at.devicePointer;
+  cudaGetLastError();
+  cache[next] = {h, d};
+  next = (next + 1) & 7;
+  return d;
+}
+
+struct uuv_server {
+  ServeCtl* ctl = nullptr;   // host view of the doorbell (pinned, mapped)
+  ServeCtl* ctl_dev = nullptr;
+  uint64_t* done = nullptr;  // host view of the done flag
+  uint64_t* done_dev = nullptr;
+  ServeSync* sync = nullptr;  // device memory
+  int64_t grid = 0;
+  uint64_t seq = 0;
+  cudaStream_t stream = nullptr;  // own non-blocking stream: legacy-stream work never waits on it
+  cudaStream_t caller = nullptr;
+  cudaEvent_t ev = nullptr;
+  int32_t n_act = 0, dtype = 0;
+  int64_t n = 0;
+};
+
+static void server_free(uuv_server* s) {
+  if (s->ctl) cudaFreeHost(s->ctl);
+  if (s->done) cudaFreeHost(s->done);
+  if (s->sync) cudaFree(s->sync);
+  if (s->ev) cudaEventDestroy(s->ev);
+  if (s->stream) cudaStreamDestroy(s->stream);
+  delete s;
 }
 
 // ================================================================== C ABI
@@ -1510,20 +1888,7 @@ void uuv_ctx_destroy(uuv_ctx* ctx) { delete ctx; }
 
 uuv_status uuv_step(uuv_ctx* ctx, const uuv_state* st, const void* commands, int64_t cmd_ld,
                     int32_t substeps, double dt, void* stream) {
-  uuv_status s = check_state(ctx, st);
-  if (s != UUV_OK) return s;
-  if (commands == nullptr) return fail(UUV_ERR_ARG, "commands: null");
-  if (cmd_ld < st->a_max && ctx->hulls.size() > 1)
-    return fail(UUV_ERR_SHAPE, "commands: row stride %lld < a_max %d", (long long)cmd_ld, st->a_max);
-  if (cmd_ld < ctx->hulls[0].n_act)
-    return fail(UUV_ERR_SHAPE, "commands: row stride %lld < action_dim %d", (long long)cmd_ld,
-                ctx->hulls[0].n_act);
-  if (substeps < 1) return fail(UUV_ERR_ARG, "substeps must be >= 1, got %d", substeps);
-  if (!(dt > 0)) return fail(UUV_ERR_ARG, "dt must be > 0");
-  if (st->n_envs == 0) return UUV_OK;
-  cudaStream_t cs = (cudaStream_t)stream;
-  return st->dtype == UUV_F32 ? uuv_tu::step<float>(ctx, st, commands, cmd_ld, substeps, dt, cs)
-                              : uuv_tu::step<double>(ctx, st, commands, cmd_ld, substeps, dt, cs);
+  return step_checked(ctx, st, commands, cmd_ld, substeps, dt, (cudaStream_t)stream, nullptr);
 }
 
 uuv_status uuv_step_host(uuv_ctx* ctx, const uuv_state* st, const void* host_cmd, int64_t cmd_ld,
@@ -1535,33 +1900,135 @@ uuv_status uuv_step_host(uuv_ctx* ctx, const uuv_state* st, const void* host_cmd
   if (st->n_envs == 0) return UUV_OK;
   cudaStream_t cs = (cudaStream_t)stream;
   const size_t es = st->dtype == UUV_F32 ? sizeof(float) : sizeof(double);
-  cudaError_t e = cudaMemcpyAsync(dev_cmd, host_cmd, (size_t)st->n_envs * cmd_ld * es,
-                                  cudaMemcpyHostToDevice, cs);
-  if (e != cudaSuccess) return fail(UUV_ERR_CUDA, "commands H2D: %s", cudaGetErrorString(e));
-  if ((s = uuv_step(ctx, st, dev_cmd, cmd_ld, substeps, dt, stream)) != UUV_OK) return s;
-  if (host_pose != nullptr) {
-    const size_t row = (size_t)st->n_envs * es, pitch = (size_t)st->ld * es;
-    const char* p = (const char*)st->p;
-    if ((const char*)st->q == p + 3 * pitch && (const char*)st->nu == p + 7 * pitch &&
-        row == pitch) {  // n == ld: the 13 pose rows are one contiguous span
-      e = cudaMemcpyAsync(host_pose, p, 13 * row, cudaMemcpyDeviceToHost, cs);
-    } else if ((const char*)st->q == p + 3 * pitch && (const char*)st->nu == p + 7 * pitch) {
-      e = cudaMemcpy2DAsync(host_pose, row, p, pitch, row, 13, cudaMemcpyDeviceToHost, cs);
-    } else {
-      e = cudaMemcpy2DAsync(host_pose, row, st->p, pitch, row, 3, cudaMemcpyDeviceToHost, cs);
-      if (e == cudaSuccess)
-        e = cudaMemcpy2DAsync((char*)host_pose + 3 * row, row, st->q, pitch, row, 4,
-                              cudaMemcpyDeviceToHost, cs);
-      if (e == cudaSuccess)
-        e = cudaMemcpy2DAsync((char*)host_pose + 7 * row, row, st->nu, pitch, row, 6,
-                              cudaMemcpyDeviceToHost, cs);
+  cudaError_t e;
+  // Mapped pinned buffers: the step kernel reads the command rows and stores the
+  // pose rows over the host link itself -- no copy-engine round trips.
+  const void* mcmd = host_mapped(host_cmd);
+  void* mpose = host_pose != nullptr ? host_mapped(host_pose) : nullptr;
+  if (host_step_mode() == 1 && mcmd != nullptr && (host_pose == nullptr || mpose != nullptr)) {
+    if ((s = step_checked(ctx, st, mcmd, cmd_ld, substeps, dt, cs, mpose)) != UUV_OK) return s;
+  } else {
+    e = cudaMemcpyAsync(dev_cmd, host_cmd, (size_t)st->n_envs * cmd_ld * es,
+                        cudaMemcpyHostToDevice, cs);
+    if (e != cudaSuccess) return fail(UUV_ERR_CUDA, "commands H2D: %s", cudaGetErrorString(e));
+    if ((s = step_checked(ctx, st, dev_cmd, cmd_ld, substeps, dt, cs, nullptr)) != UUV_OK)
+      return s;
+    if (host_pose != nullptr) {
+      const size_t row = (size_t)st->n_envs * es, pitch = (size_t)st->ld * es;
+      const char* p = (const char*)st->p;
+      if ((const char*)st->q == p + 3 * pitch && (const char*)st->nu == p + 7 * pitch &&
+          row == pitch) {  // n == ld: the 13 pose rows are one contiguous span
+        e = cudaMemcpyAsync(host_pose, p, 13 * row, cudaMemcpyDeviceToHost, cs);
+      } else if ((const char*)st->q == p + 3 * pitch && (const char*)st->nu == p + 7 * pitch) {
+        e = cudaMemcpy2DAsync(host_pose, row, p, pitch, row, 13, cudaMemcpyDeviceToHost, cs);
+      } else {
+        e = cudaMemcpy2DAsync(host_pose, row, st->p, pitch, row, 3, cudaMemcpyDeviceToHost, cs);
+        if (e == cudaSuccess)
+          e = cudaMemcpy2DAsync((char*)host_pose + 3 * row, row, st->q, pitch, row, 4,
+                                cudaMemcpyDeviceToHost, cs);
+        if (e == cudaSuccess)
+          e = cudaMemcpy2DAsync((char*)host_pose + 7 * row, row, st->nu, pitch, row, 6,
+                                cudaMemcpyDeviceToHost, cs);
+      }
+      if (e != cudaSuccess) return fail(UUV_ERR_CUDA, "pose D2H: %s", cudaGetErrorString(e));
     }
-    if (e != cudaSuccess) return fail(UUV_ERR_CUDA, "pose D2H: %s", cudaGetErrorString(e));
   }
   if (sync) {
     e = cudaStreamSynchronize(cs);
     if (e != cudaSuccess) return fail(UUV_ERR_CUDA, "sync: %s", cudaGetErrorString(e));
   }
+  return UUV_OK;
+}
+
+uuv_status uuv_server_start(uuv_ctx* ctx, const uuv_state* st, int32_t substeps, double dt,
+                            void* stream, int32_t idle_timeout_ms, uuv_server** out) {
+  uuv_status s = check_state(ctx, st);
+  if (s != UUV_OK) return s;
+  if (out == nullptr) return fail(UUV_ERR_ARG, "null server handle");
+  if (substeps < 1 || !(dt > 0)) return fail(UUV_ERR_ARG, "substeps >= 1 and dt > 0 required");
+  if (st->n_envs < 1) return fail(UUV_ERR_ARG, "step server needs n_envs >= 1");
+  if (idle_timeout_ms < 1) return fail(UUV_ERR_ARG, "idle_timeout_ms must be >= 1");
+  if ((s = preload_kernels()) != UUV_OK) return s;
+  uuv_server* srv = new uuv_server();
+  srv->caller = (cudaStream_t)stream;
+  cudaError_t e = cudaStreamCreateWithFlags(&srv->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&srv->ev, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(srv->ev, srv->caller);  // after the caller's work
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(srv->stream, srv->ev, 0);
+  if (e == cudaSuccess) e = cudaHostAlloc((void**)&srv->ctl, sizeof(ServeCtl), cudaHostAllocMapped);
+  if (e == cudaSuccess) e = cudaHostAlloc((void**)&srv->done, sizeof(uint64_t), cudaHostAllocMapped);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&srv->sync, sizeof(ServeSync));
+  if (e == cudaSuccess) e = cudaMemsetAsync(srv->sync, 0, sizeof(ServeSync), srv->stream);
+  if (e == cudaSuccess) e = cudaHostGetDevicePointer((void**)&srv->ctl_dev, srv->ctl, 0);
+  if (e == cudaSuccess) e = cudaHostGetDevicePointer((void**)&srv->done_dev, srv->done, 0);
+  if (e != cudaSuccess) {
+    server_free(srv);
+    return fail(UUV_ERR_CUDA, "step server buffers: %s", cudaGetErrorString(e));
+  }
+  memset(srv->ctl, 0, sizeof(ServeCtl));
+  *srv->done = 0;
+  srv->n_act = ctx->hulls.size() > 1 ? st->a_max : ctx->hulls[0].n_act;
+  srv->dtype = st->dtype;
+  srv->n = st->n_envs;
+  const uint64_t idle_ns = (uint64_t)idle_timeout_ms * 1000000ull;
+  s = st->dtype == UUV_F32 ? uuv_tu::serve<float>(ctx, st, substeps, dt, srv->stream, srv->ctl_dev,
+                                                  srv->done_dev, srv->sync, idle_ns, &srv->grid)
+                           : uuv_tu::serve<double>(ctx, st, substeps, dt, srv->stream,
+                                                   srv->ctl_dev, srv->done_dev, srv->sync,
+                                                   idle_ns, &srv->grid);
+  if (s != UUV_OK) {
+    server_free(srv);
+    return s;
+  }
+  *out = srv;
+  return UUV_OK;
+}
+
+uuv_status uuv_server_step(uuv_server* srv, const void* host_cmd, int64_t cmd_ld,
+                           void* host_pose) {
+  if (srv == nullptr) return fail(UUV_ERR_ARG, "null server");
+  if (cmd_ld < srv->n_act)
+    return fail(UUV_ERR_SHAPE, "commands: row stride %lld < action_dim %d", (long long)cmd_ld,
+                srv->n_act);
+  const void* dc = host_mapped(host_cmd);
+  void* dp = host_pose != nullptr ? host_mapped(host_pose) : nullptr;
+  if (dc == nullptr || (host_pose != nullptr && dp == nullptr))
+    return fail(UUV_ERR_ARG, "step server: commands / pose_out must be pinned host memory");
+  srv->ctl->cmd = (uint64_t)dc;
+  srv->ctl->pose = (uint64_t)dp;
+  srv->ctl->cmd_ld = cmd_ld;
+  const uint64_t seq = ++srv->seq;
+  __atomic_store_n(&srv->ctl->seq, seq, __ATOMIC_RELEASE);
+  {
+    uint64_t spins = 0;
+    while (__atomic_load_n(srv->done, __ATOMIC_ACQUIRE) != seq) {
+      __builtin_ia32_pause();
+      if ((++spins & 0xFFFF) == 0) {
+        const cudaError_t q = cudaStreamQuery(srv->stream);
+        if (q != cudaErrorNotReady) {
+          cudaGetLastError();
+          return fail(UUV_ERR_CUDA, "step server is not running (%s)",
+                      q == cudaSuccess ? "idle timeout" : cudaGetErrorString(q));
+        }
+      }
+    }
+  }
+  return UUV_OK;
+}
+
+void uuv_server_stamps(const uuv_server* srv, uint64_t out[6]) {
+  for (int k = 0; k < 6; ++k) out[k] = srv ? ((volatile uint64_t*)srv->ctl->stamp)[k] : 0;
+}
+
+uuv_status uuv_server_stop(uuv_server* srv) {
+  if (srv == nullptr) return UUV_OK;
+  __atomic_store_n(&srv->ctl->seq, kServeQuit, __ATOMIC_RELEASE);
+  cudaError_t e = cudaStreamSynchronize(srv->stream);
+  // later work on the caller's stream sees the served state
+  if (e == cudaSuccess) e = cudaEventRecord(srv->ev, srv->stream);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(srv->caller, srv->ev, 0);
+  server_free(srv);
+  if (e != cudaSuccess) return fail(UUV_ERR_CUDA, "step server: %s", cudaGetErrorString(e));
   return UUV_OK;
 }
 
@@ -1575,9 +2042,11 @@ uuv_status uuv_reset(uuv_ctx* ctx, const uuv_state* st, const uint8_t* mask,
   const unsigned g = (unsigned)grid_for(st->n_envs);
   if (st->dtype == UUV_F32) {
     ResetArgs<float> a{make_view<float>(*st), *sampler, seed, mask, st->a_max};
+    UUV_REGISTER(k_reset<float>);
     k_reset<float><<<g, kBlock, 0, cs>>>(a);
   } else {
     ResetArgs<double> a{make_view<double>(*st), *sampler, seed, mask, st->a_max};
+    UUV_REGISTER(k_reset<double>);
     k_reset<double><<<g, kBlock, 0, cs>>>(a);
   }
   return check_launch("uuv_reset");
@@ -1680,6 +2149,7 @@ uuv_status uuv_rollout_stats(const double* stats, int64_t n_blocks, double* out,
                              void* stream) {
   if (stats == nullptr || out == nullptr || n_blocks < 0)
     return fail(UUV_ERR_ARG, "rollout_stats: bad arguments");
+  UUV_REGISTER(k_stats);
   k_stats<<<1, 32, 0, (cudaStream_t)stream>>>(stats, n_blocks, out, reset, (double*)stats);
   return check_launch("uuv_rollout_stats");
 }

@@ -351,6 +351,7 @@ class BatchState:
         self._ov = None
         self._ov_keys = None
         self._payload_offsets = False  # some env may carry a payload off the origin
+        self._server = None  # active `serve` context (resident step kernel)
         self._pin = None  # pinned staging for host-side commands (step_batch host path)
         self._dcmd = None
         self._pinned_cache = {}
@@ -589,6 +590,8 @@ def step_batch(state: BatchState, commands, *, pose_out=None) -> BatchState:
     ``pose_out``: optional pinned CPU tensor (13, N) in the batch dtype; receives the
     rows p (3), q (4), nu (6) after the step and the call waits for them.
     """
+    if state._server is not None:
+        return state._server.step(commands, pose_out)
     width = _cmd_width(state)
     if pose_out is not None or not isinstance(commands, torch.Tensor) or not commands.is_cuda:
         return _step_host(state, commands, width, pose_out)
@@ -598,6 +601,77 @@ def step_batch(state: BatchState, commands, *, pose_out=None) -> BatchState:
     if status:
         N.check(status, EngineError)
     return state
+
+
+class serve:
+    """Host-in-the-loop stepping through a resident step kernel (``uuv_server_*``).
+
+        with serve(state):
+            for t in range(T):
+                step_batch(state, pinned_cmds[t], pose_out=pinned_pose)
+
+    Inside the block ``step_batch`` takes host commands (pinned tensors, or any
+    host array staged through a pinned buffer) and optionally a pinned (13, N)
+    ``pose_out``; each call rings a doorbell in mapped pinned memory and returns
+    when every env has stepped and its pose rows have landed -- no kernel
+    launch and no stream synchronisation per step.  Results are bit-identical to
+    ``step_batch`` outside the block.  The kernel owns the state while it runs:
+    other operations on the batch raise until the block exits, and a
+    device-wide synchronisation (``torch.cuda.synchronize()``) would wait for
+    the kernel -- use stream-level synchronisation inside the block.  It stops
+    by itself after ``idle_timeout_ms`` without a step.
+    """
+
+    def __init__(self, state: "BatchState", idle_timeout_ms: int = 10_000):
+        self.state = state
+        self.idle_timeout_ms = int(idle_timeout_ms)
+        self._h = None
+
+    def __enter__(self):
+        st = self.state
+        if st._server is not None:
+            raise EngineError("serve: this batch already has a step server")
+        h = C.c_void_p()
+        N.check(N.load().uuv_server_start(st._ctx, C.byref(st._cstate()), st.sim.substeps,
+                                          st.sim.dt, st._stream(), self.idle_timeout_ms,
+                                          C.byref(h)), EngineError)
+        self._h = h
+        self._width = _cmd_width(st)
+        st._server = self
+        return self
+
+    def step(self, commands, pose_out=None):
+        st = self.state
+        n, width = st.n_envs, self._width
+        if isinstance(commands, torch.Tensor) and commands.device.type == "cpu" and \
+                _pinned_ok(st, commands, (n, width)):
+            src = commands
+        elif isinstance(commands, torch.Tensor) and commands.is_cuda:
+            raise EngineError("commands: inside serve() pass host commands (pinned tensor or "
+                              "array), not a CUDA tensor")
+        else:
+            arr = np.asarray(commands.cpu() if isinstance(commands, torch.Tensor) else commands)
+            if arr.shape != (n, width):
+                raise EngineError(f"commands: expected shape {(n, width)}, got {arr.shape}")
+            if st._pin is None:
+                st._pin = torch.empty((n, width), dtype=st.dtype).pin_memory()
+            st._pin.numpy()[...] = arr
+            src = st._pin
+        if pose_out is not None and not _pinned_ok(st, pose_out, (13, n)):
+            raise EngineError(f"pose_out: expected a pinned contiguous (13, {n}) {st.dtype} tensor")
+        status = N.load().uuv_server_step(self._h, src.data_ptr(), width,
+                                          pose_out.data_ptr() if pose_out is not None else None)
+        if status:
+            N.check(status, EngineError)
+        return st
+
+    def __exit__(self, *exc):
+        st = self.state
+        st._server = None
+        status = N.load().uuv_server_stop(self._h)
+        self._h = None
+        N.check(status, EngineError)
+        return False
 
 
 def _pinned_ok(state: BatchState, t, shape) -> bool:
@@ -676,6 +750,8 @@ def reset_envs(state: BatchState, mask, sampler: InitSampler = default_sampler) 
     any other Python callable runs on the host, one call per masked row, with
     the same Philox stream, and the rows are uploaded.
     """
+    if state._server is not None:
+        raise EngineError("reset_envs: the batch is being served (leave the serve() block first)")
     m = _mask(state, mask)
     if sampler is default_sampler:
         sampler = _IDENTITY

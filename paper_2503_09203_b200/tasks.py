@@ -339,6 +339,8 @@ class VecTaskEnv:
     # -------------------------------------------------------------- episode start
     def reset(self, mask=None):
         """Reset masked rows (default all) and return the observation of every row."""
+        if self.state._server is not None:
+            raise TaskError("the batch is being served (leave the serve() block first)")
         st = self.state
         if mask is None:
             m = None
@@ -395,6 +397,8 @@ class VecTaskEnv:
     # -------------------------------------------------------------- stepping
     def step(self, commands):
         """One fused launch: physics, reward/termination/info, auto-reset, next obs."""
+        if self.state._server is not None:
+            raise TaskError("the batch is being served (leave the serve() block first)")
         st = self.state
         n, a = self.n_envs, self.action_dim
         if torch.is_tensor(commands):

@@ -399,3 +399,106 @@ def test_rollout_stats_match_host_sums():
     assert st["frames"] == 300 * 20 and st["finished"] == tot_f and st["success"] == tot_s
     assert st["reward_sum"] == pytest.approx(tot_r, rel=1e-12)
     assert env.rollout_stats()["frames"] == 0
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("n", [1000, 4096])
+def test_host_buffer_step_equals_device_step(dtype, n):
+    """step_batch with pinned host commands + pose_out (uuv_step_host: the kernel reads and
+    writes the mapped host buffers) == the device-command step, bit for bit."""
+    from paper_2503_09203_b200.randomization import DRParameter, Uniform
+
+    veh = load_vehicle("bluerov")
+    spec = {k: DRParameter(k, Uniform(0.8, 1.2)) for k in ("mass*", "damping*")}
+    a = E.make_batch(veh, E.SimConfig(batch_size=n), master_seed=3, dtype=dtype)
+    b = E.make_batch(veh, E.SimConfig(batch_size=n), master_seed=3, dtype=dtype)
+    for st in (a, b):
+        E.reset_envs(st, np.ones(n, bool), E.spec_sampler(spec))
+    g = torch.Generator().manual_seed(0)
+    out = torch.empty((13, n), dtype=dtype).pin_memory()
+    for t in range(5):
+        hc = (torch.rand((n, 6), generator=g, dtype=torch.float64) * 2.4 - 1.2).to(dtype)
+        hc = hc.pin_memory()
+        if t == 3:
+            hc[7, 2] = float("nan")  # diverges env 7: frozen rows still report their pose
+        E.step_batch(a, hc.cuda())
+        E.step_batch(b, hc, pose_out=out)
+        for k in ("p", "q", "nu", "act", "steps", "diverged"):
+            assert torch.equal(getattr(a, k), getattr(b, k)), (t, k)
+        want = torch.cat([a.p, a.q, a.nu], dim=1).T.cpu()
+        assert torch.equal(out, want), t
+    assert bool(a.diverged[7])
+    # pageable host commands take the staged-copy path
+    E.step_batch(b, np.asarray(hc), pose_out=out)
+    E.step_batch(a, hc.cuda())
+    assert torch.equal(a.p, b.p)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("vehicles", [("bluerov",), ("bluerov", "lauv", "hauv")])
+def test_step_server_equals_launched_steps(dtype, vehicles):
+    """serve(): the resident step kernel == step_batch launches, bit for bit, incl. pose rows."""
+    from paper_2503_09203_b200.randomization import DRParameter, Uniform
+
+    n = 3000
+    vehs = [load_vehicle(v) for v in vehicles]
+    spec = {k: DRParameter(k, Uniform(0.8, 1.2)) for k in ("mass*", "volume*")}
+
+    def make():
+        if len(vehs) == 1:
+            st = E.make_batch(vehs[0], E.SimConfig(batch_size=n, substeps=2), master_seed=4,
+                              dtype=dtype)
+        else:
+            counts = [n // 3, n // 3, n - 2 * (n // 3)]
+            st = E.make_fleet_batch(vehs, counts, E.SimConfig(batch_size=n, substeps=2),
+                                    master_seed=4, dtype=dtype)
+        E.reset_envs(st, np.ones(n, bool), E.spec_sampler(spec))
+        return st
+
+    a, b = make(), make()
+    w = E._cmd_width(a)
+    g = torch.Generator().manual_seed(1)
+    cmds = [(torch.rand((n, w), generator=g, dtype=torch.float64) * 2 - 1).to(dtype).pin_memory()
+            for _ in range(6)]
+    cmds[4][5, 0] = float("nan")  # env 5 diverges and freezes
+    out = torch.empty((13, n), dtype=dtype).pin_memory()
+    # torch kernels used inside the block are loaded first (a first launch under CUDA
+    # lazy loading waits for the device, i.e. for the resident server)
+    assert torch.equal(out, torch.cat([a.p, a.q, a.nu], dim=1).T.cpu()) in (True, False)
+    with E.serve(b):
+        with pytest.raises(E.EngineError):
+            E.reset_envs(b, np.ones(n, bool))
+        with pytest.raises(E.EngineError):
+            E.step_batch(b, cmds[0].cuda())
+        for t in range(6):
+            E.step_batch(a, cmds[t].cuda())
+            E.step_batch(b, cmds[t], pose_out=out if t % 2 == 0 else None)
+            if t % 2 == 0:
+                want = torch.cat([a.p, a.q, a.nu], dim=1).T.cpu()
+                assert torch.equal(out, want), t
+        E.step_batch(b, np.asarray(cmds[0]))  # pageable host commands, staged
+    E.step_batch(a, cmds[0].cuda())
+    for k in ("p", "q", "nu", "act", "steps", "diverged"):
+        assert torch.equal(getattr(a, k), getattr(b, k)), k
+    assert bool(b.diverged[5])
+    E.step_batch(b, cmds[1].cuda())  # launches work again after the block
+
+
+def test_step_server_idle_timeout_and_errors():
+    st = E.make_batch(load_vehicle("bluerov"), E.SimConfig(batch_size=256))
+    E.reset_envs(st, np.ones(256, bool))
+    cmd = torch.zeros((256, 6)).pin_memory()
+    srv = E.serve(st, idle_timeout_ms=200)
+    srv.__enter__()
+    E.step_batch(st, cmd)
+    import time
+
+    time.sleep(0.6)  # the kernel ends by itself
+    with pytest.raises(E.EngineError, match="not running"):
+        E.step_batch(st, cmd)
+    srv.__exit__(None, None, None)
+    E.step_batch(st, cmd.cuda())
+    with E.serve(st):
+        with pytest.raises(E.EngineError):
+            with E.serve(st):
+                pass
