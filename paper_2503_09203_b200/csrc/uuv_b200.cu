@@ -869,13 +869,18 @@ __global__ void __launch_bounds__(kBlock, MinB<R>::value) k_task_step(const __gr
 #pragma unroll
   for (int k = 0; k < UUV_ST_COUNT; ++k) st[k] = 0.0;
   if (i < sv.n) {
+    // u = clip(commands); du = u - prev_u; prev_u = u  (tasks/core.py:329-335)
+    R u[UUV_MAX_ACT], du[UUV_MAX_ACT], raw[UUV_MAX_ACT];
+    if constexpr (!POL) {  // command loads first: they are the longest-latency inputs
+      const R* crow = a.cmd + i * a.cmd_ld;
+#pragma unroll
+      for (int j = 0; j < UUV_MAX_ACT; ++j) raw[j] = j < A ? crow[j] : R(0);
+    }
     int32_t steps = sv.steps[i];
     bool div = sv.diverged[i] != 0;
     R px, py, pz, nu[6], act[UUV_MAX_ACT];
     Q4<R> q;
     load_state(sv, i, A, px, py, pz, q, nu, act);
-    // u = clip(commands); du = u - prev_u; prev_u = u  (tasks/core.py:329-335)
-    R u[UUV_MAX_ACT], du[UUV_MAX_ACT], raw[UUV_MAX_ACT];
     if constexpr (POL) {
       // the observation the last step returned, recomputed from the stored state
       R pu[UUV_MAX_ACT];
@@ -884,10 +889,6 @@ __global__ void __launch_bounds__(kBlock, MinB<R>::value) k_task_step(const __gr
       R* orow = s_obs + threadIdx.x * od;
       observe_row<R>(T, A, px, py, pz, q, nu, pu, steps, a.dt, orow, nullptr);
       policy_command<R>(a, A, od, i, orow, raw);
-    } else {
-      const R* crow = a.cmd + i * a.cmd_ld;
-#pragma unroll
-      for (int j = 0; j < UUV_MAX_ACT; ++j) raw[j] = j < A ? crow[j] : R(0);
     }
 #pragma unroll
     for (int j = 0; j < UUV_MAX_ACT; ++j) {
