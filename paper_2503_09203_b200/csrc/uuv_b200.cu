@@ -105,7 +105,7 @@ void build_hull(const uuv_hull& src, Hull<R>& dst) {
   HullR<R>& h = dst.r;
   HullD& d = dst.d;
   h.n_act = src.n_act;
-  h.flags = src.flags;
+  h.flags = src.flags & ~kHullReaction;
   if (is_diag(src.M_A) && is_diag(src.D_lin) && is_diag(src.D_quad)) h.flags |= UUV_HULL_DIAGONAL;
   else h.flags &= ~UUV_HULL_DIAGONAL;
   h.mlp_layers = src.mlp_layers;
@@ -132,6 +132,12 @@ void build_hull(const uuv_hull& src, Hull<R>& dst) {
     h.fin_rho[j] = (R)src.fin_rho[j];
     h.ct[j] = (R)src.thrust_coeff[j];
     h.tc[j] = (R)src.time_constant[j];
+    const double* m = src.mount[j];
+    const double* x = src.axis[j];
+    h.mxa[j][0] = (R)(m[1] * x[2] - m[2] * x[1]);
+    h.mxa[j][1] = (R)(m[2] * x[0] - m[0] * x[2]);
+    h.mxa[j][2] = (R)(m[0] * x[1] - m[1] * x[0]);
+    if (j < src.n_act && src.reaction[j] != 0.0) h.flags |= kHullReaction;
     d.ct[j] = src.thrust_coeff[j];
     d.tc[j] = src.time_constant[j] > 0 ? src.time_constant[j] : 1.0;
   }
@@ -314,13 +320,19 @@ UUV_D bool physics_at(const Hull<R>& H, const StateView<R>& sv, int64_t i, const
     if (sv.slot[UUV_OV_JITTER] >= 0) jit = sv.ov + sv.slot[UUV_OV_JITTER] * sv.ld + i;
   }
   bool ok = true;
-  for (int k = 0; k < K; ++k) {
-    if (!substep<R, DR, false, AC, DM>(H.r, s, jit, sv.ld, px, py, pz, q, nu, act, u, has_cur, cur, dt,
-                               nullptr)) {
-      ok = false;
-      break;
+  // the jitter record is present for every env of a launch or for none: one
+  // specialisation per case keeps its code out of the common loop
+  auto run = [&](auto with_jit) {
+    for (int k = 0; k < K; ++k) {
+      if (!substep<R, DR, false, AC, DM, decltype(with_jit)::value>(
+              H.r, s, jit, sv.ld, px, py, pz, q, nu, act, u, has_cur, cur, dt, nullptr)) {
+        ok = false;
+        break;
+      }
     }
-  }
+  };
+  if (DR && jit != nullptr) run(std::true_type{});
+  else run(std::false_type{});
   return !ok;
 }
 
