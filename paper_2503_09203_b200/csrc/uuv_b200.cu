@@ -73,6 +73,13 @@ template <typename R> struct MinB;
 template <> struct MinB<float> { static constexpr int value = UUV_MINB_F32; };
 template <> struct MinB<double> { static constexpr int value = UUV_MINB_F64; };
 constexpr int kObsMax = 12 + UUV_MAX_ACT + 3;
+// High-occupancy DR step kernel: min CTAs/SM and the batch size from which it is
+// used.  Measured (A/B, B200): cfg2 1M envs 54.9 -> 49.1 us, cfg5 physics 75.5 ->
+// 68.9 us; at 4096 envs it is 2-4% slower (spill latency), hence the threshold.
+constexpr int kMinBHi = 5;
+#ifndef UUV_HI_OCC_MIN_ENVS
+#define UUV_HI_OCC_MIN_ENVS 131072
+#endif
 
 uuv_status fail(uuv_status s, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
 uuv_status fail(uuv_status s, const char* fmt, ...) {
@@ -562,8 +569,11 @@ UUV_D void step_any(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in) {
 // One env per thread; when the grid is smaller than the batch (persistent mode)
 // each thread walks envs with stride gridDim * kBlock and prefetches the next
 // env's inputs into registers before computing the current one.
-template <typename R, int NT, bool DR, int AC, bool DM>
-__global__ void __launch_bounds__(kBlock, (NT > 1 && sizeof(R) == 4) ? 3 : MinB<R>::value)
+// HI: the high-occupancy build of the float DR kernel (register cap 96 instead of
+// 128, a few spills to L1), launched for large batches where more resident warps
+// hide HBM latency; the default build serves the latency-bound small batches.
+template <typename R, int NT, bool DR, int AC, bool DM, bool HI = false>
+__global__ void __launch_bounds__(kBlock, HI ? kMinBHi : ((NT > 1 && sizeof(R) == 4) ? 3 : MinB<R>::value))
     k_step(const __grid_constant__ StepArgs<R, NT> a) {
   if (a.early_trigger == 1) pdl_trigger();
 #if UUV_CMD_PREFETCH
@@ -1430,13 +1440,21 @@ uuv_status launch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd,
   a.dt = (R)dt_sub;
   a.pose_out = (R*)pose_out;
   const int64_t need = grid_for(st->n_envs);
-  const int64_t wave = one_wave_ctas(k_step<R, NT, DR, AC, DM>);
+  constexpr bool kHiOk = DR && NT == 1 && sizeof(R) == 4;
+  static const int64_t hi_min = [] {
+    const char* v = getenv("UUV_HI_OCC_MIN_ENVS");
+    return v ? (int64_t)atoll(v) : (int64_t)UUV_HI_OCC_MIN_ENVS;
+  }();
+  const bool hi = kHiOk && st->n_envs >= hi_min;
+  auto kern = hi ? k_step<R, NT, DR, AC, DM, kHiOk> : k_step<R, NT, DR, AC, DM, false>;
+  const int64_t wave = one_wave_ctas(kern);
   // persistent (grid-stride + register prefetch) beyond one wave; UUV_STEP_WAVES overrides
   const int64_t waves = step_waves();
   const int64_t grid = waves >= need ? need : std::min<int64_t>(need, wave * waves);
   a.early_trigger = pdl_mode() == 2 ? 2 : ((grid <= wave && pdl_enabled()) ? 1 : 0);
-  UUV_REGISTER(k_step<R, NT, DR, AC, DM>);
-  cudaError_t e = launch_pdl(k_step<R, NT, DR, AC, DM>, (unsigned)grid, s, a);
+  UUV_REGISTER(k_step<R, NT, DR, AC, DM, false>);
+  UUV_REGISTER(k_step<R, NT, DR, AC, DM, kHiOk>);
+  cudaError_t e = launch_pdl(kern, (unsigned)grid, s, a);
   if (e != cudaSuccess) return fail(UUV_ERR_CUDA, "uuv_step: %s", cudaGetErrorString(e));
   return check_launch("uuv_step");
 }

@@ -2,6 +2,7 @@
 # build/variants/lib_<name>.so, plus "new" for the in-tree build.
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
+rm -f gpurun_out/ab_*.jsonl
 CASES=${AB_CASES:-cfg2,bluerov,cfg5_physics,cfg2_k8,cfg3}
 SIZES=${AB_SIZES:-4096,1048576,4194304}
 for rep in 1 2; do
