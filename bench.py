@@ -20,7 +20,10 @@ commands U(-1, 1).  A step is one control step (one ``uuv_step`` launch).
   launch, no stream sync per step; host clock around exactly K synchronous
   steps).
 * roofline — the step kernel's algorithmic bytes per launch / average launch
-  duration vs the measured HBM copy bandwidth (MEASURED_PEAKS.json).
+  duration vs the measured HBM copy bandwidth (MEASURED_PEAKS.json).  At
+  4096 envs the step is launch/latency-bound, so ``roofline_at_scale`` also
+  reports the same kernel on 1,048,576 envs of the same workload (informational;
+  not the bench value).
 * cpu_baseline — the CPU oracle (numpy restatement of the reference) on the
   same workload on this box's host cores (rank 0, N = 1 only).
 
@@ -330,6 +333,41 @@ def run_b200(args, rank, world, local_rank):
                 "step_batch -> uuv_step_host (one launch per step, mapped pinned buffers)")
     barrier()
 
+    # the same kernel at scale (informational): 1,048,576 envs of the same
+    # workload (state + DR record + commands ~ 230 MB >> L2), CUDA graph of 20
+    # steps, CUDA events -> achieved bandwidth of the step kernel where it is
+    # HBM-bound rather than launch/latency-bound
+    scale = None
+    if not args.no_scale:
+        n_big = 1 << 20
+        big = E.make_batch(veh, E.SimConfig(batch_size=n_big), master_seed=0, device=dev,
+                           env_offset=rank * n_big)
+        E.reset_envs(big, torch.ones(n_big, dtype=torch.bool, device=dev),
+                     E.spec_sampler(dr_spec()))
+        cmd_big = torch.rand((n_big, A_BLUEROV), device=dev, generator=gen) * 2 - 1
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                E.step_batch(big, cmd_big)
+        torch.cuda.synchronize(dev)
+        gb = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            with torch.cuda.graph(gb, stream=stream):
+                for _ in range(20):
+                    E.step_batch(big, cmd_big)
+        torch.cuda.synchronize(dev)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            gb.replay()
+            e1.record(stream)
+        torch.cuda.synchronize(dev)
+        t_big = e0.elapsed_time(e1) / 1e3 / 20
+        a_big = n_big * bpf / t_big / 1e9
+        scale = {"envs_per_gpu": n_big, "us_per_step": t_big * 1e6,
+                 "env_frames_per_s": n_big / t_big, "achieved": a_big, "peak": peak,
+                 "unit": "GB/s", "frac": a_big / peak}
+        del big, cmd_big, gb
+        torch.cuda.empty_cache()
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "env-frames/s", "n_gpus": world,
@@ -353,6 +391,7 @@ def run_b200(args, rank, world, local_rank):
                          "traffic_note": "ncu dram bytes per launch (cold cache), profiles/r01",
                          "peak_source": peak_kind,
                          "bytes_per_frame": bpf, "kernel": "k_step<float,1,DR=true>"},
+            "roofline_at_scale": scale,
             "gpu_launches": k_total,
             "clocks": clk.summary(),
         }
@@ -376,6 +415,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-scale", action="store_true",
+                    help="skip the informational 1M-env roofline_at_scale measurement")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
