@@ -12,6 +12,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <ctime>
 #include <algorithm>
 #include <climits>
 #include <cstdint>
@@ -626,14 +627,17 @@ __global__ void __launch_bounds__(kBlock, HI ? kMinBHi : ((NT > 1 && sizeof(R) =
 // caller's pinned buffer, fences at system scope and raises its done flag.  The
 // host waits on all flags.  An idle timeout (%globaltimer) ends the kernel if
 // the host goes away, so it can never hold the GPU.
-struct ServeCtl {           // host-mapped, written by the host
-  uint64_t seq;             // doorbell: step number, or kServeQuit
+struct alignas(16) ServeCtl {  // host-mapped, written by the host
+  // {seq, cmd} share one 16-byte line read by a single load: the host stores cmd
+  // before seq, so a read that sees the new seq sees that step's cmd.
+  uint64_t seq;             // doorbell: step number (| kServeNewPose), or kServeQuit
   uint64_t cmd;             // device-visible address of the (n, cmd_ld) commands
   uint64_t pose;            // device-visible address of the (13, n) pose rows, or 0
-  int64_t cmd_ld;
-  uint64_t stamp[6];        // CTA 0 phase times of the last step (%globaltimer ns)
+  int64_t cmd_ld;           // {pose, cmd_ld}: re-read only when kServeNewPose is set
+  uint64_t stamp[8];        // phase times of the last step (ns; see uuv_server_stamps)
 };
 constexpr uint64_t kServeQuit = ~0ull;
+constexpr uint64_t kServeNewPose = 1ull << 62;  // pose / cmd_ld changed this step
 
 struct ServeSync {          // device memory: CTA 0 republishes the doorbell here
   uint64_t go;
@@ -660,6 +664,9 @@ UUV_D uint64_t ld_relaxed_sys(const uint64_t* p) {
   uint64_t v;
   asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
+}
+UUV_D void ld_relaxed_sys_v2(const uint64_t* p, uint64_t& a, uint64_t& b) {
+  asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
 UUV_D uint64_t ld_acquire_gpu(const uint64_t* p) {
   uint64_t v;
@@ -720,6 +727,8 @@ __global__ void __launch_bounds__(kBlock, (NT > 1 && sizeof(R) == 4) ? 3 : MinB<
     load_state(sv, i, A, in.px, in.py, in.pz, in.q, in.nu, in.act);
   }
   uint64_t seq = 0;
+  uint64_t cur_pose = 0;  // CTA 0: pose rows address / command stride of the last step
+  int64_t cur_ld = 0;
   ServeSync* sy = sa.sync;
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // start marker + the idle budget (profiling aid)
     sa.ctl->stamp[4] = sa.idle_ns;
@@ -733,10 +742,11 @@ __global__ void __launch_bounds__(kBlock, (NT > 1 && sizeof(R) == 4) ? 3 : MinB<
       // 190 us vs 20 us per step at 4096 envs)
       if (blockIdx.x == 0) {
         const uint64_t t0 = global_ns();
-        uint64_t why = 0;
+        uint64_t why = 0, word = 0, cmd = 0;
         for (;;) {
-          v = ld_relaxed_sys(&sa.ctl->seq);
-          if (v != seq) { why = 1; break; }
+          ld_relaxed_sys_v2(&sa.ctl->seq, word, cmd);  // {seq, cmd} in one read
+          v = word == kServeQuit ? kServeQuit : (word & ~kServeNewPose);
+          if (v != seq) { why = 1; sa.ctl->stamp[0] = global_ns(); break; }
           // signed: %globaltimer may step back slightly when it is re-synchronised
           if ((int64_t)(global_ns() - t0) > (int64_t)sa.idle_ns) { v = kServeQuit; why = 2; break; }
           __nanosleep(sa.sleep_ns);
@@ -746,14 +756,24 @@ __global__ void __launch_bounds__(kBlock, (NT > 1 && sizeof(R) == 4) ? 3 : MinB<
           sa.ctl->stamp[1] = global_ns() - t0;
           sa.ctl->stamp[2] = seq;
         }
-        asm volatile("fence.acq_rel.sys;" ::: "memory");
-        s_cmd = *(volatile uint64_t*)&sa.ctl->cmd;
-        s_pose = *(volatile uint64_t*)&sa.ctl->pose;
-        s_ld = *(volatile int64_t*)&sa.ctl->cmd_ld;
+        s_cmd = cmd;
+        if (v != kServeQuit && (word & kServeNewPose)) {
+          uint64_t pose, ld;
+          ld_relaxed_sys_v2(&sa.ctl->pose, pose, ld);
+          cur_pose = pose;
+          cur_ld = (int64_t)ld;
+        }
+        s_pose = cur_pose;
+        s_ld = cur_ld;
+        sa.ctl->stamp[1] = global_ns();
         sy->cmd = s_cmd;
         sy->pose = s_pose;
         sy->cmd_ld = s_ld;
         st_release_gpu(&sy->go, v);
+        // like every other CTA, acquire the republished word: a GPU-scope acquire
+        // invalidates this SM's L1, so the command rows below are fetched fresh
+        // from host memory (a system-scope acquire fence here cost 4.4 us/step)
+        (void)ld_acquire_gpu(&sy->go);
       } else {
         while ((v = ld_acquire_gpu(&sy->go)) == seq) __nanosleep(64);
         s_cmd = *(volatile uint64_t*)&sy->cmd;
@@ -766,14 +786,15 @@ __global__ void __launch_bounds__(kBlock, (NT > 1 && sizeof(R) == 4) ? 3 : MinB<
     const uint64_t v = s_seq;
     if (v == kServeQuit) break;
     const bool stamp = blockIdx.x == 0 && threadIdx.x == 0;
-    if (stamp) sa.ctl->stamp[0] = global_ns();
     if (live) {
+      // plain coalesced loads over the link (after the GPU-scope acquire above;
+      // L1-bypassing .cg/.cv loads of host memory were far slower at scale)
       const R* crow = (const R*)s_cmd + i * s_ld;
       const int A = AC > 0 ? AC : a.hull[in.ty].r.n_act;
 #pragma unroll
       for (int j = 0; j < UUV_MAX_ACT; ++j)
         in.u[j] = (j < A) ? clip_<R>(crow[j], R(-1), R(1)) : R(0);
-      if (stamp) sa.ctl->stamp[1] = global_ns() + (uint64_t)(in.u[0] > R(2));
+      if (stamp) sa.ctl->stamp[2] = global_ns() + (uint64_t)(in.u[0] > R(2));
       if constexpr (NT > 1) {
         switch (a.cls[in.ty]) {
           case 1: serve_env<R, NT, DR, 6, true>(a, i, in, (R*)s_pose); break;
@@ -786,7 +807,7 @@ __global__ void __launch_bounds__(kBlock, (NT > 1 && sizeof(R) == 4) ? 3 : MinB<
         serve_env<R, NT, DR, AC, DM>(a, i, in, (R*)s_pose);
       }
     }
-    if (stamp) sa.ctl->stamp[2] = global_ns() + (uint64_t)(in.px > R(1e30));
+    if (stamp) sa.ctl->stamp[3] = global_ns() + (uint64_t)(in.px > R(1e30));
     // One system-scope fence per step: CTAs publish their stores at GPU scope
     // and count in; the last one fences at system scope (cumulative) and
     // releases the host's done flag.
@@ -796,11 +817,12 @@ __global__ void __launch_bounds__(kBlock, (NT > 1 && sizeof(R) == 4) ? 3 : MinB<
       if (atomicAdd(&sy->arrived, 1u) == gridDim.x - 1) {
         __threadfence();
         sy->arrived = 0;
+        sa.ctl->stamp[4] = global_ns();
         __threadfence_system();
+        sa.ctl->stamp[5] = global_ns();
         st_release_sys(sa.done, v);
       }
     }
-    if (stamp) sa.ctl->stamp[3] = global_ns();
     seq = v;
   }
 }
@@ -1861,6 +1883,8 @@ struct uuv_server {
   cudaEvent_t ev = nullptr;
   int32_t n_act = 0, dtype = 0;
   int64_t n = 0;
+  uint64_t last_pose = 0;
+  int64_t last_ld = 0;
 };
 
 static void server_free(uuv_server* s) {
@@ -2045,11 +2069,20 @@ uuv_status uuv_server_step(uuv_server* srv, const void* host_cmd, int64_t cmd_ld
   void* dp = host_pose != nullptr ? host_mapped(host_pose) : nullptr;
   if (dc == nullptr || (host_pose != nullptr && dp == nullptr))
     return fail(UUV_ERR_ARG, "step server: commands / pose_out must be pinned host memory");
-  srv->ctl->cmd = (uint64_t)dc;
-  srv->ctl->pose = (uint64_t)dp;
-  srv->ctl->cmd_ld = cmd_ld;
+  uint64_t flag = 0;
+  if (srv->seq == 0 || (uint64_t)dp != srv->last_pose || cmd_ld != srv->last_ld) {
+    srv->ctl->pose = (uint64_t)dp;
+    srv->ctl->cmd_ld = cmd_ld;
+    srv->last_pose = (uint64_t)dp;
+    srv->last_ld = cmd_ld;
+    flag = kServeNewPose;
+  }
+  srv->ctl->cmd = (uint64_t)dc;  // before seq (x86 stores are not reordered)
   const uint64_t seq = ++srv->seq;
-  __atomic_store_n(&srv->ctl->seq, seq, __ATOMIC_RELEASE);
+  timespec ts;
+  clock_gettime(CLOCK_REALTIME, &ts);
+  srv->ctl->stamp[6] = (uint64_t)ts.tv_sec * 1000000000ull + (uint64_t)ts.tv_nsec;
+  __atomic_store_n(&srv->ctl->seq, seq | flag, __ATOMIC_RELEASE);
   {
     uint64_t spins = 0;
     while (__atomic_load_n(srv->done, __ATOMIC_ACQUIRE) != seq) {
@@ -2064,11 +2097,13 @@ uuv_status uuv_server_step(uuv_server* srv, const void* host_cmd, int64_t cmd_ld
       }
     }
   }
+  clock_gettime(CLOCK_REALTIME, &ts);
+  srv->ctl->stamp[7] = (uint64_t)ts.tv_sec * 1000000000ull + (uint64_t)ts.tv_nsec;
   return UUV_OK;
 }
 
-void uuv_server_stamps(const uuv_server* srv, uint64_t out[6]) {
-  for (int k = 0; k < 6; ++k) out[k] = srv ? ((volatile uint64_t*)srv->ctl->stamp)[k] : 0;
+void uuv_server_stamps(const uuv_server* srv, uint64_t out[8]) {
+  for (int k = 0; k < 8; ++k) out[k] = srv ? ((volatile uint64_t*)srv->ctl->stamp)[k] : 0;
 }
 
 uuv_status uuv_server_stop(uuv_server* srv) {

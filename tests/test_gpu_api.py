@@ -477,7 +477,15 @@ def test_step_server_equals_launched_steps(dtype, vehicles):
                 want = torch.cat([a.p, a.q, a.nu], dim=1).T.cpu()
                 assert torch.equal(out, want), t
         E.step_batch(b, np.asarray(cmds[0]))  # pageable host commands, staged
+        E.step_batch(a, cmds[0].cuda())
+        reuse = torch.empty_like(cmds[0]).pin_memory()  # one buffer, new contents each step
+        for t in range(30):
+            reuse.copy_(cmds[t % 6] * (1.0 - 0.01 * t))
+            E.step_batch(a, reuse.cuda())
+            E.step_batch(b, reuse, pose_out=out)
+            assert torch.equal(out, torch.cat([a.p, a.q, a.nu], dim=1).T.cpu()), t
     E.step_batch(a, cmds[0].cuda())
+    E.step_batch(b, cmds[0].cuda())
     for k in ("p", "q", "nu", "act", "steps", "diverged"):
         assert torch.equal(getattr(a, k), getattr(b, k)), k
     assert bool(b.diverged[5])
