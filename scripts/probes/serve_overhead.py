@@ -21,6 +21,31 @@ cmd = (torch.rand((n, 6)) * 2 - 1).pin_memory()
 out = torch.empty((13, n)).pin_memory()
 lib = N.load()
 with E.serve(st) as srv:
+    ring = (torch.rand((1000, n, 6)) * 2 - 1).pin_memory()  # a fresh buffer per step, as bench.py
+    t0 = time.perf_counter()
+    for k in range(1000):
+        E.step_batch(st, ring[k], pose_out=out)
+    print(f"n={n} step_batch, 1000-buffer ring {1e6 * (time.perf_counter() - t0) / 1000:7.2f} us/step",
+          flush=True)
+    import glob
+    import os
+    libs = glob.glob(os.path.join(os.path.dirname(torch.__file__), "lib", "libcudart*.so*")) + \
+        glob.glob(os.path.join(os.path.dirname(torch.__file__), "..", "nvidia", "cuda_runtime", "lib",
+                               "libcudart.so*"))
+    if libs:
+        cr = ctypes.CDLL(libs[0])
+        at = (ctypes.c_char * 64)()
+        ptrs = [ring[k].data_ptr() for k in range(1000)]
+        t0 = time.perf_counter()
+        for pt in ptrs:
+            cr.cudaPointerGetAttributes(at, ctypes.c_void_p(pt))
+        print(f"cudaPointerGetAttributes per new address: {1e6 * (time.perf_counter() - t0) / 1000:.2f} us",
+              flush=True)
+    t0 = time.perf_counter()
+    for k in range(1000):
+        E.step_batch(st, ring[k], pose_out=out)
+    print(f"n={n} step_batch, ring again {1e6 * (time.perf_counter() - t0) / 1000:7.2f} us/step",
+          flush=True)
     for mode in ("step_batch", "C call", "C call, no pose"):
         h, cp, op = srv._h, cmd.data_ptr(), out.data_ptr()
         f = lib.uuv_server_step
