@@ -43,20 +43,31 @@ UUV_D void reset_env(const StateView<R>& sv, int64_t i, const uuv_sampler& smp, 
   g.init(smp.rng_mode, seed, (uint64_t)(sv.env_offset + i), (uint64_t)(int64_t)ep);
   const int64_t ld = sv.ld;
   // identity record: ratios 1, cobm/payload/positions/jitter 0
+  // (cold code, run for finished rows only: loops stay rolled to keep the task
+  // kernels' instruction footprint small)
   if (sv.ov != nullptr) {
+#pragma unroll 1
     for (int k = 0; k < UUV_OV_COUNT; ++k) {
       const int s0 = sv.slot[k];
       if (s0 < 0) continue;
       const int width = k == UUV_OV_PAYLOAD_POS ? 3 : (k == UUV_OV_JITTER ? 3 * UUV_MAX_ACT : 1);
       const double ident = k <= UUV_OV_THRUST_COEFF ? 1.0 : 0.0;
+#pragma unroll 1
       for (int c = 0; c < width; ++c) sv.ov[(s0 + c) * ld + i] = ident;
     }
   }
   uint16_t keys = 0;
+#pragma unroll 1
   for (int d = 0; d < smp.n_overlay; ++d) {
     const uuv_draw& dr = smp.overlay[d];
-    double v[3];
-    for (int c = 0; c < dr.n_draws; ++c) v[c] = draw(g, dr, smp.pw_table);
+    double v[3] = {0.0, 0.0, 0.0};
+#pragma unroll 1
+    for (int c = 0; c < dr.n_draws; ++c) {
+      const double x = draw(g, dr, smp.pw_table);
+      v[0] = c == 0 ? x : v[0];
+      v[1] = c == 1 ? x : v[1];
+      v[2] = c == 2 ? x : v[2];
+    }
     keys |= (uint16_t)(1u << dr.key);
     const int s0 = sv.slot[dr.key];
     if (sv.ov == nullptr || s0 < 0) continue;
@@ -89,9 +100,21 @@ UUV_D void reset_env(const StateView<R>& sv, int64_t i, const uuv_sampler& smp, 
   // start pose / velocity
   if (smp.start_mode == UUV_START_BOX) {
     double pp[3], eu[3];
-    for (int c = 0; c < 3; ++c) pp[c] = __dadd_rn(smp.p_base[c], g.uniform(smp.p_lo[c], smp.p_hi[c]));
-    for (int c = 0; c < 3; ++c) eu[c] = g.uniform(smp.eul_lo[c], smp.eul_hi[c]);
-    for (int c = 0; c < 6; ++c) nu[c] = (R)g.uniform(smp.nu_lo[c], smp.nu_hi[c]);
+    // one rolled loop over the 12 draws in the reference's order: p (3), euler (3), nu (6)
+    const double* lo[3] = {smp.p_lo, smp.eul_lo, smp.nu_lo};
+    const double* hi[3] = {smp.p_hi, smp.eul_hi, smp.nu_hi};
+    double dv[12];
+#pragma unroll 1
+    for (int c = 0; c < 12; ++c) {
+      const int grp = c < 3 ? 0 : (c < 6 ? 1 : 2), k = c < 3 ? c : (c < 6 ? c - 3 : c - 6);
+      dv[c] = g.uniform(lo[grp][k], hi[grp][k]);
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) pp[c] = __dadd_rn(smp.p_base[c], dv[c]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) eu[c] = dv[3 + c];
+#pragma unroll
+    for (int c = 0; c < 6; ++c) nu[c] = (R)dv[6 + c];
     px = (R)pp[0]; py = (R)pp[1]; pz = (R)pp[2];
     const Q4<double> qd = euler_quat(eu[0], eu[1], eu[2]);
     q = Q4<R>{(R)qd.w, (R)qd.x, (R)qd.y, (R)qd.z};

@@ -11,6 +11,7 @@ with 0).  tests/test_gpu_baseline.py replays them with the device episode loop
 
 import json
 import os
+import time
 
 import numpy as np
 from uuvsim.baseline import Policy, cem_train, evaluate
@@ -55,6 +56,20 @@ def main():
                                 env.action_dim)
     env = small_env(seed=7, batch=30)
     out["eval_trained"] = cell(evaluate(trained, env, n_trials=45, label="trained"))
+    # the reference's acceptance run (test_acceptance.py:308-319): ~2.5 CPU-minutes
+    t0 = time.perf_counter()
+    task = TaskConfig(task="station_keeping", vehicle="bluerov_heavy")
+    res = cem_train(make_env(task, SimConfig(batch_size=512), seed=0), population=32,
+                    elite_frac=0.25, iterations=60, seed=0)
+    t1 = time.perf_counter()
+    c = evaluate(res.policy, make_env(task, SimConfig(batch_size=250), seed=1), n_trials=500)
+    out["acceptance_cem"] = {
+        "settings": "TaskConfig(station_keeping, bluerov_heavy), SimConfig(batch_size=512), "
+                    "seed 0; cem_train(population=32, elite_frac=0.25, iterations=60, seed=0); "
+                    "evaluate(batch 250, seed 1, n_trials=500)",
+        "mean_error": c.mean_error, "std_error": c.std_error, "success_rate": c.success_rate,
+        "best_return": res.best_return,
+        "reference_cpu_seconds": {"train": t1 - t0, "eval": time.perf_counter() - t1}}
     path = os.path.join(HERE, "baseline_reference.json")
     with open(path, "w") as f:
         json.dump(out, f, indent=1, sort_keys=True)

@@ -142,6 +142,12 @@ def test_baseline_learns_station_keeping(kw):
     eval_env = make_env(task, SimConfig(batch_size=250), seed=1, **kw)
     cell = B.evaluate(result.policy, eval_env, n_trials=500)
     assert cell.mean_error < 0.3, cell
+    if kw:  # float64 + the reference's streams: the reference's own run, to 1e-9
+        # (tests/golden/baseline_reference.json "acceptance_cem", made on the CPU)
+        ref = GOLD["acceptance_cem"]
+        np.testing.assert_allclose(cell.mean_error, ref["mean_error"], rtol=1e-9)
+        np.testing.assert_allclose(result.best_return, ref["best_return"], rtol=1e-9)
+        assert cell.success_rate == ref["success_rate"]
 
 
 def test_randomized_training_generalizes_in_order():
