@@ -884,12 +884,20 @@ UUV_D void policy_command(const TaskArgs<R>& a, int A, int od, int64_t i, const 
   for (int j = 0; j < UUV_MAX_ACT; ++j) raw[j] = R(0);
   if (m >= a.pol_members) return;  // rows past members * slot act with 0
   const R* th = a.pol_theta + m * a.pol_ld;
+  // fully unrolled to the widest observation (predicated): every theta load is
+  // issued up front and the A dot products interleave, instead of one
+  // load-multiply-add chain of A * obs_dim steps
+  R ob[kObsMax];
+#pragma unroll
+  for (int k = 0; k < kObsMax; ++k) ob[k] = k < od ? obs[k] : R(0);
 #pragma unroll
   for (int j = 0; j < UUV_MAX_ACT; ++j) {
     if (j < A) {
       const R* w = th + j * od;
       R acc = R(0);
-      for (int k = 0; k < od; ++k) acc = add_rn(acc, mul_rn(__ldg(w + k), obs[k]));
+#pragma unroll
+      for (int k = 0; k < kObsMax; ++k)
+        if (k < od) acc = add_rn(acc, mul_rn(__ldg(w + k), ob[k]));
       raw[j] = tanh(add_rn(acc, __ldg(th + A * od + j)));
     }
   }
