@@ -40,7 +40,8 @@
 extern "C" {
 #endif
 
-#define UUV_ABI_VERSION 3
+#define UUV_ABI_VERSION 4
+#define UUV_MAX_RUNS 8
 #define UUV_MAX_ACT 8        /* actuator columns per vehicle type             */
 #define UUV_MAX_TYPES 6      /* vehicle types in one batch (mixed fleets)     */
 #define UUV_MLP_MAX_PARAMS 128 /* packed weights+biases of one rotor network  */
@@ -140,6 +141,14 @@ typedef struct {
   int32_t n_slots;
   int32_t slot[UUV_OV_COUNT];
   int32_t flags;           /* UUV_STATE_* */
+  /* Mixed fleets whose rows form contiguous per-type runs (make_fleet_batch):
+   * run r covers rows [run_start[r], run_start[r+1]) (the last run to n_envs)
+   * with hull run_type[r].  Large batches are then stepped by one specialised
+   * single-hull launch per run on forked streams; n_runs = 0 means unknown
+   * (one generic mixed-fleet launch). */
+  int32_t n_runs;
+  int32_t run_type[UUV_MAX_RUNS];
+  int64_t run_start[UUV_MAX_RUNS];
 } uuv_state;
 
 /* uuv_state.flags */

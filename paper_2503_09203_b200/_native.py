@@ -35,7 +35,8 @@ OV_WIDTH["payload_position"] = 3
 OV_WIDTH["mount_position_jitter"] = 3 * MAX_ACT
 OV_IDENTITY = {k: (1.0 if i <= OV_INDEX["thrust_coeff*"] else 0.0) for i, k in enumerate(OV_KEYS)}
 
-ABI_VERSION = 3
+ABI_VERSION = 4
+MAX_RUNS = 8  # UUV_MAX_RUNS
 DIST_UNIFORM, DIST_PIECEWISE, DIST_GAUSSIAN = 0, 1, 2
 START_IDENTITY, START_BOX = 0, 1
 CURRENT_NONE, CURRENT_RANDOM_HEADING, CURRENT_HEADING_DRAW = 0, 1, 2
@@ -83,6 +84,8 @@ class State(C.Structure):
         ("steps", C.c_void_p), ("episodes", C.c_void_p), ("diverged", C.c_void_p),
         ("type_id", C.c_void_p), ("overlay", C.c_void_p), ("overlay_keys", C.c_void_p),
         ("n_slots", C.c_int32), ("slot", C.c_int32 * OV_COUNT), ("flags", C.c_int32),
+        ("n_runs", C.c_int32), ("run_type", C.c_int32 * MAX_RUNS),
+        ("run_start", C.c_int64 * MAX_RUNS),
     ]
 
 

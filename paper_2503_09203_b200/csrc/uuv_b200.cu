@@ -219,6 +219,15 @@ struct uuv_ctx {
   std::vector<uuv_hull> hulls;
   std::vector<Hull<float>> hf;
   std::vector<Hull<double>> hd;
+  // fork/join streams for per-run mixed-fleet steps (created on first use)
+  mutable std::vector<cudaStream_t> fork;
+  mutable std::vector<cudaEvent_t> done;
+  mutable cudaEvent_t forked = nullptr;
+  ~uuv_ctx() {
+    for (cudaStream_t s : fork) cudaStreamDestroy(s);
+    for (cudaEvent_t e : done) cudaEventDestroy(e);
+    if (forked) cudaEventDestroy(forked);
+  }
 };
 
 // ================================================================== kernels
@@ -1270,6 +1279,15 @@ uuv_status check_state(const uuv_ctx* ctx, const uuv_state* st) {
   if (st->overlay != nullptr)
     for (int k = 0; k < UUV_OV_COUNT; ++k)
       if (st->slot[k] >= st->n_slots) return fail(UUV_ERR_SHAPE, "state: slot beyond n_slots");
+  if (st->n_runs < 0 || st->n_runs > UUV_MAX_RUNS)
+    return fail(UUV_ERR_ARG, "state: n_runs %d outside [0, %d]", st->n_runs, UUV_MAX_RUNS);
+  for (int r = 0; r < st->n_runs; ++r) {
+    if (st->run_type[r] < 0 || st->run_type[r] >= (int)ctx->hulls.size())
+      return fail(UUV_ERR_ARG, "state: run %d has no hull", r);
+    if ((r == 0 && st->run_start[0] != 0) || (r > 0 && st->run_start[r] < st->run_start[r - 1]) ||
+        st->run_start[r] > st->n_envs)
+      return fail(UUV_ERR_ARG, "state: run starts must ascend from 0 within n_envs");
+  }
   return UUV_OK;
 }
 
@@ -1317,10 +1335,10 @@ template <> const std::vector<Hull<float>>& hulls_of<float>(const uuv_ctx* c) { 
 template <> const std::vector<Hull<double>>& hulls_of<double>(const uuv_ctx* c) { return c->hd; }
 
 template <typename R, int NT>
-void fill_hulls(const uuv_ctx* ctx, Hull<R>* dst, double dt_sub) {
+void fill_hulls(const uuv_ctx* ctx, Hull<R>* dst, double dt_sub, int first = 0) {
   const auto& hs = hulls_of<R>(ctx);
   for (int t = 0; t < NT; ++t) {
-    dst[t] = hs[t < (int)hs.size() ? t : 0];
+    dst[t] = hs[first + t < (int)hs.size() ? first + t : 0];
     for (int j = 0; j < UUV_MAX_ACT; ++j) dst[t].r.kdt0[j] = (R)(dt_sub / dst[t].d.tc[j]);
   }
 }
@@ -1455,14 +1473,15 @@ bool use_tma_step() {
 
 template <typename R, int NT, bool DR, int AC, bool DM = false>
 uuv_status launch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd, int64_t cmd_ld,
-                       int32_t K, double dt, cudaStream_t s, void* pose_out = nullptr) {
-  if (pose_out == nullptr && use_tma_step())
+                       int32_t K, double dt, cudaStream_t s, void* pose_out = nullptr,
+                       int hull0 = 0) {
+  if (pose_out == nullptr && hull0 == 0 && use_tma_step())
     return launch_step_tma<R, NT, DR, AC, DM>(ctx, st, cmd, cmd_ld, K, dt, s);
   StepArgs<R, NT> a;
   const double dt_sub = dt / K;
-  fill_hulls<R, NT>(ctx, a.hull, dt_sub);
+  fill_hulls<R, NT>(ctx, a.hull, dt_sub, hull0);
   for (int t = 0; t < NT; ++t)
-    a.cls[t] = t < (int)ctx->hulls.size() ? hull_class(ctx->hulls[t], st) : 0;
+    a.cls[t] = hull0 + t < (int)ctx->hulls.size() ? hull_class(ctx->hulls[hull0 + t], st) : 0;
   a.sv = make_view<R>(*st);
   a.cmd = (const R*)cmd;
   a.cmd_ld = cmd_ld;
@@ -1489,9 +1508,100 @@ uuv_status launch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd,
   return check_launch("uuv_step");
 }
 
+// One specialised single-hull launch for rows of hull `type` (a run of a fleet).
+template <typename R>
+uuv_status dispatch_one(const uuv_ctx* ctx, const uuv_state* st, int type, const void* cmd,
+                        int64_t cmd_ld, int32_t K, double dt, cudaStream_t s) {
+  const bool dr = st->overlay != nullptr;
+  const uuv_hull& h = ctx->hulls[type];
+  const bool dm = hull_diag_mass(h, st);
+  switch (hull_act_class(h)) {
+    case 6:
+      if (dm)
+        return dr ? launch_step<R, 1, true, 6, true>(ctx, st, cmd, cmd_ld, K, dt, s, nullptr, type)
+                  : launch_step<R, 1, false, 6, true>(ctx, st, cmd, cmd_ld, K, dt, s, nullptr, type);
+      return dr ? launch_step<R, 1, true, 6>(ctx, st, cmd, cmd_ld, K, dt, s, nullptr, type)
+                : launch_step<R, 1, false, 6>(ctx, st, cmd, cmd_ld, K, dt, s, nullptr, type);
+    case 8:
+      if (dm)
+        return dr ? launch_step<R, 1, true, 8, true>(ctx, st, cmd, cmd_ld, K, dt, s, nullptr, type)
+                  : launch_step<R, 1, false, 8, true>(ctx, st, cmd, cmd_ld, K, dt, s, nullptr, type);
+      return dr ? launch_step<R, 1, true, 8>(ctx, st, cmd, cmd_ld, K, dt, s, nullptr, type)
+                : launch_step<R, 1, false, 8>(ctx, st, cmd, cmd_ld, K, dt, s, nullptr, type);
+    default:
+      return dr ? launch_step<R, 1, true, 0>(ctx, st, cmd, cmd_ld, K, dt, s, nullptr, type)
+                : launch_step<R, 1, false, 0>(ctx, st, cmd, cmd_ld, K, dt, s, nullptr, type);
+  }
+}
+
+// Mixed fleet in contiguous per-type runs: one specialised launch per run, the
+// runs on forked streams (run 0 on the caller's) so they execute concurrently;
+// the caller's stream then joins them.  Same arithmetic as the mixed-fleet
+// kernel's per-type paths, so results are identical.
+static int64_t runs_min_envs() {
+  static const int64_t v = [] {
+    const char* e = getenv("UUV_RUNS_MIN_ENVS");
+    return e ? (int64_t)atoll(e) : (int64_t)131072;
+  }();
+  return v;
+}
+
+template <typename R>
+uuv_status dispatch_runs(const uuv_ctx* ctx, const uuv_state* st, const void* cmd, int64_t cmd_ld,
+                         int32_t K, double dt, cudaStream_t s) {
+  const int nr = st->n_runs;
+  cudaError_t e = cudaSuccess;
+  while ((int)ctx->fork.size() < nr - 1 && e == cudaSuccess) {
+    cudaStream_t fs;
+    cudaEvent_t ev;
+    e = cudaStreamCreateWithFlags(&fs, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) {
+      ctx->fork.push_back(fs);
+      ctx->done.push_back(ev);
+    }
+  }
+  if (e == cudaSuccess && ctx->forked == nullptr)
+    e = cudaEventCreateWithFlags(&ctx->forked, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(ctx->forked, s);
+  if (e != cudaSuccess) return fail(UUV_ERR_CUDA, "uuv_step (runs): %s", cudaGetErrorString(e));
+  const size_t es = sizeof(R);
+  for (int r = 0; r < nr; ++r) {
+    const int64_t a = st->run_start[r], b = r + 1 < nr ? st->run_start[r + 1] : st->n_envs;
+    if (b <= a) continue;
+    uuv_state sub = *st;
+    auto off = [&](void* p, size_t elem) { return p ? (void*)((char*)p + a * elem) : nullptr; };
+    sub.p = off(st->p, es);
+    sub.q = off(st->q, es);
+    sub.nu = off(st->nu, es);
+    sub.act = off(st->act, es);
+    sub.current_ned = off(st->current_ned, es);
+    sub.steps = (int32_t*)off(st->steps, sizeof(int32_t));
+    sub.episodes = (int32_t*)off(st->episodes, sizeof(int32_t));
+    sub.diverged = (uint8_t*)off(st->diverged, 1);
+    sub.type_id = nullptr;
+    sub.overlay = (double*)off(st->overlay, sizeof(double));
+    sub.overlay_keys = (uint16_t*)off(st->overlay_keys, sizeof(uint16_t));
+    sub.n_envs = b - a;
+    sub.env_offset = st->env_offset + a;
+    sub.n_runs = 0;
+    cudaStream_t rs = r == 0 ? s : ctx->fork[r - 1];
+    if (r > 0 && (e = cudaStreamWaitEvent(rs, ctx->forked, 0)) != cudaSuccess) break;
+    const uuv_status us = dispatch_one<R>(ctx, &sub, st->run_type[r],
+                                          (const char*)cmd + a * cmd_ld * es, cmd_ld, K, dt, rs);
+    if (us != UUV_OK) return us;
+    if (r > 0 && (e = cudaEventRecord(ctx->done[r - 1], rs)) != cudaSuccess) break;
+  }
+  for (int r = 1; r < nr && e == cudaSuccess; ++r) e = cudaStreamWaitEvent(s, ctx->done[r - 1], 0);
+  if (e != cudaSuccess) return fail(UUV_ERR_CUDA, "uuv_step (runs): %s", cudaGetErrorString(e));
+  return UUV_OK;
+}
+
 template <typename R>
 uuv_status dispatch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd, int64_t cmd_ld,
                          int32_t K, double dt, cudaStream_t s, void* pose = nullptr) {
+  if (ctx->hulls.size() > 1 && st->n_runs > 0 && pose == nullptr && st->n_envs >= runs_min_envs())
+    return dispatch_runs<R>(ctx, st, cmd, cmd_ld, K, dt, s);
   const bool dr = st->overlay != nullptr;
   if (ctx->hulls.size() == 1) {
     const bool dm = diag_mass(ctx, st);

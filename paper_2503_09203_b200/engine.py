@@ -344,10 +344,13 @@ class BatchState:
         self.episodes = torch.full((ld,), -1, dtype=torch.int32, **kw)[:n]
         self.diverged = torch.zeros(ld, dtype=torch.bool, **kw)[:n]
         self._type = None
+        self._runs = None  # contiguous per-type runs [(type, first row)] of a fleet batch
         if len(self.vehicles) > 1:
             ids = np.repeat(np.arange(len(counts), dtype=np.uint8), counts)
             self._type = torch.zeros(ld, dtype=torch.uint8, **kw)
             self._type[:n] = torch.from_numpy(ids).to(self.device)
+            starts = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(int)
+            self._runs = [(t, int(s0)) for t, (s0, c) in enumerate(zip(starts, counts)) if c > 0]
         self._ov = None
         self._ov_keys = None
         self._payload_offsets = False  # some env may carry a payload off the origin
@@ -494,6 +497,10 @@ class BatchState:
         for name, s0 in self._slots.items():
             s.slot[N.OV_INDEX[name]] = s0
         s.flags = 0 if self._payload_offsets else N.STATE_PAYLOAD_AT_ORIGIN
+        runs = self._runs if self._runs is not None and len(self._runs) <= N.MAX_RUNS else []
+        s.n_runs = len(runs)
+        for r, (t, s0) in enumerate(runs):
+            s.run_type[r], s.run_start[r] = t, s0
         return s
 
     def _note_sampler(self, sampler: "DeviceSampler"):
@@ -526,6 +533,7 @@ class BatchState:
         if self._type is None:
             self._type = torch.zeros(self._ld, dtype=torch.uint8, device=self.device)
         self._type[i] = t
+        self._runs = None  # rows of a type are no longer known to be contiguous
         self._cs = None
 
 

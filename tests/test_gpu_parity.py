@@ -551,3 +551,52 @@ def test_set_dr_schedule_between_rollouts_matches_fresh_spec():
     with pytest.raises(Exception):
         make_env(TaskConfig(task="station_keeping", vehicle="bluerov"),
                  E.SimConfig(batch_size=8)).set_dr(base)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_fleet_runs_equal_mixed_kernel(dtype):
+    """Contiguous per-type runs (one specialised launch per run, forked streams) vs the
+    generic mixed-fleet kernel, eager and graph-captured.  The same arithmetic compiled
+    into different kernels may contract multiply-adds differently, so the bar is the
+    parity tolerance (float32) / 1e-12 (float64), not bitwise; flags and counters exact."""
+    names = ("bluerov", "bluerov_heavy", "lauv", "iauv", "hauv")
+    vehs = [product_vehicle(x) for x in names]
+    n = 140_001  # above the per-run threshold (131,072)
+    counts = [n // 5 + (1 if i < n % 5 else 0) for i in range(5)]
+
+    def make(runs):
+        st = E.make_fleet_batch(vehs, counts, E.SimConfig(batch_size=n, substeps=2), master_seed=3,
+                                dtype=dtype)
+        E.reset_envs(st, np.ones(n, bool), E.spec_sampler(preset("train")))
+        if not runs:
+            st._runs, st._cs = None, None
+        return st
+
+    a, b = make(True), make(False)
+    assert a._cstate().n_runs == 5 and b._cstate().n_runs == 0
+    g = torch.Generator(device="cuda").manual_seed(0)
+    cmds = [(torch.rand((n, a.a_max), device="cuda", generator=g) * 2 - 1).to(dtype)
+            for _ in range(4)]
+    for c in cmds[:2]:
+        E.step_batch(a, c)
+        E.step_batch(b, c)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        E.step_batch(a, cmds[2])  # warm the fork streams before capture
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            E.step_batch(a, cmds[3])
+    E.step_batch(b, cmds[2])
+    graph.replay()
+    E.step_batch(b, cmds[3])
+    torch.cuda.synchronize()
+    for k in ("steps", "diverged"):
+        assert torch.equal(getattr(a, k), getattr(b, k)), k
+    rtol, atol = (FP32_RTOL, FP32_ATOL) if dtype == torch.float32 else (1e-12, 1e-14)
+    for k in ("p", "q", "nu", "act"):
+        ok, err = rowwise_close(host(getattr(a, k)), host(getattr(b, k)), rtol, atol)
+        assert ok, (k, err)
+    # a row reassigned to another vehicle type drops the run table
+    a.params.write_row(7, vehs[2])
+    assert a._cstate().n_runs == 0
