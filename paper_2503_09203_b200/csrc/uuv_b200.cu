@@ -569,6 +569,9 @@ UUV_D void step_any(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in) {
       case 2: step_env<R, NT, DR, 8, true>(a, i, in); return;
       case 3: step_env<R, NT, DR, 6, false>(a, i, in); return;
       case 4: step_env<R, NT, DR, 8, false>(a, i, in); return;
+      case 5: step_env<R, NT, DR, 0, true>(a, i, in); return;
+      case 6: step_env<R, NT, DR, kFinLayout, true>(a, i, in); return;
+      case 7: step_env<R, NT, DR, kFinLayout, false>(a, i, in); return;
       default: step_env<R, NT, DR, 0, false>(a, i, in); return;
     }
   } else {
@@ -810,6 +813,9 @@ __global__ void __launch_bounds__(kBlock, (NT > 1 && sizeof(R) == 4) ? 3 : MinB<
           case 2: serve_env<R, NT, DR, 8, true>(a, i, in, (R*)s_pose); break;
           case 3: serve_env<R, NT, DR, 6, false>(a, i, in, (R*)s_pose); break;
           case 4: serve_env<R, NT, DR, 8, false>(a, i, in, (R*)s_pose); break;
+          case 5: serve_env<R, NT, DR, 0, true>(a, i, in, (R*)s_pose); break;
+          case 6: serve_env<R, NT, DR, kFinLayout, true>(a, i, in, (R*)s_pose); break;
+          case 7: serve_env<R, NT, DR, kFinLayout, false>(a, i, in, (R*)s_pose); break;
           default: serve_env<R, NT, DR, 0, false>(a, i, in, (R*)s_pose); break;
         }
       } else {
@@ -1293,9 +1299,17 @@ uuv_status check_state(const uuv_ctx* ctx, const uuv_state* st) {
 
 // Actuator class of a hull (see substep): A first-order thrusters, else 0.
 int hull_act_class(const uuv_hull& h) {
+  for (int j = 0; j < h.n_act; ++j)
+    if (h.model[j] != UUV_FIRST_ORDER) return 0;
+  if (h.n_act == kFinLayout) {  // a propeller / tilt rotor, then four fins
+    if (h.kind[0] == UUV_RUDDER) return 0;
+    for (int j = 1; j < kFinLayout; ++j)
+      if (h.kind[j] != UUV_RUDDER) return 0;
+    return kFinLayout;
+  }
   if (h.n_act != 6 && h.n_act != 8) return 0;
   for (int j = 0; j < h.n_act; ++j)
-    if (h.kind[j] == UUV_RUDDER || h.model[j] != UUV_FIRST_ORDER) return 0;
+    if (h.kind[j] == UUV_RUDDER) return 0;
   return h.n_act;
 }
 
@@ -1327,7 +1341,8 @@ int8_t hull_class(const uuv_hull& h, const uuv_state* st) {
   const bool dm = hull_diag_mass(h, st);
   if (ac == 6) return dm ? 1 : 3;
   if (ac == 8) return dm ? 2 : 4;
-  return 0;
+  if (ac == kFinLayout) return dm ? 6 : 7;
+  return dm ? 5 : 0;
 }
 
 template <typename R> const std::vector<Hull<R>>& hulls_of(const uuv_ctx* c);
@@ -1528,7 +1543,18 @@ uuv_status dispatch_one(const uuv_ctx* ctx, const uuv_state* st, int type, const
                   : launch_step<R, 1, false, 8, true>(ctx, st, cmd, cmd_ld, K, dt, s, nullptr, type);
       return dr ? launch_step<R, 1, true, 8>(ctx, st, cmd, cmd_ld, K, dt, s, nullptr, type)
                 : launch_step<R, 1, false, 8>(ctx, st, cmd, cmd_ld, K, dt, s, nullptr, type);
+    case kFinLayout:
+      if (dm)
+        return dr ? launch_step<R, 1, true, kFinLayout, true>(ctx, st, cmd, cmd_ld, K, dt, s,
+                                                              nullptr, type)
+                  : launch_step<R, 1, false, kFinLayout, true>(ctx, st, cmd, cmd_ld, K, dt, s,
+                                                               nullptr, type);
+      return dr ? launch_step<R, 1, true, kFinLayout>(ctx, st, cmd, cmd_ld, K, dt, s, nullptr, type)
+                : launch_step<R, 1, false, kFinLayout>(ctx, st, cmd, cmd_ld, K, dt, s, nullptr, type);
     default:
+      if (dm)
+        return dr ? launch_step<R, 1, true, 0, true>(ctx, st, cmd, cmd_ld, K, dt, s, nullptr, type)
+                  : launch_step<R, 1, false, 0, true>(ctx, st, cmd, cmd_ld, K, dt, s, nullptr, type);
       return dr ? launch_step<R, 1, true, 0>(ctx, st, cmd, cmd_ld, K, dt, s, nullptr, type)
                 : launch_step<R, 1, false, 0>(ctx, st, cmd, cmd_ld, K, dt, s, nullptr, type);
   }
@@ -1618,7 +1644,16 @@ uuv_status dispatch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cm
                     : launch_step<R, 1, false, 8, true>(ctx, st, cmd, cmd_ld, K, dt, s, pose);
         return dr ? launch_step<R, 1, true, 8>(ctx, st, cmd, cmd_ld, K, dt, s, pose)
                   : launch_step<R, 1, false, 8>(ctx, st, cmd, cmd_ld, K, dt, s, pose);
+      case kFinLayout:
+        if (dm)
+          return dr ? launch_step<R, 1, true, kFinLayout, true>(ctx, st, cmd, cmd_ld, K, dt, s, pose)
+                    : launch_step<R, 1, false, kFinLayout, true>(ctx, st, cmd, cmd_ld, K, dt, s, pose);
+        return dr ? launch_step<R, 1, true, kFinLayout>(ctx, st, cmd, cmd_ld, K, dt, s, pose)
+                  : launch_step<R, 1, false, kFinLayout>(ctx, st, cmd, cmd_ld, K, dt, s, pose);
       default:
+        if (dm)
+          return dr ? launch_step<R, 1, true, 0, true>(ctx, st, cmd, cmd_ld, K, dt, s, pose)
+                    : launch_step<R, 1, false, 0, true>(ctx, st, cmd, cmd_ld, K, dt, s, pose);
         return dr ? launch_step<R, 1, true, 0>(ctx, st, cmd, cmd_ld, K, dt, s, pose)
                   : launch_step<R, 1, false, 0>(ctx, st, cmd, cmd_ld, K, dt, s, pose);
     }
@@ -1700,8 +1735,12 @@ void launch_task_step(bool dr, int ac, bool dm, unsigned g, cudaStream_t cs, con
   } else if (ac == 8) {
     if (dm) launch_task_dr<R, 8, true, POL>(dr, g, cs, a);
     else launch_task_dr<R, 8, false, POL>(dr, g, cs, a);
+  } else if (ac == kFinLayout) {
+    if (dm) launch_task_dr<R, kFinLayout, true, POL>(dr, g, cs, a);
+    else launch_task_dr<R, kFinLayout, false, POL>(dr, g, cs, a);
   } else {
-    launch_task_dr<R, 0, false, POL>(dr, g, cs, a);
+    if (dm) launch_task_dr<R, 0, true, POL>(dr, g, cs, a);
+    else launch_task_dr<R, 0, false, POL>(dr, g, cs, a);
   }
 }
 
@@ -1805,7 +1844,18 @@ uuv_status serve(const uuv_ctx* ctx, const uuv_state* st, int32_t K, double dt, 
                   : serve_kernel<R, 1, false, 8, true>(ctx, st, K, dt, s, ctl, done, sy, idle_ns, g);
       return dr ? serve_kernel<R, 1, true, 8>(ctx, st, K, dt, s, ctl, done, sy, idle_ns, g)
                 : serve_kernel<R, 1, false, 8>(ctx, st, K, dt, s, ctl, done, sy, idle_ns, g);
+    case kFinLayout:
+      if (dm)
+        return dr ? serve_kernel<R, 1, true, kFinLayout, true>(ctx, st, K, dt, s, ctl, done, sy,
+                                                               idle_ns, g)
+                  : serve_kernel<R, 1, false, kFinLayout, true>(ctx, st, K, dt, s, ctl, done, sy,
+                                                                idle_ns, g);
+      return dr ? serve_kernel<R, 1, true, kFinLayout>(ctx, st, K, dt, s, ctl, done, sy, idle_ns, g)
+                : serve_kernel<R, 1, false, kFinLayout>(ctx, st, K, dt, s, ctl, done, sy, idle_ns, g);
     default:
+      if (dm)
+        return dr ? serve_kernel<R, 1, true, 0, true>(ctx, st, K, dt, s, ctl, done, sy, idle_ns, g)
+                  : serve_kernel<R, 1, false, 0, true>(ctx, st, K, dt, s, ctl, done, sy, idle_ns, g);
       return dr ? serve_kernel<R, 1, true, 0>(ctx, st, K, dt, s, ctl, done, sy, idle_ns, g)
                 : serve_kernel<R, 1, false, 0>(ctx, st, K, dt, s, ctl, done, sy, idle_ns, g);
   }

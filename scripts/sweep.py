@@ -56,6 +56,12 @@ def make_case(name, n):
                      E.spec_sampler(spec or None))
         width = 6
         bpf = frame_bytes(6, len(keys), False)
+    elif name.startswith("veh:"):  # one vehicle, no DR: veh:<name>
+        veh = load_vehicle(name[4:])
+        st = E.make_batch(veh, E.SimConfig(batch_size=n), device=dev)
+        E.reset_envs(st, torch.ones(n, dtype=torch.bool, device=dev))
+        width = veh.action_dim
+        bpf = frame_bytes(width, 0, False)
     elif name == "cfg5_physics":  # bluerov_heavy + train preset (7 ratios) + current
         veh = load_vehicle("bluerov_heavy")
         st = E.make_batch(veh, E.SimConfig(batch_size=n), device=dev)

@@ -595,7 +595,10 @@ def test_fleet_runs_equal_mixed_kernel(dtype):
         assert torch.equal(getattr(a, k), getattr(b, k)), k
     rtol, atol = (FP32_RTOL, FP32_ATOL) if dtype == torch.float32 else (1e-12, 1e-14)
     for k in ("p", "q", "nu", "act"):
-        ok, err = rowwise_close(host(getattr(a, k)), host(getattr(b, k)), rtol, atol)
+        # actuator states against their operating range: a rotor speed near 0 is the
+        # cancellation of O(100) rad/s terms, so its rounding is relative to those
+        floor = 100.0 if k == "act" else None
+        ok, err = rowwise_close(host(getattr(a, k)), host(getattr(b, k)), rtol, atol, floor)
         assert ok, (k, err)
     # a row reassigned to another vehicle type drops the run table
     a.params.write_row(7, vehs[2])
