@@ -884,7 +884,20 @@ template <typename R>
 UUV_D void flush_obs(const R* s_obs, R* obs, int64_t obs_ld, int obs_dim, int64_t row0, int64_t n) {
   const int rows = (int)min((int64_t)kBlock, n - row0);
   const int total = rows * obs_dim;
-  for (int e = threadIdx.x; e < total; e += kBlock) {
+  if (obs_ld == obs_dim) {  // dense rows: the CTA's rows are one contiguous span
+    R* dst = obs + row0 * obs_ld;
+    const int bytes = total * (int)sizeof(R);
+    if ((((uintptr_t)dst | (uintptr_t)s_obs) & 15) == 0) {  // 16-byte vector copies
+      const int v = bytes >> 4;
+      for (int e = threadIdx.x; e < v; e += kBlock)
+        reinterpret_cast<uint4*>(dst)[e] = reinterpret_cast<const uint4*>(s_obs)[e];
+      for (int e = (v << 4) / (int)sizeof(R) + threadIdx.x; e < total; e += kBlock) dst[e] = s_obs[e];
+    } else {
+      for (int e = threadIdx.x; e < total; e += kBlock) dst[e] = s_obs[e];
+    }
+    return;
+  }
+  for (int e = threadIdx.x; e < total; e += kBlock) {  // strided rows
     const int r = e / obs_dim, c = e - r * obs_dim;
     obs[(row0 + r) * obs_ld + c] = s_obs[e];
   }
@@ -920,7 +933,7 @@ UUV_D void policy_command(const TaskArgs<R>& a, int A, int od, int64_t i, const 
 
 template <typename R, bool DR, int AC, bool DM, bool POL = false>
 __global__ void __launch_bounds__(kBlock, MinB<R>::value) k_task_step(const __grid_constant__ TaskArgs<R> a) {
-  __shared__ R s_obs[kBlock * kObsMax];
+  __shared__ __align__(16) R s_obs[kBlock * kObsMax];
   __shared__ double s_red[kBlock / 32][UUV_ST_COUNT];
   if (POL && a.ep_live != nullptr && a.ep_live[a.ep_t - 1] == 0) return;  // the episode loop broke
   bool live = false;
@@ -1080,7 +1093,7 @@ __global__ void __launch_bounds__(kBlock, MinB<R>::value) k_task_step(const __gr
 // Task reset (mode 1: masked rows reset, prev_u / dev_sum cleared) + observe all rows.
 template <typename R>
 __global__ void __launch_bounds__(kBlock) k_task_reset(const __grid_constant__ TaskArgs<R> a) {
-  __shared__ R s_obs[kBlock * kObsMax];
+  __shared__ __align__(16) R s_obs[kBlock * kObsMax];
   const int64_t row0 = (int64_t)blockIdx.x * kBlock;
   const int64_t i = row0 + threadIdx.x;
   const StateView<R>& sv = a.sv;
