@@ -221,8 +221,8 @@ class DeviceSampler:
                 d.dist, d.mu, d.sigma = N.DIST_GAUSSIAN, dist.mu, dist.sigma
                 d.lo, d.hi = dist.clip
             else:
-                raise EngineError(f"{type(dist).__name__} distributions are sampled by the "
-                                  "host reset path, not the device sampler")
+                raise EngineError(f"{type(dist).__name__}: not a device-encodable distribution "
+                                  "(use a sampler callable for the host reset path)")
 
         keys = self.keys()
         if len(keys) > N.MAX_DRAWS:
