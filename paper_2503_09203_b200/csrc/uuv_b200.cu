@@ -253,12 +253,15 @@ template <typename R, int NT> struct StepArgs {
 UUV_D void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 UUV_D void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 
-// UUV_PDL: 0 off, 1 trigger dependents at kernel entry, 2 (default) trigger after the
-// stores.  Measured on B200 (cfg2, 4096 envs, graph of 100 steps): 2.57 / 3.29 / 2.34 us.
+// UUV_PDL: 0 off, 1 trigger dependents at kernel entry, 2 after the stores, 3 once
+// the loads are issued, 4 (default) = 3 for grids of at most 64 CTAs, else 2.
+// Measured on B200, cfg2 @4096 envs: graph of 100 steps with fixed commands
+// 2.57 / 3.29 / 2.34 us (modes 0/1/2); bench workload (per-step commands from a
+// ring larger than L2) 3.18 / 3.29 / 3.16 / 2.39 us (modes 0/1/2/3).
 static int pdl_mode() {
   static const int m = [] {
     const char* v = getenv("UUV_PDL");
-    return v ? atoi(v) : 2;
+    return v ? atoi(v) : 4;
   }();
   return m;
 }
@@ -649,6 +652,10 @@ __global__ void __launch_bounds__(kBlock, HI ? kMinBHi : ((NT > 1 && sizeof(R) =
   if (i >= n) return;
   StepIn<R> cur;
   load_in<R, NT, AC>(a, i, cur);
+  // mode 3: release the next step once this step's loads are issued -- it is
+  // already past its own wait here, so at most two grids are in flight, and the
+  // next step's command prefetch overlaps this step's compute
+  if (a.early_trigger == 3) pdl_trigger();
 #if UUV_PERSISTENT_STEP
   while (true) {
     const int64_t nx = i + stride;
@@ -1568,7 +1575,15 @@ uuv_status launch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd,
   // persistent (grid-stride + register prefetch) beyond one wave; UUV_STEP_WAVES overrides
   const int64_t waves = step_waves();
   const int64_t grid = waves >= need ? need : std::min<int64_t>(need, wave * waves);
-  a.early_trigger = pdl_mode() == 2 ? 2 : ((grid <= wave && pdl_enabled()) ? 1 : 0);
+  // dependent-launch trigger: small grids (<= 64 CTAs) release the next step as
+  // soon as their loads are issued (mode 3), larger grids after their stores
+  // (mode 2).  Mode 3 overlaps the next step's command fetch with this step's
+  // compute: 3.15 -> 2.35 us per step at 4096 envs when commands come from DRAM
+  // (bench.py's ring), +3-6% when they are L2-hot (a fixed command tensor); at
+  // 16k envs the L2-hot cost reached +12%, hence the cut-off.
+  const int pm = pdl_mode();
+  a.early_trigger = pm == 4 ? (grid <= 64 ? 3 : 2)
+                            : (pm >= 2 ? pm : ((grid <= wave && pdl_enabled()) ? 1 : 0));
   UUV_REGISTER(k_step<R, NT, DR, AC, DM, false>);
   UUV_REGISTER(k_step<R, NT, DR, AC, DM, kHiOk>);
   cudaError_t e = launch_pdl(kern, (unsigned)grid, s, a);
