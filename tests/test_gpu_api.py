@@ -510,3 +510,22 @@ def test_step_server_idle_timeout_and_errors():
         with pytest.raises(E.EngineError):
             with E.serve(st):
                 pass
+
+
+def test_pdl_modes_bitwise():
+    """The dependent-launch trigger mode only changes scheduling: a graph-replayed DR
+    rollout (commands from a ring) ends in the same state bit for bit under every mode."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    out = {}
+    for n in (4096, 40000):
+        for mode in ("0", "2", "3", "4"):
+            env = dict(os.environ, UUV_PDL=mode)
+            r = subprocess.run([sys.executable, os.path.join(here, "pdl_rollout.py"), str(n)],
+                               env=env, capture_output=True, text=True, timeout=240)
+            assert r.returncode == 0, r.stderr[-2000:]
+            out[(n, mode)] = r.stdout.strip().splitlines()[-1]
+        assert len({out[(n, m)] for m in ("0", "2", "3", "4")}) == 1, out
