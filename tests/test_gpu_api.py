@@ -510,6 +510,12 @@ def test_step_server_idle_timeout_and_errors():
         with pytest.raises(E.EngineError):
             with E.serve(st):
                 pass
+    # a grid that cannot be resident in one wave is refused, not deadlocked
+    big = E.make_batch(load_vehicle("bluerov"), E.SimConfig(batch_size=2_000_000))
+    with pytest.raises(E.EngineError, match="one wave"):
+        with E.serve(big):
+            pass
+    E.step_batch(big, torch.zeros((2_000_000, 6), device="cuda"))  # still usable
 
 
 def test_pdl_modes_bitwise():
