@@ -1084,7 +1084,9 @@ __global__ void __launch_bounds__(kBlock, MinB<R>::value) k_task_step(const __gr
       div = false;
       dev = R(0);
     }
-    observe_row<R>(T, A, px, py, pz, q, nu, u, steps, a.dt, srow, nullptr);
+    // (the policy episode loop passes no obs buffer: its next launch recomputes
+    // the observation from the stored state)
+    if (a.obs != nullptr) observe_row<R>(T, A, px, py, pz, q, nu, u, steps, a.dt, srow, nullptr);
     store_state(sv, i, A, px, py, pz, q, nu, act);
     sv.steps[i] = steps;
     sv.diverged[i] = div ? 1 : 0;
