@@ -323,9 +323,10 @@ uuv_status uuv_server_start(uuv_ctx* ctx, const uuv_state* state, int32_t subste
  * or NULL) must be pinned host memory; returns when every env has stepped. */
 uuv_status uuv_server_step(uuv_server* server, const void* host_cmd, int64_t cmd_ld,
                            void* host_pose);
-/* Phase times of the last step, ns (profiling aid; GPU %globaltimer and host
- * CLOCK_REALTIME): doorbell seen, acquire fence done, commands read, physics
- * done (CTA 0), system fence begin / end (last CTA), host ring, host done. */
+/* Phase times of the last step, ns (profiling aid, written when the process
+ * runs with UUV_SERVE_STAMPS=1; GPU %globaltimer and host CLOCK_REALTIME):
+ * doorbell seen, doorbell fields read, commands read, physics done (CTA 0),
+ * system fence begin / end (last CTA), host ring, host done. */
 void uuv_server_stamps(const uuv_server* server, uint64_t out[8]);
 /* Stop the kernel, wait for it and free the server. */
 uuv_status uuv_server_stop(uuv_server* server);

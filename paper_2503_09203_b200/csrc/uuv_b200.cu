@@ -711,6 +711,7 @@ template <typename R, int NT> struct ServeArgs {
   ServeSync* sync;
   uint64_t idle_ns;
   uint32_t sleep_ns;        // back-off between doorbell polls
+  uint32_t stamps;          // write phase stamps (UUV_SERVE_STAMPS=1; profiling aid)
 };
 
 UUV_D uint64_t ld_acquire_sys(const uint64_t* p) {
@@ -788,7 +789,7 @@ __global__ void __launch_bounds__(kBlock, (NT > 1 && sizeof(R) == 4) ? 3 : MinB<
   uint64_t cur_pose = 0;  // CTA 0: pose rows address / command stride of the last step
   int64_t cur_ld = 0;
   ServeSync* sy = sa.sync;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {  // start marker + the idle budget (profiling aid)
+  if (sa.stamps && blockIdx.x == 0 && threadIdx.x == 0) {  // start marker + idle budget
     sa.ctl->stamp[4] = sa.idle_ns;
     sa.ctl->stamp[5] = global_ns();
   }
@@ -804,7 +805,7 @@ __global__ void __launch_bounds__(kBlock, (NT > 1 && sizeof(R) == 4) ? 3 : MinB<
         for (;;) {
           ld_relaxed_sys_v2(&sa.ctl->seq, word, cmd);  // {seq, cmd} in one read
           v = word == kServeQuit ? kServeQuit : (word & ~kServeNewPose);
-          if (v != seq) { why = 1; sa.ctl->stamp[0] = global_ns(); break; }
+          if (v != seq) { why = 1; if (sa.stamps) sa.ctl->stamp[0] = global_ns(); break; }
           // signed: %globaltimer may step back slightly when it is re-synchronised
           if ((int64_t)(global_ns() - t0) > (int64_t)sa.idle_ns) { v = kServeQuit; why = 2; break; }
           __nanosleep(sa.sleep_ns);
@@ -823,7 +824,7 @@ __global__ void __launch_bounds__(kBlock, (NT > 1 && sizeof(R) == 4) ? 3 : MinB<
         }
         s_pose = cur_pose;
         s_ld = cur_ld;
-        sa.ctl->stamp[1] = global_ns();
+        if (sa.stamps) sa.ctl->stamp[1] = global_ns();
         sy->cmd = s_cmd;
         sy->pose = s_pose;
         sy->cmd_ld = s_ld;
@@ -843,7 +844,7 @@ __global__ void __launch_bounds__(kBlock, (NT > 1 && sizeof(R) == 4) ? 3 : MinB<
     __syncthreads();
     const uint64_t v = s_seq;
     if (v == kServeQuit) break;
-    const bool stamp = blockIdx.x == 0 && threadIdx.x == 0;
+    const bool stamp = sa.stamps && blockIdx.x == 0 && threadIdx.x == 0;
     if (live) {
       // plain coalesced loads over the link (after the GPU-scope acquire above;
       // L1-bypassing .cg/.cv loads of host memory were far slower at scale)
@@ -878,9 +879,9 @@ __global__ void __launch_bounds__(kBlock, (NT > 1 && sizeof(R) == 4) ? 3 : MinB<
       if (atomicAdd(&sy->arrived, 1u) == gridDim.x - 1) {
         __threadfence();
         sy->arrived = 0;
-        sa.ctl->stamp[4] = global_ns();
+        if (sa.stamps) sa.ctl->stamp[4] = global_ns();
         __threadfence_system();
-        sa.ctl->stamp[5] = global_ns();
+        if (sa.stamps) sa.ctl->stamp[5] = global_ns();
         st_release_sys(sa.done, v);
       }
     }
@@ -1883,6 +1884,11 @@ uuv_status serve_kernel(const uuv_ctx* ctx, const uuv_state* st, int32_t K, doub
     return v ? (uint32_t)atoi(v) : 0u;
   }();
   sa.sleep_ns = sleep_ns;
+  static const uint32_t stamps = [] {
+    const char* v = getenv("UUV_SERVE_STAMPS");
+    return v ? (uint32_t)atoi(v) : 0u;
+  }();
+  sa.stamps = stamps;
 
   const int64_t grid = grid_for(st->n_envs);
   if (grid > one_wave_ctas(k_serve<R, NT, DR, AC, DM>))

@@ -1,5 +1,7 @@
 """Served-step cost split: step_batch (Python) vs the bare C call vs GPU-side phases."""
 import ctypes
+import os
+os.environ.setdefault("UUV_SERVE_STAMPS", "1")
 import sys
 import time
 

@@ -19,6 +19,8 @@ cmd = (torch.rand((n, 6)) * 2 - 1).pin_memory()
 out = torch.empty((13, n)).pin_memory()
 lat = []
 import ctypes
+import os
+os.environ.setdefault("UUV_SERVE_STAMPS", "1")
 from paper_2503_09203_b200 import _native as N
 stamps = []
 with E.serve(st, idle_timeout_ms=2000) as srv:
