@@ -148,3 +148,12 @@ def test_sampler_packs_gaussian_draws():
     assert smp.overlay[1].dist == N.DIST_UNIFORM
     assert smp.current_speed.dist == N.DIST_GAUSSIAN and smp.current_speed.sigma == 0.05
     assert isinstance(DeviceSampler(spec), DeviceSampler)
+
+
+def test_every_distribution_is_device_encodable():
+    from paper_2503_09203_b200.randomization import Piecewise, device_encodable
+
+    spec = {"mass*": DRParameter("mass*", Gaussian(1.0, 0.1, (0.8, 1.2))),
+            "volume*": DRParameter("volume*", Uniform(0.9, 1.1)),
+            "damping*": DRParameter("damping*", Piecewise([0.5, 1.0, 1.5], [1.0, 3.0]))}
+    assert device_encodable(spec) and device_encodable(None)
