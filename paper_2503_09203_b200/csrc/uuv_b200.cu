@@ -1633,8 +1633,9 @@ uuv_status dispatch_one(const uuv_ctx* ctx, const uuv_state* st, int type, const
 
 // Mixed fleet in contiguous per-type runs: one specialised launch per run, the
 // runs on forked streams (run 0 on the caller's) so they execute concurrently;
-// the caller's stream then joins them.  Same arithmetic as the mixed-fleet
-// kernel's per-type paths, so results are identical.
+// the caller's stream then joins them.  Same source as the mixed-fleet kernel's
+// per-type paths; the separate compilations may contract FMAs differently, so
+// results agree to rounding (tests/test_gpu_parity.py::test_fleet_runs...).
 static int64_t runs_min_envs() {
   static const int64_t v = [] {
     const char* e = getenv("UUV_RUNS_MIN_ENVS");
