@@ -283,14 +283,18 @@ int32_t uuv_abi_version(void);
 /* sizeof of the ABI structs, for binding self-checks: hull, state, sampler, task, task_io. */
 void uuv_abi_sizes(int64_t out[6]);  /* sizeof hull, state, sampler, task, task_io, policy */
 
-/* Context: owns the hull list of one batch (host copy; travels by value in each launch). */
+/* Context: owns the hull list of one batch (host copy; travels by value in each launch).
+ * Replaces compile_layout / VehicleLayout (engine.py:84-189) and the per-vehicle
+ * part of make_batch (engine.py:298-326). */
 uuv_status uuv_ctx_create(const uuv_hull* hulls, int32_t n_types, uuv_ctx** out);
 uuv_status uuv_ctx_set_hulls(uuv_ctx* ctx, const uuv_hull* hulls, int32_t n_types);
 void uuv_ctx_destroy(uuv_ctx* ctx);
 
 /* Advance every env one control step of `substeps` fused physics substeps
  * (dt_sub = dt / substeps).  commands: (n_envs, cmd_ld) row-major Real,
- * clipped to [-1, 1] inside. */
+ * clipped to [-1, 1] inside.  Replaces step_batch (engine.py:465-484) with
+ * _step_slice / _substeps (engine.py:405-449); non-finite rows freeze and set
+ * diverged (engine.py:435-449), never an error. */
 uuv_status uuv_step(uuv_ctx* ctx, const uuv_state* st, const void* commands, int64_t cmd_ld,
                     int32_t substeps, double dt, void* stream);
 
@@ -305,7 +309,6 @@ uuv_status uuv_step_host(uuv_ctx* ctx, const uuv_state* st, const void* host_cmd
                          void* dev_cmd, void* host_pose, int32_t substeps, double dt,
                          void* stream, int32_t sync);
 
-/* Reset rows with mask[i] != 0 (mask NULL = all rows) from the declarative sampler. */
 /*
  * Step server: a resident kernel that advances the batch one control step each
  * time the host rings a doorbell in mapped pinned memory -- no kernel launch and
@@ -320,7 +323,9 @@ typedef struct uuv_server uuv_server;
 uuv_status uuv_server_start(uuv_ctx* ctx, const uuv_state* state, int32_t substeps, double dt,
                             void* stream, int32_t idle_timeout_ms, uuv_server** out);
 /* One step: host_cmd (n_envs, cmd_ld) and host_pose ((13, n_envs) rows p, q, nu,
- * or NULL) must be pinned host memory; returns when every env has stepped. */
+ * or NULL) must be pinned host memory; returns when every env has stepped.
+ * Replaces step_batch (engine.py:465-484) called step after step with host
+ * (numpy) arrays. */
 uuv_status uuv_server_step(uuv_server* server, const void* host_cmd, int64_t cmd_ld,
                            void* host_pose);
 /* Phase times of the last step, ns (profiling aid, written when the process
@@ -331,28 +336,37 @@ void uuv_server_stamps(const uuv_server* server, uint64_t out[8]);
 /* Stop the kernel, wait for it and free the server. */
 uuv_status uuv_server_stop(uuv_server* server);
 
+/* Reset rows with mask[i] != 0 (mask NULL = all rows) from the declarative
+ * sampler: episodes += 1, per-(seed, env, episode) stream, overlay draws, start
+ * state.  Replaces reset_envs (engine.py:487-512) with sample_overlay /
+ * sample_current (randomization.py:213-234) and apply_overlay
+ * (vehicles/__init__.py:443-505). */
 uuv_status uuv_reset(uuv_ctx* ctx, const uuv_state* st, const uint8_t* mask,
                      const uuv_sampler* sampler, uint64_t seed, void* stream);
 
-/* Fused task step: physics, reward/termination/info, auto-reset, next obs. */
+/* Fused task step: physics, reward/termination/info, auto-reset, next obs.
+ * Replaces VecTaskEnv.step (tasks/core.py:328-370) with the per-task
+ * _task_step / reward functions (tasks/core.py:170-214, 409-520). */
 uuv_status uuv_task_step(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task,
                          const uuv_sampler* sampler, uint64_t seed, const void* commands,
                          int64_t cmd_ld, int32_t substeps, double dt, const uuv_task_io* io,
                          void* stream);
 
-/* Reset masked rows (prev_u and dev_sum zeroed too), then observe all rows. */
 /* uuv_task_step with the commands computed on the device by a policy
  * population (uuv_policy); io->obs may be NULL (the observation is recomputed
  * in-kernel from the state).  Replaces the act_fn(obs) -> env.step round trip
- * of baseline._rollout_returns / evaluate / cem_train. */
+ * of baseline._rollout_returns / evaluate / cem_train (baseline.py:109-192). */
 uuv_status uuv_policy_step(uuv_ctx* ctx, const uuv_state* state, const uuv_task* task,
                            const uuv_sampler* sampler, uint64_t seed, const uuv_policy* policy,
                            int32_t substeps, double dt, const uuv_task_io* io, void* stream);
+/* Reset masked rows (prev_u and dev_sum zeroed too), then observe all rows.
+ * Replaces VecTaskEnv.reset (tasks/core.py:294-301). */
 uuv_status uuv_task_reset(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task,
                           const uuv_sampler* sampler, uint64_t seed, const uint8_t* mask,
                           double dt, const uuv_task_io* io, void* stream);
 
-/* Observation of every row into io->obs. */
+/* Observation of every row into io->obs.  Replaces VecTaskEnv.observe
+ * (tasks/core.py:316-321). */
 uuv_status uuv_observe(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task, double dt,
                        const uuv_task_io* io, void* stream);
 
@@ -360,7 +374,8 @@ uuv_status uuv_observe(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task, 
 int64_t uuv_stats_blocks(int64_t n_envs);
 
 /* Reduce io->stats over blocks (fixed order) into out[UUV_ST_COUNT] (device float64);
- * reset != 0 zeroes the running sums afterwards. */
+ * reset != 0 zeroes the running sums afterwards.  Replaces the numpy return
+ * reduction of baseline._rollout_returns (baseline.py:109-127). */
 uuv_status uuv_rollout_stats(const double* stats, int64_t n_blocks, double* out, int32_t reset,
                              void* stream);
 
