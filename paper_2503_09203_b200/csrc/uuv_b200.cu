@@ -336,7 +336,14 @@ UUV_D bool physics_at(const Hull<R>& H, const StateView<R>& sv, int64_t i, const
   const double* jit = nullptr;
   if (DR) {
     EnvD e;
+#ifdef UUV_EXP_NODERIVE  // diagnostic build only (scripts/gpu_ab_exp.sh): hull values, no record reads
+    {
+      const int32_t none[UUV_OV_COUNT] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
+      derive_env(H.d, ov, ov_ld, ov_i, none, e);
+    }
+#else
     derive_env(H.d, ov, ov_ld, ov_i, sv.slot, e);
+#endif
     sub_from_env<R, DM>(H.r, e, s);
     if (sv.slot[UUV_OV_JITTER] >= 0) jit = sv.ov + sv.slot[UUV_OV_JITTER] * sv.ld + i;
   }
