@@ -25,6 +25,39 @@ from paper_2503_09203_b200.vehicles import BUILTIN_VEHICLES, load_vehicle  # noq
 
 PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
     if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+# FP32 side of the per-step roofline: the FFMA-chain measurement of this pool's
+# B200s (scripts/probes/fp32_peak.cu -> profiles/r01/fp32_peak.json); else the
+# nominal 148 SM x 128 lanes x 2 flops x 1.965 GHz.
+_FP32 = os.path.join(ROOT, "profiles", "r01", "fp32_peak.json")
+FP32_TFLOPS, FP32_SOURCE = (json.load(open(_FP32))["fp32_tflops"], "measured") \
+    if os.path.exists(_FP32) else (74.4, "nominal")
+
+# Executed flops per substep (SURVEY.md §8(d) counting: +,-,x,/ = 1, FMA = 2,
+# sqrt/sin/cos/atan2 = 1, clamps 0): 5A + 16P + 87F + 6(A-1) + C with C = 332 on
+# the diagonal-hull, r_g = 0 path the kernel specialises (bluerov, bluerov_heavy,
+# lauv) and 638 for the general formulation (iauv, hauv: r_g != 0); + 33 for the
+# current-relative velocity R(q)^T c.  Task layer (obs, reward, termination):
+# ~250 per frame (SURVEY's upper estimate).
+FLEET_SHAPE = {"bluerov": (6, 6, 0, True), "bluerov_heavy": (8, 8, 0, True),
+               "lauv": (5, 1, 4, True), "iauv": (5, 1, 4, False), "hauv": (8, 8, 0, False)}
+TASK_FLOPS = 250
+
+
+def substep_flops(vehicle, current=False):
+    a, p, f, dm = FLEET_SHAPE[vehicle]
+    return 5 * a + 16 * p + 87 * f + 6 * (a - 1) + (332 if dm else 638) + (33 if current else 0)
+
+
+def roofline(us_per_step, n, bpf, fpf):
+    """Per-step roofline: the slower of n*bpf bytes at the HBM copy bandwidth and
+    n*fpf flops at the FP32 peak; frac = roofline time / measured time."""
+    t_hbm = n * bpf / (PEAK * 1e9) * 1e6
+    t_fp = n * fpf / (FP32_TFLOPS * 1e12) * 1e6
+    return {"flops_per_frame": fpf, "tflops": n * fpf / us_per_step / 1e6,
+            "frac_fp32": t_fp / us_per_step, "roofline_us": max(t_hbm, t_fp),
+            "bound": "hbm" if t_hbm >= t_fp else "fp32",
+            "frac_roofline": max(t_hbm, t_fp) / us_per_step,
+            "fp32_peak_tflops": FP32_TFLOPS, "fp32_peak_source": FP32_SOURCE}
 
 
 def frame_bytes(a, n_dr, cur, dtype_bytes=4, mixed=False):
@@ -46,6 +79,7 @@ def make_case(name, n):
         a_mean = sum(v.action_dim * c for v, c in zip(vehs, counts)) / n
         width = st.a_max
         bpf = frame_bytes(a_mean, 0, False, mixed=True)
+        fpf = sum(substep_flops(v.name) * c for v, c in zip(vehs, counts)) / n
     elif name.startswith("cfg2") or name.startswith("bluerov"):
         veh = load_vehicle("bluerov")
         substeps = 8 if name.endswith("k8") else 1
@@ -56,12 +90,14 @@ def make_case(name, n):
                      E.spec_sampler(spec or None))
         width = 6
         bpf = frame_bytes(6, len(keys), False)
+        fpf = substep_flops("bluerov") * substeps
     elif name.startswith("veh:"):  # one vehicle, no DR: veh:<name>
         veh = load_vehicle(name[4:])
         st = E.make_batch(veh, E.SimConfig(batch_size=n), device=dev)
         E.reset_envs(st, torch.ones(n, dtype=torch.bool, device=dev))
         width = veh.action_dim
         bpf = frame_bytes(width, 0, False)
+        fpf = substep_flops(name[4:])
     elif name == "cfg5_physics":  # bluerov_heavy + train preset (7 ratios) + current
         veh = load_vehicle("bluerov_heavy")
         st = E.make_batch(veh, E.SimConfig(batch_size=n), device=dev)
@@ -69,9 +105,11 @@ def make_case(name, n):
                      E.spec_sampler(preset("train")))
         width = 8
         bpf = frame_bytes(8, 7, True)
+        # payload / cobm draws move r_g: counted with the general formulation
+        fpf = 5 * 8 + 16 * 8 + 6 * 7 + 638 + 33
     else:
         raise ValueError(name)
-    return st, width, bpf
+    return st, width, bpf, fpf
 
 
 def measure_task(name, n, steps):
@@ -83,10 +121,18 @@ def measure_task(name, n, steps):
         task = TaskConfig(task="tracking", vehicle="bluerov", level="disturbed")
         env = make_env(task, E.SimConfig(batch_size=n, substeps=8), seed=0, device=dev)
         a = 6
+        # physics 198 B (current) + task: obs 4*(12+6+3), reward 4, term/trunc 2,
+        # prev_u 8*6, _dev_sum 8; flops 8 substeps + task layer
+        bpf = frame_bytes(6, 0, True) + 4 * (12 + 6 + 3) + 4 + 2 + 8 * 6 + 8
+        fpf = 8 * substep_flops("bluerov", current=True) + TASK_FLOPS
     else:  # task_cfg5: docking, train-preset DR, auto-reset on
         task = TaskConfig(task="docking", vehicle="bluerov_heavy", level="disturbed_dr")
         env = make_env(task, E.SimConfig(batch_size=n), seed=0, device=dev)
         a = 8
+        # physics 278 B (train DR: 7 ratios + current) + obs 4*(12+8+1), reward 4,
+        # term/trunc 2, prev_u 8*8
+        bpf = frame_bytes(8, 7, True) + 4 * (12 + 8 + 1) + 4 + 2 + 8 * 8
+        fpf = 5 * 8 + 16 * 8 + 6 * 7 + 638 + 33 + TASK_FLOPS
     env.reset()
     cmds = torch.rand((n, a), device=dev) * 2 - 1
     s = torch.cuda.Stream(dev)
@@ -112,14 +158,17 @@ def measure_task(name, n, steps):
         t = e0.elapsed_time(e1) / 1e3 / steps
         best = t if best is None else min(best, t)
     stats = env.rollout_stats()
+    gbs = n * bpf / best / 1e9
     return {"case": name, "n": n, "us_per_step": best * 1e6, "frames_per_s": n / best,
+            "bytes_per_frame": bpf, "gbs": gbs, "frac_hbm": gbs / PEAK,
+            **roofline(best * 1e6, n, bpf, fpf),
             "finished_per_frame": stats["finished"] / max(stats["frames"], 1)}
 
 
 def measure(name, n, steps):
     if name.startswith("task_"):
         return measure_task(name, n, steps)
-    st, width, bpf = make_case(name, n)
+    st, width, bpf, fpf = make_case(name, n)
     dev = st.device
     cmds = torch.rand((n, width), device=dev) * 2 - 1
     s = torch.cuda.Stream(dev)
@@ -147,6 +196,7 @@ def measure(name, n, steps):
     gbs = n * bpf / best / 1e9
     return {"case": name, "n": n, "us_per_step": best * 1e6, "frames_per_s": n / best,
             "bytes_per_frame": bpf, "gbs": gbs, "frac_hbm": gbs / PEAK,
+            **roofline(best * 1e6, n, bpf, fpf),
             "diverged": int(st.diverged.sum().item())}
 
 
