@@ -81,6 +81,12 @@ constexpr int kMinBHi = 5;
 #ifndef UUV_HI_OCC_MIN_ENVS
 #define UUV_HI_OCC_MIN_ENVS 131072
 #endif
+// Min CTAs/SM of the float task-step kernel (A/B builds override it).
+#ifndef UUV_MINB_TASK_F32
+#define UUV_MINB_TASK_F32 UUV_MINB_F32
+#endif
+template <typename R> struct MinBTask { static constexpr int value = MinB<R>::value; };
+template <> struct MinBTask<float> { static constexpr int value = UUV_MINB_TASK_F32; };
 
 uuv_status fail(uuv_status s, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
 uuv_status fail(uuv_status s, const char* fmt, ...) {
@@ -986,7 +992,7 @@ UUV_D void policy_command(const TaskArgs<R>& a, int A, int od, int64_t i, const 
 }
 
 template <typename R, bool DR, int AC, bool DM, bool POL = false>
-__global__ void __launch_bounds__(kBlock, MinB<R>::value) k_task_step(const __grid_constant__ TaskArgs<R> a) {
+__global__ void __launch_bounds__(kBlock, MinBTask<R>::value) k_task_step(const __grid_constant__ TaskArgs<R> a) {
   __shared__ __align__(16) R s_obs[kBlock * kObsMax];
   __shared__ double s_red[kBlock / 32][UUV_ST_COUNT];
   if (POL && a.ep_live != nullptr && a.ep_live[a.ep_t - 1] == 0) return;  // the episode loop broke
@@ -1579,7 +1585,9 @@ uuv_status launch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd,
     const char* v = getenv("UUV_HI_OCC_MIN_ENVS");
     return v ? (int64_t)atoll(v) : (int64_t)UUV_HI_OCC_MIN_ENVS;
   }();
-  const bool hi = kHiOk && st->n_envs >= hi_min;
+  // K = 1 only: with fused substeps the kernel is issue-bound and the uncapped
+  // build is faster (cfg2 K = 8: 1M envs 129.4 -> 127.3 us, 4M 503.8 -> 495.1 us)
+  const bool hi = kHiOk && st->n_envs >= hi_min && K == 1;
   auto kern = hi ? k_step<R, NT, DR, AC, DM, kHiOk> : k_step<R, NT, DR, AC, DM, false>;
   const int64_t wave = one_wave_ctas(kern);
   // persistent (grid-stride + register prefetch) beyond one wave; UUV_STEP_WAVES overrides
