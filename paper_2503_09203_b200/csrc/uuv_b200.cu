@@ -334,7 +334,7 @@ UUV_D void store_state(const StateView<R>& sv, int64_t i, int A, R px, R py, R p
 // Physics of one control step for env i; returns the post-step diverged flag.
 // K substeps for one env.  The overlay record is read at (ov, ov_ld, ov_i) — global
 // memory or a shared-memory slab; jitter always comes from the global record.
-template <typename R, bool DR, int AC, bool DM>
+template <typename R, bool DR, int AC, bool DM, bool PRE = false>
 UUV_D bool physics_at(const Hull<R>& H, const StateView<R>& sv, int64_t i, const double* ov,
                       int64_t ov_ld, int64_t ov_i, bool has_cur, V3<R> cur, int K, R dt,
                       const R* u, R& px, R& py, R& pz, Q4<R>& q, R* nu, R* act) {
@@ -350,7 +350,7 @@ UUV_D bool physics_at(const Hull<R>& H, const StateView<R>& sv, int64_t i, const
 #else
     derive_env(H.d, ov, ov_ld, ov_i, sv.slot, e);
 #endif
-    sub_from_env<R, DM>(H.r, e, s);
+    sub_from_env<R, DM, PRE, AC>(H.r, e, s);
     if (sv.slot[UUV_OV_JITTER] >= 0) jit = sv.ov + sv.slot[UUV_OV_JITTER] * sv.ld + i;
   }
   bool ok = true;
@@ -358,7 +358,7 @@ UUV_D bool physics_at(const Hull<R>& H, const StateView<R>& sv, int64_t i, const
   // specialisation per case keeps its code out of the common loop
   auto run = [&](auto with_jit) {
     for (int k = 0; k < K; ++k) {
-      if (!substep<R, DR, false, AC, DM, decltype(with_jit)::value>(
+      if (!substep<R, DR, false, AC, DM, decltype(with_jit)::value, PRE>(
               H.r, s, jit, sv.ld, px, py, pz, q, nu, act, u, has_cur, cur, dt, nullptr)) {
         ok = false;
         break;
@@ -370,13 +370,13 @@ UUV_D bool physics_at(const Hull<R>& H, const StateView<R>& sv, int64_t i, const
   return !ok;
 }
 
-template <typename R, bool DR, int AC, bool DM>
+template <typename R, bool DR, int AC, bool DM, bool PRE = false>
 UUV_D bool physics(const Hull<R>& H, const StateView<R>& sv, int64_t i, int K, R dt, const R* u,
                    R& px, R& py, R& pz, Q4<R>& q, R* nu, R* act) {
   const bool has_cur = sv.cur != nullptr;
   V3<R> cur{R(0), R(0), R(0)};
   if (has_cur) cur = V3<R>{sv.cur[i], sv.cur[sv.ld + i], sv.cur[2 * sv.ld + i]};
-  return physics_at<R, DR, AC, DM>(H, sv, i, sv.ov, sv.ld, i, has_cur, cur, K, dt, u, px, py, pz,
+  return physics_at<R, DR, AC, DM, PRE>(H, sv, i, sv.ov, sv.ld, i, has_cur, cur, K, dt, u, px, py, pz,
                                    q, nu, act);
 }
 
@@ -562,8 +562,8 @@ UUV_D void step_env(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in) {
     }
     const Hull<R>& H = a.hull[in.ty];
     const int A = AC > 0 ? AC : H.r.n_act;
-    const bool div = physics<R, DR, AC, DM>(H, sv, i, a.K, a.dt, in.u, in.px, in.py, in.pz,
-                                            in.q, in.nu, in.act);
+    const bool div = physics<R, DR, AC, DM, true>(H, sv, i, a.K, a.dt, in.u, in.px, in.py, in.pz,
+                                                  in.q, in.nu, in.act);
     store_state(sv, i, A, in.px, in.py, in.pz, in.q, in.nu, in.act);
     sv.diverged[i] = div ? 1 : 0;
     sv.steps[i] = in.steps + 1;
@@ -577,7 +577,7 @@ UUV_D void step_env(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in) {
   // the branch (register pressure; +40% otherwise).
   const Hull<R>& H = a.hull[in.ty];
   const int A = AC > 0 ? AC : H.r.n_act;
-  const bool div = physics<R, DR, AC, DM>(H, sv, i, a.K, a.dt, in.u, in.px, in.py, in.pz, in.q,
+  const bool div = physics<R, DR, AC, DM, true>(H, sv, i, a.K, a.dt, in.u, in.px, in.py, in.pz, in.q,
                                           in.nu, in.act);
   if (!in.div) {
     store_state(sv, i, A, in.px, in.py, in.pz, in.q, in.nu, in.act);
@@ -764,8 +764,8 @@ UUV_D void serve_env(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in, R* pose
   if (!in.div) {
     const Hull<R>& H = a.hull[in.ty];
     const int A = AC > 0 ? AC : H.r.n_act;
-    const bool div = physics<R, DR, AC, DM>(H, sv, i, a.K, a.dt, in.u, in.px, in.py, in.pz,
-                                            in.q, in.nu, in.act);
+    const bool div = physics<R, DR, AC, DM, true>(H, sv, i, a.K, a.dt, in.u, in.px, in.py, in.pz,
+                                                  in.q, in.nu, in.act);
     store_state(sv, i, A, in.px, in.py, in.pz, in.q, in.nu, in.act);
     in.div = div ? 1 : 0;
     sv.diverged[i] = in.div;
