@@ -26,7 +26,7 @@ def main():
     args = ap.parse_args()
     if args.case.startswith("task_") or args.case == "policy":
         return task_case(args)
-    st, width, _ = make_case(args.case, args.n)
+    st, width = make_case(args.case, args.n)[:2]
     cmds = torch.rand((args.n, width), device=st.device) * 2 - 1
     for _ in range(args.steps):
         E.step_batch(st, cmds)
