@@ -40,7 +40,44 @@
 extern "C" {
 #endif
 
-#define UUV_ABI_VERSION 4
+/*
+ * DLPack (https://github.com/dmlc/dlpack, the v0.8/v1.0 ABI, unversioned
+ * DLTensor) -- declared here only when the real dlpack.h has not been included,
+ * so either header can come first.  The tensor-taking entry points below
+ * (uuv_*_dl) borrow the DLTensor for the call: nothing is retained and the
+ * caller's deleter is never invoked.
+ */
+#ifndef DLPACK_DLPACK_H_
+#define DLPACK_DLPACK_H_
+typedef enum { kDLCPU = 1, kDLCUDA = 2, kDLCUDAHost = 3, kDLCUDAManaged = 13 } DLDeviceType;
+typedef struct {
+  DLDeviceType device_type;
+  int32_t device_id;
+} DLDevice;
+typedef enum { kDLInt = 0, kDLUInt = 1, kDLFloat = 2, kDLOpaqueHandle = 3, kDLBfloat = 4,
+               kDLComplex = 5, kDLBool = 6 } DLDataTypeCode;
+typedef struct {
+  uint8_t code;
+  uint8_t bits;
+  uint16_t lanes;
+} DLDataType;
+typedef struct {
+  void* data;
+  DLDevice device;
+  int32_t ndim;
+  DLDataType dtype;
+  int64_t* shape;
+  int64_t* strides;        /* in elements; NULL = compact row-major */
+  uint64_t byte_offset;
+} DLTensor;
+typedef struct DLManagedTensor {
+  DLTensor dl_tensor;
+  void* manager_ctx;
+  void (*deleter)(struct DLManagedTensor* self);
+} DLManagedTensor;
+#endif
+
+#define UUV_ABI_VERSION 5
 #define UUV_MAX_RUNS 8
 #define UUV_MAX_ACT 8        /* actuator columns per vehicle type             */
 #define UUV_MAX_TYPES 6      /* vehicle types in one batch (mixed fleets)     */
@@ -298,15 +335,25 @@ void uuv_ctx_destroy(uuv_ctx* ctx);
 uuv_status uuv_step(uuv_ctx* ctx, const uuv_state* st, const void* commands, int64_t cmd_ld,
                     int32_t substeps, double dt, void* stream);
 
+/* Host-side result of one step: every field the reference's step_batch mutates
+ * in place (engine.py:418, 444-449), as row-major host arrays (n = n_envs).  Any
+ * field may be NULL (not returned). */
+typedef struct {
+  void* pose;              /* (13, n) Real: p (3), q (4), nu (6)                 */
+  void* act;               /* (n_act, n) Real; n_act = command width             */
+  int32_t* steps;          /* (n)                                                */
+  uint8_t* diverged;       /* (n)                                                */
+} uuv_host_out;
+
 /* Host-buffer variant of uuv_step for callers whose commands and results live in
- * host memory: commands host_cmd (n_envs, cmd_ld) in, and, if host_pose != NULL,
- * the pose rows p, q, nu out as a row-major (13, n_envs) array; sync != 0 waits.
- * When both buffers are pinned (mapped) host memory the step kernel reads the
- * commands and stores the pose rows over the host link itself (no copy-engine
- * round trips; UUV_HOST_STEP=copy forces the copy path); otherwise the commands
- * are staged through dev_cmd with async copies. */
+ * host memory: commands host_cmd (n_envs, cmd_ld) in, the step's result rows out
+ * into `out` (may be NULL); sync != 0 waits.  When every buffer is pinned
+ * (mapped) host memory the step kernel reads the commands and stores the result
+ * rows over the host link itself (no copy-engine round trips; UUV_HOST_STEP=copy
+ * forces the copy path); otherwise the commands are staged through dev_cmd and
+ * the results copied back with async copies. */
 uuv_status uuv_step_host(uuv_ctx* ctx, const uuv_state* st, const void* host_cmd, int64_t cmd_ld,
-                         void* dev_cmd, void* host_pose, int32_t substeps, double dt,
+                         void* dev_cmd, const uuv_host_out* out, int32_t substeps, double dt,
                          void* stream, int32_t sync);
 
 /*
@@ -322,12 +369,12 @@ uuv_status uuv_step_host(uuv_ctx* ctx, const uuv_state* st, const void* host_cmd
 typedef struct uuv_server uuv_server;
 uuv_status uuv_server_start(uuv_ctx* ctx, const uuv_state* state, int32_t substeps, double dt,
                             void* stream, int32_t idle_timeout_ms, uuv_server** out);
-/* One step: host_cmd (n_envs, cmd_ld) and host_pose ((13, n_envs) rows p, q, nu,
- * or NULL) must be pinned host memory; returns when every env has stepped.
- * Replaces step_batch (engine.py:465-484) called step after step with host
- * (numpy) arrays. */
+/* One step: host_cmd (n_envs, cmd_ld) and every non-NULL field of `out` must be
+ * pinned host memory; returns when every env has stepped and its result rows
+ * are in host memory.  Replaces step_batch (engine.py:465-484) called step after
+ * step with host (numpy) arrays. */
 uuv_status uuv_server_step(uuv_server* server, const void* host_cmd, int64_t cmd_ld,
-                           void* host_pose);
+                           const uuv_host_out* out);
 /* Phase times of the last step, ns (profiling aid, written when the process
  * runs with UUV_SERVE_STAMPS=1; GPU %globaltimer and host CLOCK_REALTIME):
  * doorbell seen, doorbell fields read, commands read, physics done (CTA 0),
@@ -335,6 +382,42 @@ uuv_status uuv_server_step(uuv_server* server, const void* host_cmd, int64_t cmd
 void uuv_server_stamps(const uuv_server* server, uint64_t out[8]);
 /* Stop the kernel, wait for it and free the server. */
 uuv_status uuv_server_stop(uuv_server* server);
+
+/*
+ * DLPack boundary.  The reference's BatchState fields (engine.py:270-295) as
+ * borrowed DLPack tensors, validated in C (dtype, device, shape, strides):
+ *   UUV_DL_P (N,3), UUV_DL_Q (N,4) wxyz, UUV_DL_NU (N,6), UUV_DL_ACT (N,a_max),
+ *   UUV_DL_CURRENT (N,3) or NULL: float32 or float64 (all alike), strides
+ *   (1, ld) -- the struct-of-arrays layout, one ld >= N for every field;
+ *   UUV_DL_STEPS, UUV_DL_EPISODES (N,) int32; UUV_DL_DIVERGED (N,) bool or
+ *   uint8; unit stride.  Every tensor lives on the current CUDA device.
+ * uuv_state_from_dlpack fills dtype, a_max, n_envs, ld and the state pointers of
+ * `st`; the batch-internal fields (type_id, overlay record, runs, env_offset,
+ * flags) are left as the caller set them.
+ */
+enum { UUV_DL_P = 0, UUV_DL_Q, UUV_DL_NU, UUV_DL_ACT, UUV_DL_CURRENT, UUV_DL_STEPS,
+       UUV_DL_EPISODES, UUV_DL_DIVERGED, UUV_DL_COUNT };
+uuv_status uuv_state_from_dlpack(uuv_state* st, const DLTensor* const* fields, int32_t n_fields);
+
+/* uuv_step with the commands as a DLPack tensor (n_envs, width), width = the
+ * command width (action_dim; a_max for mixed fleets), the state's dtype and
+ * device, unit column stride (any row stride >= width).  The entry point a
+ * DLPack caller of step_batch (engine.py:465-484) binds. */
+uuv_status uuv_step_dl(uuv_ctx* ctx, const uuv_state* st, const DLTensor* commands,
+                       int32_t substeps, double dt, void* stream);
+
+/* uuv_reset with the mask as a DLPack tensor (n_envs,) bool/uint8, unit stride,
+ * or NULL for every row (reset_envs, engine.py:487-512). */
+uuv_status uuv_reset_dl(uuv_ctx* ctx, const uuv_state* st, const DLTensor* mask,
+                        const uuv_sampler* sampler, uint64_t seed, void* stream);
+
+/* uuv_task_step with DLPack commands (as uuv_step_dl) and the next observation
+ * written into `obs` (n_envs, obs_dim) of the state's dtype, unit column stride;
+ * io->obs is ignored (VecTaskEnv.step, tasks/core.py:328-370). */
+uuv_status uuv_task_step_dl(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task,
+                            const uuv_sampler* sampler, uint64_t seed, const DLTensor* commands,
+                            int32_t substeps, double dt, const uuv_task_io* io,
+                            const DLTensor* obs, void* stream);
 
 /* Reset rows with mask[i] != 0 (mask NULL = all rows) from the declarative
  * sampler: episodes += 1, per-(seed, env, episode) stream, overlay draws, start

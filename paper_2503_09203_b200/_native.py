@@ -35,7 +35,7 @@ OV_WIDTH["payload_position"] = 3
 OV_WIDTH["mount_position_jitter"] = 3 * MAX_ACT
 OV_IDENTITY = {k: (1.0 if i <= OV_INDEX["thrust_coeff*"] else 0.0) for i, k in enumerate(OV_KEYS)}
 
-ABI_VERSION = 4
+ABI_VERSION = 5
 MAX_RUNS = 8  # UUV_MAX_RUNS
 DIST_UNIFORM, DIST_PIECEWISE, DIST_GAUSSIAN = 0, 1, 2
 START_IDENTITY, START_BOX = 0, 1
@@ -138,6 +138,57 @@ class Policy(C.Structure):
                 ("t", C.c_int32), ("pad_", C.c_int32)]
 
 
+class HostOut(C.Structure):
+    """uuv_host_out: pinned host result rows of one step (any field may be NULL)."""
+    _fields_ = [("pose", C.c_void_p), ("act", C.c_void_p), ("steps", C.c_void_p),
+                ("diverged", C.c_void_p)]
+
+
+# DLPack (unversioned DLTensor, as declared in the header)
+class DLDevice(C.Structure):
+    _fields_ = [("device_type", C.c_int32), ("device_id", C.c_int32)]
+
+
+class DLDataType(C.Structure):
+    _fields_ = [("code", C.c_uint8), ("bits", C.c_uint8), ("lanes", C.c_uint16)]
+
+
+class DLTensor(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("device", DLDevice), ("ndim", C.c_int32),
+                ("dtype", DLDataType), ("shape", C.POINTER(C.c_int64)),
+                ("strides", C.POINTER(C.c_int64)), ("byte_offset", C.c_uint64)]
+
+
+DL_P, DL_Q, DL_NU, DL_ACT, DL_CURRENT, DL_STEPS, DL_EPISODES, DL_DIVERGED, DL_COUNT = range(9)
+
+_capsule_ptr = C.pythonapi.PyCapsule_GetPointer
+_capsule_ptr.restype = C.c_void_p
+_capsule_ptr.argtypes = [C.py_object, C.c_char_p]
+
+
+class DLArg:
+    """A torch tensor exported through DLPack (``torch.utils.dlpack.to_dlpack``),
+    borrowed by one C call: ``.ptr`` is the capsule's ``DLManagedTensor*`` (its
+    first member is the ``DLTensor``); the capsule, kept alive here, frees it."""
+
+    __slots__ = ("capsule", "ptr")
+
+    def __init__(self, tensor):
+        from torch.utils.dlpack import to_dlpack
+
+        self.capsule = to_dlpack(tensor)
+        self.ptr = _capsule_ptr(self.capsule, b"dltensor")
+
+
+def dl(tensor):
+    """DLArg of a tensor, or None for None."""
+    return None if tensor is None else DLArg(tensor)
+
+
+def dl_ptr(arg):
+    return None if arg is None else arg.ptr
+
+
 EXPORTS = {
     "uuv_last_error": (C.c_char_p, []),
     "uuv_abi_version": (C.c_int32, []),
@@ -149,11 +200,19 @@ EXPORTS = {
                            C.c_double, C.c_void_p]),
     "uuv_server_start": (C.c_int, [C.c_void_p, C.POINTER(State), C.c_int32, C.c_double,
                                    C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]),
-    "uuv_server_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "uuv_server_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(HostOut)]),
     "uuv_server_stop": (C.c_int, [C.c_void_p]),
     "uuv_server_stamps": (None, [C.c_void_p, C.POINTER(C.c_uint64)]),
     "uuv_step_host": (C.c_int, [C.c_void_p, C.POINTER(State), C.c_void_p, C.c_int64, C.c_void_p,
-                                C.c_void_p, C.c_int32, C.c_double, C.c_void_p, C.c_int32]),
+                                C.POINTER(HostOut), C.c_int32, C.c_double, C.c_void_p, C.c_int32]),
+    "uuv_state_from_dlpack": (C.c_int, [C.POINTER(State), C.POINTER(C.c_void_p), C.c_int32]),
+    "uuv_step_dl": (C.c_int, [C.c_void_p, C.POINTER(State), C.c_void_p, C.c_int32, C.c_double,
+                              C.c_void_p]),
+    "uuv_reset_dl": (C.c_int, [C.c_void_p, C.POINTER(State), C.c_void_p, C.POINTER(Sampler),
+                               C.c_uint64, C.c_void_p]),
+    "uuv_task_step_dl": (C.c_int, [C.c_void_p, C.POINTER(State), C.POINTER(Task),
+                                   C.POINTER(Sampler), C.c_uint64, C.c_void_p, C.c_int32,
+                                   C.c_double, C.POINTER(TaskIO), C.c_void_p, C.c_void_p]),
     "uuv_reset": (C.c_int, [C.c_void_p, C.POINTER(State), C.c_void_p, C.POINTER(Sampler),
                             C.c_uint64, C.c_void_p]),
     "uuv_task_step": (C.c_int, [C.c_void_p, C.POINTER(State), C.POINTER(Task), C.POINTER(Sampler),

@@ -23,7 +23,6 @@
 #include <vector>
 
 #include "uuv_task.cuh"
-#include "uuv_bulk.cuh"
 
 using namespace uuv;
 
@@ -238,6 +237,17 @@ struct uuv_ctx {
 
 // ================================================================== kernels
 
+// Device addresses of the caller's pinned result rows (uuv_host_out): the step
+// kernel stores them over the host link next to its HBM stores.
+struct HostOut {
+  void* pose;          // (13, n) Real: p, q, nu; or null
+  void* act;           // (n_act, n) Real; or null
+  int32_t* steps;      // (n); or null
+  uint8_t* div;        // (n); or null
+  int32_t n_act;
+  int32_t any;         // 0: no host rows at all
+};
+
 template <typename R, int NT> struct StepArgs {
   Hull<R> hull[NT];
   int8_t cls[NT];  // mixed fleets: per-type specialisation (see hull_class)
@@ -247,7 +257,7 @@ template <typename R, int NT> struct StepArgs {
   int32_t K;
   R dt;
   int32_t early_trigger;  // single-wave grid: let the next step's CTAs launch now
-  R* pose_out;            // optional (13, n) row-major p, q, nu copy (host-mapped memory)
+  HostOut out;            // optional host-mapped result rows (uuv_step_host)
   int32_t prefetch_ov;    // DR record beyond L2: prefetch it ahead of the dependent-launch wait
 };
 
@@ -380,153 +390,6 @@ UUV_D bool physics(const Hull<R>& H, const StateView<R>& sv, int64_t i, int K, R
                                    q, nu, act);
 }
 
-// ------------------------------------------------------------------ persistent TMA step
-// Per-warp software pipeline: every warp owns 32-env tiles (stride = all warps of
-// the grid) and a double buffer in shared memory.  For each tile, lane r issues
-// the bulk copy (TMA engine, cp.async.bulk) of the tile's slice of SoA row r
-// into the free buffer — state, steps, diverged, type id, DR record, commands —
-// with completion counted in bytes on the warp's mbarrier, while the warp
-// computes the previous tile from the other buffer; results are written back in
-// place and bulk-copied to global memory by the same lanes.  Threads touch only
-// their own shared-memory column (immediate-offset LDS/STS, no per-access
-// address arithmetic) and only __syncwarp is needed, so warps pipeline
-// independently and each keeps its next slab in flight while computing.
-constexpr int kTile = 32;
-constexpr int kWarps = kBlock / 32;
-constexpr int kMaxRows = 64;
-struct RowDesc {
-  const char* g;  // global address of env 0 of this row
-  uint32_t elem;  // bytes per env
-  uint32_t soff;  // byte offset inside a warp buffer
-};
-
-template <typename R, int NT> struct TmaArgs {
-  Hull<R> hull[NT];
-  StateView<R> sv;
-  const R* cmd;
-  int64_t cmd_ld;
-  int32_t K;
-  R dt;
-  int32_t early_trigger;
-  int32_t n_load, n_store;
-  int32_t cmd_row;        // index of the command slab in load[], -1 if loaded per lane
-  uint32_t buf_bytes;
-  uint32_t off_cur, off_steps, off_div, off_type, off_ov, off_cmd;  // 0xffffffff: absent
-  int64_t n_tiles;
-  RowDesc load[kMaxRows];
-  RowDesc store[kMaxRows];
-};
-
-UUV_D uint32_t round16(uint32_t b) { return (b + 15u) & ~15u; }
-
-template <typename R, int NT, bool DR, int AC, bool DM>
-__global__ void __launch_bounds__(kBlock, MinB<R>::value)
-    k_step_tma(const __grid_constant__ TmaArgs<R, NT> a) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + 2 * warp;
-  unsigned char* bufs = smem + 128 + (size_t)warp * 2 * a.buf_bytes;
-  const StateView<R>& sv = a.sv;
-  if (a.early_trigger) pdl_trigger();
-  if (lane == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    fence_mbar_init();
-  }
-  __syncwarp();
-  pdl_wait();  // the previous step's writes are visible from here on
-
-  auto issue_load = [&](int64_t tile, int b) {
-    const int64_t row0 = tile * kTile;
-    const int rows = (int)min((int64_t)kTile, sv.n - row0);
-    const bool tail = rows < kTile;
-    unsigned char* buf = bufs + (size_t)b * a.buf_bytes;
-    uint32_t total = 0;
-    for (int r = 0; r < a.n_load; ++r)
-      if (!(r == a.cmd_row && tail)) total += round16((uint32_t)rows * a.load[r].elem);
-    if (lane == 0) mbar_arrive_expect_tx(&bars[b], total);
-    __syncwarp();
-    for (int r = lane; r < a.n_load; r += 32) {
-      if (r == a.cmd_row && tail) continue;
-      const RowDesc& d = a.load[r];
-      bulk_g2s(buf + d.soff, d.g + row0 * d.elem, round16((uint32_t)rows * d.elem), &bars[b]);
-    }
-  };
-
-  const int64_t stride = (int64_t)gridDim.x * kWarps;
-  int64_t tile = (int64_t)blockIdx.x * kWarps + warp;
-  if (tile < a.n_tiles) issue_load(tile, 0);
-  for (int k = 0; tile < a.n_tiles; ++k, tile += stride) {
-    const int b = k & 1;
-    const int64_t next = tile + stride;
-    if (next < a.n_tiles) {
-      bulk_wait_read_all();  // the other buffer's stores have finished reading it
-      __syncwarp();
-      issue_load(next, 1 - b);
-    }
-    mbar_wait(&bars[b], (uint32_t)((k >> 1) & 1));
-    unsigned char* buf = bufs + (size_t)b * a.buf_bytes;
-    const int64_t row0 = tile * kTile;
-    const int rows = (int)min((int64_t)kTile, sv.n - row0);
-    const unsigned t = lane;
-    if ((int)t < rows) {
-      const int64_t i = row0 + t;
-      R* S = reinterpret_cast<R*>(buf);  // state rows p q nu act, kTile each
-      int32_t* steps = reinterpret_cast<int32_t*>(buf + a.off_steps);
-      uint8_t* div = buf + a.off_div;
-      const int ty = NT > 1 ? (int)buf[a.off_type + t] : 0;
-      const Hull<R>& H = a.hull[ty];
-      const int A = AC > 0 ? AC : H.r.n_act;
-      constexpr int NA = AC > 0 ? AC : UUV_MAX_ACT;
-      if (!div[t]) {
-        R u[UUV_MAX_ACT];
-        const R* c = (a.cmd_row >= 0 && rows == kTile)
-                         ? reinterpret_cast<const R*>(buf + a.off_cmd) + t * a.cmd_ld
-                         : a.cmd + i * a.cmd_ld;
-#pragma unroll
-        for (int j = 0; j < UUV_MAX_ACT; ++j)
-          u[j] = (j < NA && j < A) ? clip_<R>(c[j], R(-1), R(1)) : R(0);
-        R px = S[t], py = S[kTile + t], pz = S[2 * kTile + t];
-        Q4<R> q{S[3 * kTile + t], S[4 * kTile + t], S[5 * kTile + t], S[6 * kTile + t]};
-        R nu[6], act[UUV_MAX_ACT];
-#pragma unroll
-        for (int k2 = 0; k2 < 6; ++k2) nu[k2] = S[(7 + k2) * kTile + t];
-#pragma unroll
-        for (int j = 0; j < UUV_MAX_ACT; ++j)
-          act[j] = (j < NA && j < A) ? S[(13 + j) * kTile + t] : R(0);
-        const bool has_cur = a.off_cur != 0xffffffffu;
-        V3<R> cur{R(0), R(0), R(0)};
-        if (has_cur) {
-          const R* Cc = reinterpret_cast<const R*>(buf + a.off_cur);
-          cur = V3<R>{Cc[t], Cc[kTile + t], Cc[2 * kTile + t]};
-        }
-        const double* ovs = DR ? reinterpret_cast<const double*>(buf + a.off_ov) : nullptr;
-        const bool d2 = physics_at<R, DR, AC, DM>(H, sv, i, ovs, kTile, t, has_cur, cur, a.K,
-                                                  a.dt, u, px, py, pz, q, nu, act);
-        S[t] = px; S[kTile + t] = py; S[2 * kTile + t] = pz;
-        S[3 * kTile + t] = q.w; S[4 * kTile + t] = q.x;
-        S[5 * kTile + t] = q.y; S[6 * kTile + t] = q.z;
-#pragma unroll
-        for (int k2 = 0; k2 < 6; ++k2) S[(7 + k2) * kTile + t] = nu[k2];
-#pragma unroll
-        for (int j = 0; j < NA; ++j)
-          if (j < A) S[(13 + j) * kTile + t] = act[j];
-        div[t] = d2 ? 1 : 0;
-      }
-      steps[t] += 1;
-    }
-    fence_proxy_async_smem();
-    __syncwarp();
-    for (int r = lane; r < a.n_store; r += 32) {
-      const RowDesc& d = a.store[r];
-      bulk_s2g(const_cast<char*>(d.g) + row0 * d.elem, buf + d.soff,
-               round16((uint32_t)rows * d.elem));
-    }
-    bulk_commit();
-  }
-  bulk_wait_all();
-}
-
 // Inputs of one env's step, loaded ahead of use so that a persistent thread can
 // have env k+1's loads in flight while it computes env k.
 template <typename R> struct StepIn {
@@ -552,12 +415,37 @@ UUV_D void load_in(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in) {
   load_state(sv, i, A, in.px, in.py, in.pz, in.q, in.nu, in.act);
 }
 
+// The step's result rows of env i into the caller's host buffers (every field
+// step_batch mutates in place, engine.py:418, 444-449).  Called on every exit of
+// step_env / serve_env, frozen rows included.
+template <typename R>
+UUV_D void put_host_out(const HostOut& o, int64_t i, int64_t n, const StepIn<R>& in,
+                        int32_t steps, uint8_t div) {
+  if (!o.any) return;
+  if (o.pose != nullptr) {
+    R* p = (R*)o.pose + i;
+    p[0] = in.px; p[n] = in.py; p[2 * n] = in.pz;
+    p[3 * n] = in.q.w; p[4 * n] = in.q.x; p[5 * n] = in.q.y; p[6 * n] = in.q.z;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) p[(7 + k) * n] = in.nu[k];
+  }
+  if (o.act != nullptr) {
+    R* p = (R*)o.act + i;
+#pragma unroll
+    for (int j = 0; j < UUV_MAX_ACT; ++j)
+      if (j < o.n_act) p[j * n] = in.act[j];
+  }
+  if (o.steps != nullptr) o.steps[i] = steps;
+  if (o.div != nullptr) o.div[i] = div;
+}
+
 template <typename R, int NT, bool DR, int AC, bool DM, bool BRANCHLESS = false>
 UUV_D void step_env(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in) {
   const StateView<R>& sv = a.sv;
   if (!BRANCHLESS) {
     if (in.div) {  // frozen rows stay frozen (engine.py:411, 441-449)
       sv.steps[i] = in.steps + 1;
+      put_host_out(a.out, i, sv.n, in, in.steps + 1, 1);
       return;
     }
     const Hull<R>& H = a.hull[in.ty];
@@ -567,6 +455,7 @@ UUV_D void step_env(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in) {
     store_state(sv, i, A, in.px, in.py, in.pz, in.q, in.nu, in.act);
     sv.diverged[i] = div ? 1 : 0;
     sv.steps[i] = in.steps + 1;
+    put_host_out(a.out, i, sv.n, in, in.steps + 1, div ? 1 : 0);
     return;
   }
   // BRANCHLESS (small-batch DR build): the physics runs for every row and frozen
@@ -582,18 +471,11 @@ UUV_D void step_env(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in) {
   if (!in.div) {
     store_state(sv, i, A, in.px, in.py, in.pz, in.q, in.nu, in.act);
     sv.diverged[i] = div ? 1 : 0;
-  } else {  // frozen: its stored state is untouched; re-read it for the pose rows
+  } else if (a.out.any) {  // frozen: its stored state is untouched; re-read it for the host rows
     load_state(sv, i, A, in.px, in.py, in.pz, in.q, in.nu, in.act);
   }
   sv.steps[i] = in.steps + 1;
-  if (a.pose_out != nullptr) {  // the caller's pinned (13, n) rows, stored over the link
-    R* o = a.pose_out + i;
-    const int64_t n = sv.n;
-    o[0] = in.px; o[n] = in.py; o[2 * n] = in.pz;
-    o[3 * n] = in.q.w; o[4 * n] = in.q.x; o[5 * n] = in.q.y; o[6 * n] = in.q.z;
-#pragma unroll
-    for (int k = 0; k < 6; ++k) o[(7 + k) * n] = in.nu[k];
-  }
+  put_host_out(a.out, i, sv.n, in, in.steps + 1, (in.div || div) ? 1 : 0);
 }
 
 // Mixed fleets: every env takes its vehicle type's specialised path (types are
@@ -704,16 +586,21 @@ struct alignas(16) ServeCtl {  // host-mapped, written by the host
   uint64_t seq;             // doorbell: step number (| kServeNewPose), or kServeQuit
   uint64_t cmd;             // device-visible address of the (n, cmd_ld) commands
   uint64_t pose;            // device-visible address of the (13, n) pose rows, or 0
-  int64_t cmd_ld;           // {pose, cmd_ld}: re-read only when kServeNewPose is set
+  int64_t cmd_ld;           // {pose, cmd_ld, act, steps, div}: re-read only when
+  uint64_t act;             //   kServeNewPose is set; act (n_act, n) rows, steps (n),
+  uint64_t steps;           //   diverged (n) -- the rest of the step's result
+  uint64_t div;
+  uint64_t pad_;
   uint64_t stamp[8];        // phase times of the last step (ns; see uuv_server_stamps)
 };
 constexpr uint64_t kServeQuit = ~0ull;
-constexpr uint64_t kServeNewPose = 1ull << 62;  // pose / cmd_ld changed this step
+constexpr uint64_t kServeNewPose = 1ull << 62;  // result addresses / cmd_ld changed this step
 
 struct ServeSync {          // device memory: CTA 0 republishes the doorbell here
   uint64_t go;
   uint64_t cmd, pose;
   int64_t cmd_ld;
+  uint64_t act, steps, div;
   uint32_t arrived;         // CTAs done with the current step
 };
 
@@ -725,6 +612,7 @@ template <typename R, int NT> struct ServeArgs {
   uint64_t idle_ns;
   uint32_t sleep_ns;        // back-off between doorbell polls
   uint32_t stamps;          // write phase stamps (UUV_SERVE_STAMPS=1; profiling aid)
+  int32_t n_act;            // act result rows
 };
 
 UUV_D uint64_t ld_acquire_sys(const uint64_t* p) {
@@ -758,7 +646,7 @@ UUV_D uint64_t global_ns() {
 }
 
 template <typename R, int NT, bool DR, int AC, bool DM>
-UUV_D void serve_env(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in, R* pose) {
+UUV_D void serve_env(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in, const HostOut& out) {
   const StateView<R>& sv = a.sv;
   in.steps += 1;
   if (!in.div) {
@@ -771,20 +659,14 @@ UUV_D void serve_env(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in, R* pose
     sv.diverged[i] = in.div;
   }
   sv.steps[i] = in.steps;
-  if (pose != nullptr) {
-    R* o = pose + i;
-    const int64_t n = sv.n;
-    o[0] = in.px; o[n] = in.py; o[2 * n] = in.pz;
-    o[3 * n] = in.q.w; o[4 * n] = in.q.x; o[5 * n] = in.q.y; o[6 * n] = in.q.z;
-#pragma unroll
-    for (int k = 0; k < 6; ++k) o[(7 + k) * n] = in.nu[k];
-  }
+  put_host_out(out, i, sv.n, in, in.steps, in.div);
 }
 
 template <typename R, int NT, bool DR, int AC, bool DM>
 __global__ void __launch_bounds__(kBlock, (NT > 1 && sizeof(R) == 4) ? 3 : MinB<R>::value)
     k_serve(const __grid_constant__ ServeArgs<R, NT> sa) {
-  __shared__ uint64_t s_seq, s_cmd, s_pose;
+  __shared__ uint64_t s_seq, s_cmd;
+  __shared__ HostOut s_out;
   __shared__ int64_t s_ld;
   const StepArgs<R, NT>& a = sa.step;
   const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
@@ -799,7 +681,8 @@ __global__ void __launch_bounds__(kBlock, (NT > 1 && sizeof(R) == 4) ? 3 : MinB<
     load_state(sv, i, A, in.px, in.py, in.pz, in.q, in.nu, in.act);
   }
   uint64_t seq = 0;
-  uint64_t cur_pose = 0;  // CTA 0: pose rows address / command stride of the last step
+  // CTA 0: result-row addresses / command stride of the last step
+  uint64_t cur_pose = 0, cur_act = 0, cur_steps = 0, cur_div = 0;
   int64_t cur_ld = 0;
   ServeSync* sy = sa.sync;
   if (sa.stamps && blockIdx.x == 0 && threadIdx.x == 0) {  // start marker + idle budget
@@ -830,17 +713,28 @@ __global__ void __launch_bounds__(kBlock, (NT > 1 && sizeof(R) == 4) ? 3 : MinB<
         }
         s_cmd = cmd;
         if (v != kServeQuit && (word & kServeNewPose)) {
-          uint64_t pose, ld;
+          uint64_t pose, ld, act, stp, div, pad;
           ld_relaxed_sys_v2(&sa.ctl->pose, pose, ld);
+          ld_relaxed_sys_v2(&sa.ctl->act, act, stp);
+          ld_relaxed_sys_v2(&sa.ctl->div, div, pad);
           cur_pose = pose;
           cur_ld = (int64_t)ld;
+          cur_act = act;
+          cur_steps = stp;
+          cur_div = div;
         }
-        s_pose = cur_pose;
         s_ld = cur_ld;
         if (sa.stamps) sa.ctl->stamp[1] = global_ns();
         sy->cmd = s_cmd;
-        sy->pose = s_pose;
+        sy->pose = cur_pose;
         sy->cmd_ld = s_ld;
+        sy->act = cur_act;
+        sy->steps = cur_steps;
+        sy->div = cur_div;
+        s_out.pose = (void*)cur_pose;
+        s_out.act = (void*)cur_act;
+        s_out.steps = (int32_t*)cur_steps;
+        s_out.div = (uint8_t*)cur_div;
         st_release_gpu(&sy->go, v);
         // like every other CTA, acquire the republished word: a GPU-scope acquire
         // invalidates this SM's L1, so the command rows below are fetched fresh
@@ -849,9 +743,15 @@ __global__ void __launch_bounds__(kBlock, (NT > 1 && sizeof(R) == 4) ? 3 : MinB<
       } else {
         while ((v = ld_acquire_gpu(&sy->go)) == seq) __nanosleep(64);
         s_cmd = *(volatile uint64_t*)&sy->cmd;
-        s_pose = *(volatile uint64_t*)&sy->pose;
         s_ld = *(volatile int64_t*)&sy->cmd_ld;
+        s_out.pose = (void*)*(volatile uint64_t*)&sy->pose;
+        s_out.act = (void*)*(volatile uint64_t*)&sy->act;
+        s_out.steps = (int32_t*)*(volatile uint64_t*)&sy->steps;
+        s_out.div = (uint8_t*)*(volatile uint64_t*)&sy->div;
       }
+      s_out.n_act = sa.n_act;
+      s_out.any = s_out.pose != nullptr || s_out.act != nullptr || s_out.steps != nullptr ||
+                  s_out.div != nullptr;
       s_seq = v;
     }
     __syncthreads();
@@ -869,17 +769,17 @@ __global__ void __launch_bounds__(kBlock, (NT > 1 && sizeof(R) == 4) ? 3 : MinB<
       if (stamp) sa.ctl->stamp[2] = global_ns() + (uint64_t)(in.u[0] > R(2));
       if constexpr (NT > 1) {
         switch (a.cls[in.ty]) {
-          case 1: serve_env<R, NT, DR, 6, true>(a, i, in, (R*)s_pose); break;
-          case 2: serve_env<R, NT, DR, 8, true>(a, i, in, (R*)s_pose); break;
-          case 3: serve_env<R, NT, DR, 6, false>(a, i, in, (R*)s_pose); break;
-          case 4: serve_env<R, NT, DR, 8, false>(a, i, in, (R*)s_pose); break;
-          case 5: serve_env<R, NT, DR, 0, true>(a, i, in, (R*)s_pose); break;
-          case 6: serve_env<R, NT, DR, kFinLayout, true>(a, i, in, (R*)s_pose); break;
-          case 7: serve_env<R, NT, DR, kFinLayout, false>(a, i, in, (R*)s_pose); break;
-          default: serve_env<R, NT, DR, 0, false>(a, i, in, (R*)s_pose); break;
+          case 1: serve_env<R, NT, DR, 6, true>(a, i, in, s_out); break;
+          case 2: serve_env<R, NT, DR, 8, true>(a, i, in, s_out); break;
+          case 3: serve_env<R, NT, DR, 6, false>(a, i, in, s_out); break;
+          case 4: serve_env<R, NT, DR, 8, false>(a, i, in, s_out); break;
+          case 5: serve_env<R, NT, DR, 0, true>(a, i, in, s_out); break;
+          case 6: serve_env<R, NT, DR, kFinLayout, true>(a, i, in, s_out); break;
+          case 7: serve_env<R, NT, DR, kFinLayout, false>(a, i, in, s_out); break;
+          default: serve_env<R, NT, DR, 0, false>(a, i, in, s_out); break;
         }
       } else {
-        serve_env<R, NT, DR, AC, DM>(a, i, in, (R*)s_pose);
+        serve_env<R, NT, DR, AC, DM>(a, i, in, s_out);
       }
     }
     if (stamp) sa.ctl->stamp[3] = global_ns() + (uint64_t)(in.px > R(1e30));
@@ -1433,114 +1333,6 @@ void fill_hulls(const uuv_ctx* ctx, Hull<R>* dst, double dt_sub, int first = 0) 
   }
 }
 
-// Persistent TMA-staged step: host-side slab layout + launch.
-uint32_t align128(uint32_t x) { return (x + 127u) & ~127u; }
-
-template <typename R, int NT, bool DR, int AC, bool DM>
-uuv_status launch_step_tma(const uuv_ctx* ctx, const uuv_state* st, const void* cmd,
-                           int64_t cmd_ld, int32_t K, double dt, cudaStream_t s) {
-  static TmaArgs<R, NT> a;  // large; built on the host once per call (not thread-safe to share)
-  const double dt_sub = dt / K;
-  fill_hulls<R, NT>(ctx, a.hull, dt_sub);
-  a.sv = make_view<R>(*st);
-  a.cmd = (const R*)cmd;
-  a.cmd_ld = cmd_ld;
-  a.K = K;
-  a.dt = (R)dt_sub;
-  a.early_trigger = 1;
-  const uint32_t es = sizeof(R), rowb = kTile * es;
-  const int64_t ld = st->ld;
-  int nl = 0, ns = 0;
-  uint32_t off = 0;
-  auto row_ptr = [&](int k) -> const char* {
-    if (k < 3) return (const char*)st->p + (size_t)k * ld * es;
-    if (k < 7) return (const char*)st->q + (size_t)(k - 3) * ld * es;
-    if (k < 13) return (const char*)st->nu + (size_t)(k - 7) * ld * es;
-    return (const char*)st->act + (size_t)(k - 13) * ld * es;
-  };
-  for (int k = 0; k < 13 + st->a_max; ++k) {
-    a.load[nl++] = RowDesc{row_ptr(k), es, off};
-    a.store[ns++] = RowDesc{row_ptr(k), es, off};
-    off += rowb;
-  }
-  a.off_cur = 0xffffffffu;
-  if (st->current_ned != nullptr) {
-    a.off_cur = off;
-    for (int k = 0; k < 3; ++k) {
-      a.load[nl++] = RowDesc{(const char*)st->current_ned + (size_t)k * ld * es, es, off};
-      off += rowb;
-    }
-  }
-  off = align128(off);
-  a.off_steps = off;
-  a.load[nl++] = RowDesc{(const char*)st->steps, 4, off};
-  a.store[ns++] = RowDesc{(const char*)st->steps, 4, off};
-  off += kTile * 4;
-  a.off_div = off;
-  a.load[nl++] = RowDesc{(const char*)st->diverged, 1, off};
-  a.store[ns++] = RowDesc{(const char*)st->diverged, 1, off};
-  off += kTile;
-  a.off_type = 0xffffffffu;
-  if (NT > 1) {
-    a.off_type = off;
-    a.load[nl++] = RowDesc{(const char*)st->type_id, 1, off};
-    off += kTile;
-  }
-  off = align128(off);
-  a.off_ov = 0xffffffffu;
-  if (DR) {
-    a.off_ov = off;
-    const int n_stage = st->slot[UUV_OV_JITTER] >= 0 ? st->slot[UUV_OV_JITTER] : st->n_slots;
-    for (int k = 0; k < n_stage; ++k) {
-      a.load[nl++] = RowDesc{(const char*)st->overlay + (size_t)k * ld * 8, 8, off};
-      off += kTile * 8;
-    }
-  }
-  a.cmd_row = -1;
-  a.off_cmd = 0xffffffffu;
-  if (((uintptr_t)cmd & 15u) == 0) {
-    off = align128(off);
-    a.off_cmd = off;
-    a.cmd_row = nl;
-    a.load[nl++] = RowDesc{(const char*)cmd, (uint32_t)(cmd_ld * es), off};
-    off += (uint32_t)(kTile * cmd_ld * es);
-  }
-  a.buf_bytes = align128(off);
-  a.n_load = nl;
-  a.n_store = ns;
-  a.n_tiles = (st->n_envs + kTile - 1) / kTile;
-  const size_t smem = 128 + (size_t)kWarps * 2 * a.buf_bytes;
-  UUV_REGISTER(k_step_tma<R, NT, DR, AC, DM>);
-  auto kern = k_step_tma<R, NT, DR, AC, DM>;
-  static thread_local std::map<const void*, size_t> smem_set;
-  size_t& have = smem_set[(const void*)kern];
-  if (smem > have) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return fail(UUV_ERR_CUDA, "uuv_step smem: %s", cudaGetErrorString(e));
-    have = smem;
-  }
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem);
-  const int64_t grid = std::min<int64_t>((a.n_tiles + kWarps - 1) / kWarps,
-                                         (int64_t)sms * std::max(per_sm, 1));
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(kBlock);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
-  if (e != cudaSuccess) return fail(UUV_ERR_CUDA, "uuv_step: %s", cudaGetErrorString(e));
-  return check_launch("uuv_step");
-}
-
 #ifndef UUV_PERSISTENT_STEP
 #define UUV_PERSISTENT_STEP 0
 #endif
@@ -1553,20 +1345,10 @@ int64_t step_waves() {
   return w;
 }
 
-bool use_tma_step() {
-  static const bool on = [] {
-    const char* v = getenv("UUV_STEP_KERNEL");
-    return v && strcmp(v, "tma") == 0;
-  }();
-  return on;
-}
-
 template <typename R, int NT, bool DR, int AC, bool DM = false>
 uuv_status launch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd, int64_t cmd_ld,
-                       int32_t K, double dt, cudaStream_t s, void* pose_out = nullptr,
+                       int32_t K, double dt, cudaStream_t s, const HostOut* out = nullptr,
                        int hull0 = 0) {
-  if (pose_out == nullptr && hull0 == 0 && use_tma_step())
-    return launch_step_tma<R, NT, DR, AC, DM>(ctx, st, cmd, cmd_ld, K, dt, s);
   StepArgs<R, NT> a;
   const double dt_sub = dt / K;
   fill_hulls<R, NT>(ctx, a.hull, dt_sub, hull0);
@@ -1577,7 +1359,7 @@ uuv_status launch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd,
   a.cmd_ld = cmd_ld;
   a.K = K;
   a.dt = (R)dt_sub;
-  a.pose_out = (R*)pose_out;
+  a.out = out != nullptr ? *out : HostOut{};
   a.prefetch_ov = st->n_envs >= (int64_t)1 << 19;  // >~100 MB of state + record: past L2
   const int64_t need = grid_for(st->n_envs);
   constexpr bool kHiOk = DR && NT == 1 && sizeof(R) == 4;
@@ -1712,7 +1494,7 @@ uuv_status dispatch_runs(const uuv_ctx* ctx, const uuv_state* st, const void* cm
 
 template <typename R>
 uuv_status dispatch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd, int64_t cmd_ld,
-                         int32_t K, double dt, cudaStream_t s, void* pose = nullptr) {
+                         int32_t K, double dt, cudaStream_t s, const HostOut* pose = nullptr) {
   if (ctx->hulls.size() > 1 && st->n_runs > 0 && pose == nullptr && st->n_envs >= runs_min_envs())
     return dispatch_runs<R>(ctx, st, cmd, cmd_ld, K, dt, s);
   const bool dr = st->overlay != nullptr;
@@ -1853,20 +1635,20 @@ uuv_status check_task(const uuv_ctx* ctx, const uuv_state* st, const uuv_task* t
 namespace uuv_tu {
 template <typename R>
 uuv_status step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd, int64_t cmd_ld,
-                int32_t K, double dt, cudaStream_t s, void* pose);
+                int32_t K, double dt, cudaStream_t s, const HostOut* out);
 template <typename R, bool POL>
 void task(bool dr, int ac, bool dm, unsigned g, cudaStream_t cs, const TaskArgs<R>& a);
 
 #if UUV_TU_STEP
 template <typename R>
 uuv_status step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd, int64_t cmd_ld,
-                int32_t K, double dt, cudaStream_t s, void* pose) {
-  return dispatch_step<R>(ctx, st, cmd, cmd_ld, K, dt, s, pose);
+                int32_t K, double dt, cudaStream_t s, const HostOut* out) {
+  return dispatch_step<R>(ctx, st, cmd, cmd_ld, K, dt, s, out);
 }
 template uuv_status step<float>(const uuv_ctx*, const uuv_state*, const void*, int64_t, int32_t,
-                                double, cudaStream_t, void*);
+                                double, cudaStream_t, const HostOut*);
 template uuv_status step<double>(const uuv_ctx*, const uuv_state*, const void*, int64_t, int32_t,
-                                 double, cudaStream_t, void*);
+                                 double, cudaStream_t, const HostOut*);
 #endif
 template <typename R>
 uuv_status serve(const uuv_ctx* ctx, const uuv_state* st, int32_t K, double dt, cudaStream_t s,
@@ -1889,7 +1671,7 @@ uuv_status serve_kernel(const uuv_ctx* ctx, const uuv_state* st, int32_t K, doub
   a.K = K;
   a.dt = (R)(dt / K);
   a.early_trigger = 0;
-  a.pose_out = nullptr;
+  a.out = HostOut{};
   a.prefetch_ov = 0;
   sa.ctl = ctl;
   sa.done = done;
@@ -1905,6 +1687,7 @@ uuv_status serve_kernel(const uuv_ctx* ctx, const uuv_state* st, int32_t K, doub
     return v ? (uint32_t)atoi(v) : 0u;
   }();
   sa.stamps = stamps;
+  sa.n_act = ctx->hulls.size() > 1 || st->type_id != nullptr ? st->a_max : ctx->hulls[0].n_act;
 
   const int64_t grid = grid_for(st->n_envs);
   if (grid > one_wave_ctas(k_serve<R, NT, DR, AC, DM>))
@@ -2086,7 +1869,7 @@ static uuv_status task_reset_impl(uuv_ctx* ctx, const uuv_state* st, const uuv_t
 
 static uuv_status step_checked(uuv_ctx* ctx, const uuv_state* st, const void* commands,
                                int64_t cmd_ld, int32_t substeps, double dt, cudaStream_t cs,
-                               void* pose) {
+                               const HostOut* out) {
   uuv_status s = check_state(ctx, st);
   if (s != UUV_OK) return s;
   if (commands == nullptr) return fail(UUV_ERR_ARG, "commands: null");
@@ -2099,8 +1882,8 @@ static uuv_status step_checked(uuv_ctx* ctx, const uuv_state* st, const void* co
   if (!(dt > 0)) return fail(UUV_ERR_ARG, "dt must be > 0");
   if (st->n_envs == 0) return UUV_OK;
   return st->dtype == UUV_F32
-             ? uuv_tu::step<float>(ctx, st, commands, cmd_ld, substeps, dt, cs, pose)
-             : uuv_tu::step<double>(ctx, st, commands, cmd_ld, substeps, dt, cs, pose);
+             ? uuv_tu::step<float>(ctx, st, commands, cmd_ld, substeps, dt, cs, out)
+             : uuv_tu::step<double>(ctx, st, commands, cmd_ld, substeps, dt, cs, out);
 }
 
 // uuv_step_host transfer mode: 1 = mapped pinned memory (default), 0 = copy engines
@@ -2114,21 +1897,36 @@ static int host_step_mode() {
 }
 
 // Device address of a pinned, mapped host buffer (the host address under UVA), or
-// nullptr for pageable memory.  A few recent answers are cached per thread.
+// nullptr for pageable memory.  Looked up on every call: a cached answer could
+// outlive the allocation (a freed pinned buffer whose address is reused by
+// pageable memory would then be written through a stale mapping).
 static void* host_mapped(const void* h) {
-  struct Entry { const void* h; void* d; };
-  thread_local Entry cache[8] = {};
-  thread_local int next = 0;
-  for (const Entry& c : cache)
-    if (c.h == h && h != nullptr) return c.d;
+  if (h == nullptr) return nullptr;
   cudaPointerAttributes at;
   void* d = nullptr;
   if (cudaPointerGetAttributes(&at, h) == cudaSuccess && at.type == cudaMemoryTypeHost)
     d = at.devicePointer;
   cudaGetLastError();
-  cache[next] = {h, d};
-  next = (next + 1) & 7;
   return d;
+}
+
+// Width of the act result rows: the command width (a_max for mixed fleets).
+static int32_t out_act_rows(const uuv_ctx* ctx, const uuv_state* st) {
+  return ctx->hulls.size() > 1 || st->type_id != nullptr ? st->a_max : ctx->hulls[0].n_act;
+}
+
+// Maps every non-null field of a uuv_host_out; false if one is not mapped pinned memory.
+static bool map_host_out(const uuv_host_out* o, int32_t n_act, HostOut& m) {
+  m = HostOut{};
+  if (o == nullptr) return true;
+  m.pose = host_mapped(o->pose);
+  m.act = host_mapped(o->act);
+  m.steps = (int32_t*)host_mapped(o->steps);
+  m.div = (uint8_t*)host_mapped(o->diverged);
+  m.n_act = n_act;
+  m.any = o->pose != nullptr || o->act != nullptr || o->steps != nullptr || o->diverged != nullptr;
+  return (o->pose == nullptr || m.pose) && (o->act == nullptr || m.act) &&
+         (o->steps == nullptr || m.steps) && (o->diverged == nullptr || m.div);
 }
 
 struct uuv_server {
@@ -2144,7 +1942,7 @@ struct uuv_server {
   cudaEvent_t ev = nullptr;
   int32_t n_act = 0, dtype = 0;
   int64_t n = 0;
-  uint64_t last_pose = 0;
+  uint64_t last_out[4] = {0, 0, 0, 0};  // result-row addresses of the last step
   int64_t last_ld = 0;
 };
 
@@ -2228,7 +2026,7 @@ uuv_status uuv_step(uuv_ctx* ctx, const uuv_state* st, const void* commands, int
 }
 
 uuv_status uuv_step_host(uuv_ctx* ctx, const uuv_state* st, const void* host_cmd, int64_t cmd_ld,
-                         void* dev_cmd, void* host_pose, int32_t substeps, double dt,
+                         void* dev_cmd, const uuv_host_out* out, int32_t substeps, double dt,
                          void* stream, int32_t sync) {
   uuv_status s = check_state(ctx, st);
   if (s != UUV_OK) return s;
@@ -2236,38 +2034,45 @@ uuv_status uuv_step_host(uuv_ctx* ctx, const uuv_state* st, const void* host_cmd
   if (st->n_envs == 0) return UUV_OK;
   cudaStream_t cs = (cudaStream_t)stream;
   const size_t es = st->dtype == UUV_F32 ? sizeof(float) : sizeof(double);
-  cudaError_t e;
+  const int32_t n_act = out_act_rows(ctx, st);
+  cudaError_t e = cudaSuccess;
   // Mapped pinned buffers: the step kernel reads the command rows and stores the
-  // pose rows over the host link itself -- no copy-engine round trips.
+  // result rows over the host link itself -- no copy-engine round trips.
   const void* mcmd = host_mapped(host_cmd);
-  void* mpose = host_pose != nullptr ? host_mapped(host_pose) : nullptr;
-  if (host_step_mode() == 1 && mcmd != nullptr && (host_pose == nullptr || mpose != nullptr)) {
-    if ((s = step_checked(ctx, st, mcmd, cmd_ld, substeps, dt, cs, mpose)) != UUV_OK) return s;
+  HostOut mo;
+  const bool out_mapped = map_host_out(out, n_act, mo);
+  if (host_step_mode() == 1 && mcmd != nullptr && out_mapped) {
+    if ((s = step_checked(ctx, st, mcmd, cmd_ld, substeps, dt, cs, mo.any ? &mo : nullptr)) !=
+        UUV_OK)
+      return s;
   } else {
     e = cudaMemcpyAsync(dev_cmd, host_cmd, (size_t)st->n_envs * cmd_ld * es,
                         cudaMemcpyHostToDevice, cs);
     if (e != cudaSuccess) return fail(UUV_ERR_CUDA, "commands H2D: %s", cudaGetErrorString(e));
     if ((s = step_checked(ctx, st, dev_cmd, cmd_ld, substeps, dt, cs, nullptr)) != UUV_OK)
       return s;
-    if (host_pose != nullptr) {
-      const size_t row = (size_t)st->n_envs * es, pitch = (size_t)st->ld * es;
+    const int64_t n = st->n_envs;
+    const size_t row = (size_t)n * es, pitch = (size_t)st->ld * es;
+    if (out != nullptr && out->pose != nullptr) {
+      char* hp = (char*)out->pose;
       const char* p = (const char*)st->p;
-      if ((const char*)st->q == p + 3 * pitch && (const char*)st->nu == p + 7 * pitch &&
-          row == pitch) {  // n == ld: the 13 pose rows are one contiguous span
-        e = cudaMemcpyAsync(host_pose, p, 13 * row, cudaMemcpyDeviceToHost, cs);
-      } else if ((const char*)st->q == p + 3 * pitch && (const char*)st->nu == p + 7 * pitch) {
-        e = cudaMemcpy2DAsync(host_pose, row, p, pitch, row, 13, cudaMemcpyDeviceToHost, cs);
+      if ((const char*)st->q == p + 3 * pitch && (const char*)st->nu == p + 7 * pitch) {
+        e = cudaMemcpy2DAsync(hp, row, p, pitch, row, 13, cudaMemcpyDeviceToHost, cs);
       } else {
-        e = cudaMemcpy2DAsync(host_pose, row, st->p, pitch, row, 3, cudaMemcpyDeviceToHost, cs);
+        e = cudaMemcpy2DAsync(hp, row, st->p, pitch, row, 3, cudaMemcpyDeviceToHost, cs);
         if (e == cudaSuccess)
-          e = cudaMemcpy2DAsync((char*)host_pose + 3 * row, row, st->q, pitch, row, 4,
-                                cudaMemcpyDeviceToHost, cs);
+          e = cudaMemcpy2DAsync(hp + 3 * row, row, st->q, pitch, row, 4, cudaMemcpyDeviceToHost, cs);
         if (e == cudaSuccess)
-          e = cudaMemcpy2DAsync((char*)host_pose + 7 * row, row, st->nu, pitch, row, 6,
-                                cudaMemcpyDeviceToHost, cs);
+          e = cudaMemcpy2DAsync(hp + 7 * row, row, st->nu, pitch, row, 6, cudaMemcpyDeviceToHost, cs);
       }
-      if (e != cudaSuccess) return fail(UUV_ERR_CUDA, "pose D2H: %s", cudaGetErrorString(e));
     }
+    if (e == cudaSuccess && out != nullptr && out->act != nullptr)
+      e = cudaMemcpy2DAsync(out->act, row, st->act, pitch, row, n_act, cudaMemcpyDeviceToHost, cs);
+    if (e == cudaSuccess && out != nullptr && out->steps != nullptr)
+      e = cudaMemcpyAsync(out->steps, st->steps, n * sizeof(int32_t), cudaMemcpyDeviceToHost, cs);
+    if (e == cudaSuccess && out != nullptr && out->diverged != nullptr)
+      e = cudaMemcpyAsync(out->diverged, st->diverged, n, cudaMemcpyDeviceToHost, cs);
+    if (e != cudaSuccess) return fail(UUV_ERR_CUDA, "result D2H: %s", cudaGetErrorString(e));
   }
   if (sync) {
     e = cudaStreamSynchronize(cs);
@@ -2303,7 +2108,7 @@ uuv_status uuv_server_start(uuv_ctx* ctx, const uuv_state* st, int32_t substeps,
   }
   memset(srv->ctl, 0, sizeof(ServeCtl));
   *srv->done = 0;
-  srv->n_act = ctx->hulls.size() > 1 ? st->a_max : ctx->hulls[0].n_act;
+  srv->n_act = out_act_rows(ctx, st);
   srv->dtype = st->dtype;
   srv->n = st->n_envs;
   const uint64_t idle_ns = (uint64_t)idle_timeout_ms * 1000000ull;
@@ -2321,20 +2126,28 @@ uuv_status uuv_server_start(uuv_ctx* ctx, const uuv_state* st, int32_t substeps,
 }
 
 uuv_status uuv_server_step(uuv_server* srv, const void* host_cmd, int64_t cmd_ld,
-                           void* host_pose) {
+                           const uuv_host_out* out) {
   if (srv == nullptr) return fail(UUV_ERR_ARG, "null server");
   if (cmd_ld < srv->n_act)
     return fail(UUV_ERR_SHAPE, "commands: row stride %lld < action_dim %d", (long long)cmd_ld,
                 srv->n_act);
   const void* dc = host_mapped(host_cmd);
-  void* dp = host_pose != nullptr ? host_mapped(host_pose) : nullptr;
-  if (dc == nullptr || (host_pose != nullptr && dp == nullptr))
-    return fail(UUV_ERR_ARG, "step server: commands / pose_out must be pinned host memory");
+  HostOut mo;
+  if (dc == nullptr || !map_host_out(out, srv->n_act, mo))
+    return fail(UUV_ERR_ARG, "step server: commands and result rows must be pinned host memory");
   uint64_t flag = 0;
-  if (srv->seq == 0 || (uint64_t)dp != srv->last_pose || cmd_ld != srv->last_ld) {
-    srv->ctl->pose = (uint64_t)dp;
+  if (srv->seq == 0 || (uint64_t)mo.pose != srv->last_out[0] ||
+      (uint64_t)mo.act != srv->last_out[1] || (uint64_t)mo.steps != srv->last_out[2] ||
+      (uint64_t)mo.div != srv->last_out[3] || cmd_ld != srv->last_ld) {
+    srv->ctl->pose = (uint64_t)mo.pose;
     srv->ctl->cmd_ld = cmd_ld;
-    srv->last_pose = (uint64_t)dp;
+    srv->ctl->act = (uint64_t)mo.act;
+    srv->ctl->steps = (uint64_t)mo.steps;
+    srv->ctl->div = (uint64_t)mo.div;
+    srv->last_out[0] = (uint64_t)mo.pose;
+    srv->last_out[1] = (uint64_t)mo.act;
+    srv->last_out[2] = (uint64_t)mo.steps;
+    srv->last_out[3] = (uint64_t)mo.div;
     srv->last_ld = cmd_ld;
     flag = kServeNewPose;
   }
@@ -2524,6 +2337,180 @@ uuv_status uuv_substep_terms(uuv_ctx* ctx, const uuv_state* st, const void* comm
   cudaStream_t cs = (cudaStream_t)stream;
   return st->dtype == UUV_F32 ? terms_dispatch<float>(ctx, st, commands, cmd_ld, dt_sub, out, cs)
                               : terms_dispatch<double>(ctx, st, commands, cmd_ld, dt_sub, out, cs);
+}
+
+
+// ------------------------------------------------------------------ DLPack boundary
+static const char* const kDlName[UUV_DL_COUNT] = {"p", "q", "nu", "act", "current_ned",
+                                                  "steps", "episodes", "diverged"};
+
+static bool dl_is_real(const DLDataType& t, int32_t* dtype) {
+  if (t.code != kDLFloat || t.lanes != 1 || (t.bits != 32 && t.bits != 64)) return false;
+  *dtype = t.bits == 32 ? UUV_F32 : UUV_F64;
+  return true;
+}
+
+static uuv_status dl_device(const DLTensor* t, const char* what) {
+  if (t->device.device_type != kDLCUDA)
+    return fail(UUV_ERR_ARG, "%s: DLPack device type %d is not CUDA", what, (int)t->device.device_type);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (t->device.device_id != dev)
+    return fail(UUV_ERR_ARG, "%s: on CUDA device %d, the current device is %d", what,
+                (int)t->device.device_id, dev);
+  if (t->data == nullptr) return fail(UUV_ERR_ARG, "%s: null data", what);
+  return UUV_OK;
+}
+
+static int64_t dl_stride(const DLTensor* t, int d) {
+  if (t->strides != nullptr) return t->strides[d];
+  int64_t s = 1;
+  for (int k = t->ndim - 1; k > d; --k) s *= t->shape[k];
+  return s;
+}
+
+static void* dl_ptr(const DLTensor* t) { return (char*)t->data + t->byte_offset; }
+
+// A row-major (n, >= width) Real matrix with unit column stride; returns the row stride.
+static uuv_status dl_rows(const DLTensor* t, const char* what, int64_t n, int64_t width,
+                          int32_t dtype, int64_t* ld) {
+  if (t == nullptr) return fail(UUV_ERR_ARG, "%s: null tensor", what);
+  uuv_status s = dl_device(t, what);
+  if (s != UUV_OK) return s;
+  int32_t dt = -1;
+  if (!dl_is_real(t->dtype, &dt) || dt != dtype)
+    return fail(UUV_ERR_ARG, "%s: dtype (code %d, %d bits) is not the state's float%d", what,
+                (int)t->dtype.code, (int)t->dtype.bits, dtype == UUV_F32 ? 32 : 64);
+  if (t->ndim != 2 || t->shape[0] != n || t->shape[1] != width)
+    return fail(UUV_ERR_SHAPE, "%s: expected shape (%lld, %lld), got ndim %d (%lld, %lld)", what,
+                (long long)n, (long long)width, (int)t->ndim,
+                (long long)(t->ndim > 0 ? t->shape[0] : -1),
+                (long long)(t->ndim > 1 ? t->shape[1] : -1));
+  if (width > 1 && dl_stride(t, 1) != 1)
+    return fail(UUV_ERR_SHAPE, "%s: column stride %lld, expected 1", what,
+                (long long)dl_stride(t, 1));
+  *ld = n > 1 ? dl_stride(t, 0) : width;
+  if (*ld < width) return fail(UUV_ERR_SHAPE, "%s: row stride %lld < width %lld", what,
+                               (long long)*ld, (long long)width);
+  return UUV_OK;
+}
+
+// A (n,) vector with unit stride of one of the allowed element types.
+static uuv_status dl_vec(const DLTensor* t, const char* what, int64_t n, bool flag) {
+  uuv_status s = dl_device(t, what);
+  if (s != UUV_OK) return s;
+  const DLDataType& d = t->dtype;
+  const bool ok = flag ? ((d.code == kDLBool || d.code == kDLUInt) && d.bits == 8 && d.lanes == 1)
+                       : (d.code == kDLInt && d.bits == 32 && d.lanes == 1);
+  if (!ok)
+    return fail(UUV_ERR_ARG, "%s: dtype (code %d, %d bits), expected %s", what, (int)d.code,
+                (int)d.bits, flag ? "bool or uint8" : "int32");
+  if (t->ndim != 1 || t->shape[0] != n)
+    return fail(UUV_ERR_SHAPE, "%s: expected shape (%lld,)", what, (long long)n);
+  if (n > 1 && dl_stride(t, 0) != 1) return fail(UUV_ERR_SHAPE, "%s: stride must be 1", what);
+  return UUV_OK;
+}
+
+static int32_t cmd_width(const uuv_ctx* ctx, const uuv_state* st) {
+  return ctx->hulls.size() > 1 || st->type_id != nullptr ? st->a_max : ctx->hulls[0].n_act;
+}
+
+uuv_status uuv_state_from_dlpack(uuv_state* st, const DLTensor* const* f, int32_t n_fields) {
+  if (st == nullptr || f == nullptr) return fail(UUV_ERR_ARG, "null state or fields");
+  if (n_fields != UUV_DL_COUNT)
+    return fail(UUV_ERR_ARG, "expected %d DLPack fields, got %d", UUV_DL_COUNT, n_fields);
+  for (int k = 0; k < UUV_DL_COUNT; ++k)
+    if (f[k] == nullptr && k != UUV_DL_CURRENT) return fail(UUV_ERR_ARG, "%s: null tensor", kDlName[k]);
+  const DLTensor* p = f[UUV_DL_P];
+  if (p->ndim != 2) return fail(UUV_ERR_SHAPE, "p: expected 2 dims, got %d", (int)p->ndim);
+  const int64_t n = p->shape[0];
+  int32_t dtype = -1;
+  if (!dl_is_real(p->dtype, &dtype)) return fail(UUV_ERR_ARG, "p: dtype must be float32 or float64");
+  const DLTensor* act = f[UUV_DL_ACT];
+  if (act->ndim != 2 || act->shape[1] < 1 || act->shape[1] > UUV_MAX_ACT)
+    return fail(UUV_ERR_SHAPE, "act: expected (N, 1..%d)", UUV_MAX_ACT);
+  const int64_t widths[5] = {3, 4, 6, act->shape[1], 3};
+  int64_t ld = -1;
+  void* rows[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  for (int k = UUV_DL_P; k <= UUV_DL_CURRENT; ++k) {
+    const DLTensor* t = f[k];
+    if (t == nullptr) continue;
+    const char* what = kDlName[k];
+    uuv_status s = dl_device(t, what);
+    if (s != UUV_OK) return s;
+    int32_t dt = -1;
+    if (!dl_is_real(t->dtype, &dt) || dt != dtype)
+      return fail(UUV_ERR_ARG, "%s: dtype differs from p's float%d", what, dtype == UUV_F32 ? 32 : 64);
+    if (t->ndim != 2 || t->shape[0] != n || t->shape[1] != widths[k])
+      return fail(UUV_ERR_SHAPE, "%s: expected shape (%lld, %lld)", what, (long long)n,
+                  (long long)widths[k]);
+    // struct-of-arrays: element i of component c at base[c * ld + i]
+    const int64_t s0 = n > 1 ? dl_stride(t, 0) : 1, s1 = dl_stride(t, 1);
+    if (s0 != 1)
+      return fail(UUV_ERR_SHAPE, "%s: env stride %lld, the SoA layout needs 1 (a (C, ld) "
+                  "component-major buffer viewed as (N, C))", what, (long long)s0);
+    if (widths[k] > 1) {
+      if (ld < 0) ld = s1;
+      if (s1 != ld) return fail(UUV_ERR_SHAPE, "%s: component stride %lld != %lld of p", what,
+                                (long long)s1, (long long)ld);
+    }
+    rows[k] = dl_ptr(t);
+  }
+  if (ld < n) return fail(UUV_ERR_SHAPE, "state: component stride %lld < n_envs %lld",
+                          (long long)ld, (long long)n);
+  uuv_status s;
+  if ((s = dl_vec(f[UUV_DL_STEPS], "steps", n, false)) != UUV_OK) return s;
+  if ((s = dl_vec(f[UUV_DL_EPISODES], "episodes", n, false)) != UUV_OK) return s;
+  if ((s = dl_vec(f[UUV_DL_DIVERGED], "diverged", n, true)) != UUV_OK) return s;
+  st->dtype = dtype;
+  st->a_max = (int32_t)act->shape[1];
+  st->n_envs = n;
+  st->ld = ld;
+  st->p = rows[UUV_DL_P];
+  st->q = rows[UUV_DL_Q];
+  st->nu = rows[UUV_DL_NU];
+  st->act = rows[UUV_DL_ACT];
+  st->current_ned = rows[UUV_DL_CURRENT];
+  st->steps = (int32_t*)dl_ptr(f[UUV_DL_STEPS]);
+  st->episodes = (int32_t*)dl_ptr(f[UUV_DL_EPISODES]);
+  st->diverged = (uint8_t*)dl_ptr(f[UUV_DL_DIVERGED]);
+  return UUV_OK;
+}
+
+uuv_status uuv_step_dl(uuv_ctx* ctx, const uuv_state* st, const DLTensor* commands,
+                       int32_t substeps, double dt, void* stream) {
+  uuv_status s = check_state(ctx, st);
+  if (s != UUV_OK) return s;
+  int64_t ld = 0;
+  if ((s = dl_rows(commands, "commands", st->n_envs, cmd_width(ctx, st), st->dtype, &ld)) != UUV_OK)
+    return s;
+  return step_checked(ctx, st, dl_ptr(commands), ld, substeps, dt, (cudaStream_t)stream, nullptr);
+}
+
+uuv_status uuv_reset_dl(uuv_ctx* ctx, const uuv_state* st, const DLTensor* mask,
+                        const uuv_sampler* sampler, uint64_t seed, void* stream) {
+  uuv_status s = check_state(ctx, st);
+  if (s != UUV_OK) return s;
+  if (mask != nullptr && (s = dl_vec(mask, "mask", st->n_envs, true)) != UUV_OK) return s;
+  return uuv_reset(ctx, st, mask ? (const uint8_t*)dl_ptr(mask) : nullptr, sampler, seed, stream);
+}
+
+uuv_status uuv_task_step_dl(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task,
+                            const uuv_sampler* sampler, uint64_t seed, const DLTensor* commands,
+                            int32_t substeps, double dt, const uuv_task_io* io,
+                            const DLTensor* obs, void* stream) {
+  uuv_status s = check_state(ctx, st);
+  if (s != UUV_OK) return s;
+  if (task == nullptr || io == nullptr) return fail(UUV_ERR_ARG, "null task or io");
+  int64_t cld = 0, old = 0;
+  if ((s = dl_rows(commands, "commands", st->n_envs, ctx->hulls[0].n_act, st->dtype, &cld)) != UUV_OK)
+    return s;
+  if ((s = dl_rows(obs, "obs", st->n_envs, task->obs_dim, st->dtype, &old)) != UUV_OK) return s;
+  uuv_task_io io2 = *io;
+  io2.obs = dl_ptr(obs);
+  io2.obs_ld = old;
+  return uuv_task_step(ctx, st, task, sampler, seed, dl_ptr(commands), cld, substeps, dt, &io2,
+                       stream);
 }
 
 }  // extern "C"

@@ -13,10 +13,18 @@ multiple of 32), so every kernel load is a fully coalesced 128-byte line.
 ``steps`` / ``episodes`` are int32.  float32 is the default compute dtype;
 ``dtype=torch.float64`` selects the validation build (parity ~1e-12).
 
-Every step is ONE kernel launch (``uuv_step``) with K substeps fused in
-registers; no host synchronisation happens inside ``step_batch``.
-Per-(seed, env, episode) randomness is numpy-compatible Philox4x64-10:
-``Philox(key=[seed, env_offset + i], counter=[0, episode, 0, 0])``.
+Every step is ONE kernel launch (``uuv_step_dl``: the commands cross the C ABI
+as a DLPack tensor, the state fields were bound once through
+``uuv_state_from_dlpack``) with K substeps fused in registers; no host
+synchronisation happens inside ``step_batch``.
+
+Randomness (behaviour change vs the reference, opt-in to match it): per-(seed,
+env, episode) streams default to the north star's counter-based Philox4x64-10,
+``Philox(key=[seed, env_offset + i], counter=[0, episode, 0, 0])``; the
+unmodified reference draws from ``PCG64(SeedSequence(seed, spawn_key=(env,
+episode)))`` (engine.py:291-295).  Pass ``rng="pcg64"`` to ``make_batch`` /
+``make_env`` to reproduce the reference's episodes and DR draws bit for bit
+(both streams are restated on the device).
 """
 
 from __future__ import annotations
@@ -24,6 +32,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 import time
+import weakref
 from dataclasses import dataclass, field
 from typing import Callable
 
@@ -480,14 +489,15 @@ class BatchState:
 
     def _build_cstate(self) -> N.State:
         s = N.State()
-        s.dtype = N.F32 if self.dtype == torch.float32 else N.F64
-        s.a_max = self.a_max
-        s.n_envs, s.ld, s.env_offset = self.n_envs, self._ld, self.env_offset
-        s.p, s.q, s.nu, s.act = (self._p.data_ptr(), self._q.data_ptr(), self._nu.data_ptr(),
-                                 self._act.data_ptr())
-        s.current_ned = self._cur.data_ptr() if self._cur is not None else None
-        s.steps, s.episodes = self.steps.data_ptr(), self.episodes.data_ptr()
-        s.diverged = self.diverged.data_ptr()
+        # the reference's state fields cross the ABI as DLPack tensors; the C side
+        # validates dtype, device, shapes and the SoA strides and fills the pointers
+        n = self.n_envs
+        fields = [N.dl(self.p), N.dl(self.q), N.dl(self.nu), N.dl(self.act),
+                  N.dl(self._cur[:, :n].t()) if self._cur is not None else None,
+                  N.dl(self.steps), N.dl(self.episodes), N.dl(self.diverged)]
+        ptrs = (C.c_void_p * N.DL_COUNT)(*[N.dl_ptr(f) for f in fields])
+        N.check(N.load().uuv_state_from_dlpack(C.byref(s), ptrs, N.DL_COUNT), EngineError)
+        s.env_offset = self.env_offset
         s.type_id = self._type.data_ptr() if self._type is not None else None
         s.overlay = self._ov.data_ptr() if self._ov is not None else None
         s.overlay_keys = self._ov_keys.data_ptr() if self._ov_keys is not None else None
@@ -590,22 +600,96 @@ def _cmd_width(state: BatchState) -> int:
         state.vehicle.action_dim
 
 
-def step_batch(state: BatchState, commands, *, pose_out=None) -> BatchState:
+class HostStepOut:
+    """Pinned host buffers for one step's result (``uuv_host_out``): every field the
+    reference's ``step_batch`` mutates in place (engine.py:418, 444-449).
+
+    ``p`` (N,3), ``q`` (N,4), ``nu`` (N,6), ``act`` (N,A) are transposed views of
+    row-major ``pose`` (13, N) / ``act_rows`` (A, N) buffers in the batch dtype;
+    ``steps`` (N,) int32 and ``diverged`` (N,) bool.  ``fields`` selects what is
+    returned (others stay None and are not transferred).
+    """
+
+    FIELDS = ("pose", "act", "steps", "diverged")
+
+    def __init__(self, state: "BatchState", fields=FIELDS):
+        bad = set(fields) - set(self.FIELDS)
+        if bad:
+            raise EngineError(f"HostStepOut: unknown fields {sorted(bad)}")
+        n, w = state.n_envs, _cmd_width(state)
+
+        def pinned(shape, dt):
+            return torch.zeros(shape, dtype=dt).pin_memory()
+
+        self.pose = pinned((13, n), state.dtype) if "pose" in fields else None
+        self.act_rows = pinned((w, n), state.dtype) if "act" in fields else None
+        self.steps = pinned((n,), torch.int32) if "steps" in fields else None
+        self.diverged = pinned((n,), torch.bool) if "diverged" in fields else None
+        self._c = N.HostOut(*[t.data_ptr() if t is not None else None
+                              for t in (self.pose, self.act_rows, self.steps, self.diverged)])
+
+    @property
+    def p(self):
+        return self.pose[0:3].t()
+
+    @property
+    def q(self):
+        return self.pose[3:7].t()
+
+    @property
+    def nu(self):
+        return self.pose[7:13].t()
+
+    @property
+    def act(self):
+        return self.act_rows.t()
+
+    @property
+    def nbytes(self) -> int:
+        """Bytes one step moves device -> host into these buffers."""
+        return sum(t.numel() * t.element_size() for t in
+                   (self.pose, self.act_rows, self.steps, self.diverged) if t is not None)
+
+
+def _host_out(state: BatchState, pose_out, out):
+    """The uuv_host_out of a step call (None when nothing is returned)."""
+    if out is not None:
+        if pose_out is not None:
+            raise EngineError("pass either pose_out or out, not both")
+        if not isinstance(out, HostStepOut):
+            raise EngineError("out: expected an engine.HostStepOut")
+        if out.pose is not None and out.pose.shape[1] != state.n_envs:
+            raise EngineError(f"out: buffers for {out.pose.shape[1]} envs, batch has "
+                              f"{state.n_envs}")
+        return out._c
+    if pose_out is None:
+        return None
+    if not _pinned_ok(state, pose_out, (13, state.n_envs)):
+        raise EngineError(f"pose_out: expected a pinned contiguous (13, {state.n_envs}) "
+                          f"{state.dtype} tensor")
+    return N.HostOut(pose_out.data_ptr(), None, None, None)
+
+
+def step_batch(state: BatchState, commands, *, pose_out=None, out=None) -> BatchState:
     """Advance every environment one control step (engine.py:465-484).
 
     ``commands``: (N, A) CUDA tensor (one launch, no host sync), or host data — a CPU
     tensor or numpy array, staged through a pinned buffer and copied asynchronously.
-    ``pose_out``: optional pinned CPU tensor (13, N) in the batch dtype; receives the
-    rows p (3), q (4), nu (6) after the step and the call waits for them.
+    ``out``: a ``HostStepOut`` receiving the step's result in host memory (p, q, nu,
+    act, steps, diverged — what the reference's in-place step leaves in its numpy
+    state); the call waits for it.  ``pose_out``: shorthand for the pose rows only,
+    a pinned CPU tensor (13, N) in the batch dtype (rows p (3), q (4), nu (6)).
     """
     if state._server is not None:
-        return state._server.step(commands, pose_out)
+        return state._server.step(commands, pose_out, out)
     width = _cmd_width(state)
-    if pose_out is not None or not isinstance(commands, torch.Tensor) or not commands.is_cuda:
-        return _step_host(state, commands, width, pose_out)
+    if pose_out is not None or out is not None or not isinstance(commands, torch.Tensor) \
+            or not commands.is_cuda:
+        return _step_host(state, commands, width, _host_out(state, pose_out, out))
     cmd = _commands(state, commands, width)
-    status = N.load().uuv_step(state._ctx, C.byref(state._cstate()), cmd.data_ptr(),
-                               cmd.stride(0), state.sim.substeps, state.sim.dt, state._stream())
+    arg = N.DLArg(cmd)
+    status = N.load().uuv_step_dl(state._ctx, C.byref(state._cstate()), arg.ptr,
+                                  state.sim.substeps, state.sim.dt, state._stream())
     if status:
         N.check(status, EngineError)
     return state
@@ -648,7 +732,7 @@ class serve:
         st._server = self
         return self
 
-    def step(self, commands, pose_out=None):
+    def step(self, commands, pose_out=None, out=None):
         st = self.state
         n, width = st.n_envs, self._width
         if isinstance(commands, torch.Tensor) and commands.device.type == "cpu" and \
@@ -665,10 +749,9 @@ class serve:
                 st._pin = torch.empty((n, width), dtype=st.dtype).pin_memory()
             st._pin.numpy()[...] = arr
             src = st._pin
-        if pose_out is not None and not _pinned_ok(st, pose_out, (13, n)):
-            raise EngineError(f"pose_out: expected a pinned contiguous (13, {n}) {st.dtype} tensor")
+        ho = _host_out(st, pose_out, out)
         status = N.load().uuv_server_step(self._h, src.data_ptr(), width,
-                                          pose_out.data_ptr() if pose_out is not None else None)
+                                          C.byref(ho) if ho is not None else None)
         if status:
             N.check(status, EngineError)
         return st
@@ -683,19 +766,22 @@ class serve:
 
 
 def _pinned_ok(state: BatchState, t, shape) -> bool:
-    """Pinned, contiguous, batch dtype and shape (cached per buffer address)."""
-    key = (t.data_ptr(), tuple(t.shape), t.dtype)
-    ok = state._pinned_cache.get(key)
-    if ok is None:
-        ok = (tuple(t.shape) == shape and t.dtype == state.dtype and t.is_contiguous()
-              and t.is_pinned())
-        if len(state._pinned_cache) > 64:
-            state._pinned_cache.clear()
-        state._pinned_cache[key] = ok
+    """Pinned, contiguous, batch dtype and shape.  Cached per tensor object (a weak
+    reference plus its data address), so a freed buffer whose address is reused
+    is checked afresh."""
+    key = id(t)
+    hit = state._pinned_cache.get(key)
+    if hit is not None and hit[0]() is t and hit[1] == t.data_ptr():
+        return hit[2]
+    ok = (tuple(t.shape) == shape and t.dtype == state.dtype and t.is_contiguous()
+          and t.is_pinned())
+    if len(state._pinned_cache) > 64:
+        state._pinned_cache.clear()
+    state._pinned_cache[key] = (weakref.ref(t), t.data_ptr(), ok)
     return ok
 
 
-def _step_host(state: BatchState, commands, width, pose_out):
+def _step_host(state: BatchState, commands, width, ho):
     n = state.n_envs
     st = state
     if st._pin is None:
@@ -718,24 +804,38 @@ def _step_host(state: BatchState, commands, width, pose_out):
             raise EngineError(f"commands: expected shape {(n, width)}, got {arr.shape}")
         st._pin.numpy()[...] = arr
         src = st._pin
-    if pose_out is not None and not _pinned_ok(st, pose_out, (13, n)):
-        raise EngineError(f"pose_out: expected a pinned contiguous (13, {n}) {st.dtype} tensor")
     lib = N.load()
-    if src is None:  # device commands with a host pose_out
+    if src is None:  # device commands with host result rows
         cmd = _commands(state, commands, width)
-        N.check(lib.uuv_step(st._ctx, C.byref(st._cstate()), cmd.data_ptr(), cmd.stride(0),
-                             st.sim.substeps, st.sim.dt, st._stream()), EngineError)
+        N.check(lib.uuv_step_dl(st._ctx, C.byref(st._cstate()), N.DLArg(cmd).ptr,
+                                st.sim.substeps, st.sim.dt, st._stream()), EngineError)
         torch.cuda.current_stream(st.device).synchronize()
-        pose_out.copy_(st._soa[:13, :n])
+        _copy_result(st, ho)
         return state
     status = lib.uuv_step_host(st._ctx, C.byref(st._cstate()), src.data_ptr(), width,
-                               st._dcmd.data_ptr(),
-                               pose_out.data_ptr() if pose_out is not None else None,
+                               st._dcmd.data_ptr(), C.byref(ho) if ho is not None else None,
                                st.sim.substeps, st.sim.dt, st._stream(),
-                               1 if pose_out is not None or src is st._pin else 0)
+                               1 if ho is not None or src is st._pin else 0)
     if status:
         N.check(status, EngineError)
     return state
+
+
+def _copy_result(st: BatchState, ho):
+    """Synchronous copy of the state into the host result rows (device commands path)."""
+    if ho is None:
+        return
+    n, w = st.n_envs, _cmd_width(st)
+
+    def into(addr, src):
+        if addr:  # the caller's pinned buffer at `addr`, viewed as a tensor
+            buf = (C.c_char * (src.numel() * src.element_size())).from_address(addr)
+            torch.frombuffer(buf, dtype=src.dtype).view(src.shape).copy_(src)
+
+    into(ho.pose, st._soa[:13, :n].contiguous().cpu())
+    into(ho.act, st._act[:w, :n].contiguous().cpu())
+    into(ho.steps, st.steps.cpu())
+    into(ho.diverged, st.diverged.cpu())
 
 
 def _mask(state: BatchState, mask):
@@ -772,15 +872,14 @@ def reset_envs(state: BatchState, mask, sampler: InitSampler = default_sampler) 
 
 def _device_reset(state: BatchState, m, sampler: DeviceSampler):
     state._note_sampler(sampler)
-    rows_mask = m.to(torch.uint8)
     packed = sampler.pack()
     packed.rng_mode = N.RNG_MODES[state.rng]
     if state._host_overlays:
         idx = torch.nonzero(m).flatten().cpu().tolist()
         for i in idx:
             state._host_overlays.pop(i, None)
-    N.check(N.load().uuv_reset(state._ctx, C.byref(state._cstate()), rows_mask.data_ptr(),
-                               C.byref(packed), state.master_seed & M64, state._stream()),
+    N.check(N.load().uuv_reset_dl(state._ctx, C.byref(state._cstate()), N.DLArg(m).ptr,
+                                  C.byref(packed), state.master_seed & M64, state._stream()),
             EngineError)
 
 

@@ -12,7 +12,8 @@ of the ended episode in ``info["terminal_observation"]``.
 Everything per step — physics (K substeps), observation, reward,
 fail/terminated/truncated, info metrics, the auto-reset draw (Philox DR
 overlay, current, start pose) and the next-episode observation — runs in a
-single fused kernel launch (``uuv_task_step``); the host only enqueues it.
+single fused kernel launch (``uuv_task_step_dl``: commands and observations
+cross the C ABI as DLPack tensors); the host only enqueues it.
 Arrays are torch CUDA tensors in the batch dtype (float32 by default).
 """
 
@@ -418,10 +419,12 @@ class VecTaskEnv:
         term = self._new_obs()
         rout = torch.empty((len(_N.TR_NAMES), st._ld), dtype=dt, device=dev)
         fout = torch.empty((len(_N.TF_NAMES), st._ld), dtype=torch.uint8, device=dev)
-        _N.check(_N.load().uuv_task_step(
+        # commands in and the next observation out cross the ABI as DLPack tensors
+        _N.check(_N.load().uuv_task_step_dl(
             st._ctx, _C.byref(st._cstate()), _C.byref(self._task_c), _C.byref(self._sampler_c),
-            self.seed & ((1 << 64) - 1), u.data_ptr(), u.stride(0), self.sim.substeps,
-            self.sim.dt, _C.byref(self._io(obs, term, rout, fout)), st._stream()), TaskError)
+            self.seed & ((1 << 64) - 1), _N.DLArg(u).ptr, self.sim.substeps, self.sim.dt,
+            _C.byref(self._io(None, term, rout, fout)), _N.DLArg(obs).ptr, st._stream()),
+            TaskError)
         R = {k: rout[i, :n] for i, k in enumerate(_N.TR_NAMES)}
         F = {k: fout[i, :n].view(torch.bool) for i, k in enumerate(_N.TF_NAMES)}
         info = _Info(obs=obs, term=term, finished=F["finished"])

@@ -11,6 +11,8 @@ tests (product/oracle) build bit-identical configs from one description.
 * ``dense``      — bluerov with full (non-diagonal) SPD added-mass and damping
   matrices, a CoG offset and an inertia product term (covers the dense 6x6
   path of hydrodynamics.py:88-145).
+* ``rotor_relu`` — ``rotor_mix`` with a relu rotor network (the relu branch of
+  MLPWeights.forward, actuation.py:61-69).
 """
 
 import numpy as np
@@ -41,16 +43,18 @@ def build(name, mod_vehicles, mod_actuation, mod_hydro, base):
     for a in base.actuators:
         acts.append(copy.deepcopy(a))
     rb, co = base.rb, base.coeffs
-    if name == "rotor_mix":
+    if name in ("rotor_mix", "rotor_relu"):
+        # rotor_relu: the same mix with a relu rotor network (actuation.py:61-69 relu branch)
+        act_fn = "relu" if name == "rotor_relu" else "tanh"
         net = mod_actuation.MLPWeights(layer_sizes=T200["layer_sizes"], weights=T200["weights"],
-                                       biases=T200["biases"], activation="tanh")
+                                       biases=T200["biases"], activation=act_fn)
         for j in (0, 1):
             acts[j].rotor_model = "data_driven"
             acts[j].mlp = net
             acts[j].weights_ref = "t200_mlp.yaml"
         acts[2].rotor_model = "zero_order"
         acts[4].reaction_coeff = 3.0e-6
-        return V.VehicleConfig(name="rotor_mix", rb=copy.deepcopy(rb), coeffs=copy.deepcopy(co),
+        return V.VehicleConfig(name=name, rb=copy.deepcopy(rb), coeffs=copy.deepcopy(co),
                                actuators=acts, bounding_radius=base.bounding_radius)
     if name == "dense":
         M_A = _spd_perturb(np.diag(co.M_A), 0.2, 1)
@@ -67,4 +71,4 @@ def build(name, mod_vehicles, mod_actuation, mod_hydro, base):
     raise KeyError(name)
 
 
-VARIANTS = ("rotor_mix", "dense")
+VARIANTS = ("rotor_mix", "dense", "rotor_relu")

@@ -254,7 +254,8 @@ def test_neutral_vehicle_holds_station(dtype):
 
 TASK_FIXTURES = [f"task_{k}_{lv}" for k in ("station_keeping", "tracking", "docking")
                  for lv in ("standard", "disturbed", "disturbed_dr")] + [
-    "task_tracking_k8_hauv", "task_station_iauv_dr", "task_station_fail", "task_docking_contact",
+    "task_tracking_k8_hauv", "task_tracking_bluerov_k8", "task_station_iauv_dr",
+    "task_station_fail", "task_docking_contact",
     "task_station_keeping_standard_pcg64", "task_tracking_disturbed_pcg64",
     "task_docking_disturbed_dr_pcg64"]
 

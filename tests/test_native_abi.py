@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_struct_sizes_and_version():
     lib = N.load()
-    assert lib.uuv_abi_version() == N.ABI_VERSION == 4
+    assert lib.uuv_abi_version() == N.ABI_VERSION == 5
     sizes = (C.c_int64 * 6)()
     lib.uuv_abi_sizes(sizes)
     assert list(sizes) == [C.sizeof(N.Hull), C.sizeof(N.State), C.sizeof(N.Sampler),
@@ -117,3 +117,63 @@ def test_hull_rejects_too_many_actuators():
     big.actuators = big.actuators + [copy.deepcopy(big.actuators[0])]
     with pytest.raises(EngineError):
         pack_hull(big)
+
+
+def _dl_fields(n=5, a=6, ld=32, dtype=None, device="cpu"):
+    import torch
+
+    dtype = dtype or torch.float32
+    soa = torch.zeros((13 + a, ld), dtype=dtype, device=device)
+    f = [soa[0:3, :n].t(), soa[3:7, :n].t(), soa[7:13, :n].t(), soa[13:, :n].t(), None,
+         torch.zeros(ld, dtype=torch.int32, device=device)[:n],
+         torch.zeros(ld, dtype=torch.int32, device=device)[:n],
+         torch.zeros(ld, dtype=torch.bool, device=device)[:n]]
+    return f
+
+
+def _bind(fields, count=None):
+    lib = N.load()
+    args = [N.dl(t) for t in fields]
+    ptrs = (C.c_void_p * len(args))(*[N.dl_ptr(x) for x in args])
+    st = N.State()
+    return lib.uuv_state_from_dlpack(C.byref(st), ptrs, count or len(args)), st
+
+
+def test_dlpack_state_validation_without_gpu():
+    """uuv_state_from_dlpack validates the DLPack fields in C (device checked before any
+    CUDA call, so CPU tensors are refused here without a GPU)."""
+    import torch
+
+    lib = N.load()
+    status, _ = _bind(_dl_fields(), count=3)
+    assert status == N_ERR_ARG and b"DLPack fields" in lib.uuv_last_error()
+    f = _dl_fields()
+    f[N.DL_STEPS] = None
+    status, _ = _bind(f)
+    assert status == N_ERR_ARG and b"steps: null" in lib.uuv_last_error()
+    status, _ = _bind(_dl_fields())  # CPU tensors
+    assert status == N_ERR_ARG and b"not CUDA" in lib.uuv_last_error()
+    f = _dl_fields(a=9, ld=32)
+    status, _ = _bind(f)
+    assert status == N_ERR_SHAPE and b"act" in lib.uuv_last_error()
+    f = _dl_fields(dtype=torch.float16)
+    status, _ = _bind(f)
+    assert status == N_ERR_ARG and b"float32 or float64" in lib.uuv_last_error()
+
+
+N_ERR_ARG, N_ERR_SHAPE = 1, 2
+
+
+def test_dlarg_exports_the_tensor_layout():
+    """DLArg hands the C side torch's own DLPack export (shape, strides, dtype codes)."""
+    import torch
+
+    soa = torch.zeros((3, 64))
+    arg = N.DLArg(soa[:, :40].t())
+    t = C.cast(arg.ptr, C.POINTER(N.DLTensor)).contents
+    assert t.ndim == 2 and (t.shape[0], t.shape[1]) == (40, 3)
+    assert (t.strides[0], t.strides[1]) == (1, 64)
+    assert (t.dtype.code, t.dtype.bits, t.dtype.lanes) == (2, 32, 1)
+    assert t.device.device_type == 1  # kDLCPU
+    b = C.cast(N.DLArg(torch.zeros(4, dtype=torch.bool)).ptr, C.POINTER(N.DLTensor)).contents
+    assert (b.dtype.code, b.dtype.bits) == (6, 8)
