@@ -1,6 +1,9 @@
-# Full GPU test suite (+ optional -k filter in $1) on the box.
-cd $GRAFT_REPO_ROOT
+#!/bin/bash
+# GPU test suite + smoke on the box; logs under gpurun_out/
+cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -x -q ${1:+-k "$1"} > gpurun_out/pytest_gpu.log 2>&1
-echo "pytest exit $?"
-tail -15 gpurun_out/pytest_gpu.log
+python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 900 ${PYTEST_ARGS:-} > gpurun_out/pytest_gpu.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+echo "smoke rc=$?" >> gpurun_out/smoke.log
+tail -5 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log
