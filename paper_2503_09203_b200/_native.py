@@ -169,15 +169,19 @@ _capsule_ptr.argtypes = [C.py_object, C.c_char_p]
 class DLArg:
     """A torch tensor exported through DLPack (``torch.utils.dlpack.to_dlpack``),
     borrowed by one C call: ``.ptr`` is the capsule's ``DLManagedTensor*`` (its
-    first member is the ``DLTensor``); the capsule, kept alive here, frees it."""
+    first member is the ``DLTensor``); the capsule, owned here, frees it when this
+    object goes away.  Pass the DLArg ITSELF as the ctypes argument
+    (``_as_parameter_``): the call's argument tuple then keeps the capsule alive --
+    ``DLArg(t).ptr`` alone would let it be freed before the call runs."""
 
-    __slots__ = ("capsule", "ptr")
+    __slots__ = ("capsule", "ptr", "_as_parameter_")
 
     def __init__(self, tensor):
         from torch.utils.dlpack import to_dlpack
 
         self.capsule = to_dlpack(tensor)
         self.ptr = _capsule_ptr(self.capsule, b"dltensor")
+        self._as_parameter_ = C.c_void_p(self.ptr)
 
 
 def dl(tensor):

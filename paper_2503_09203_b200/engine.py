@@ -688,7 +688,7 @@ def step_batch(state: BatchState, commands, *, pose_out=None, out=None) -> Batch
         return _step_host(state, commands, width, _host_out(state, pose_out, out))
     cmd = _commands(state, commands, width)
     arg = N.DLArg(cmd)
-    status = N.load().uuv_step_dl(state._ctx, C.byref(state._cstate()), arg.ptr,
+    status = N.load().uuv_step_dl(state._ctx, C.byref(state._cstate()), arg,
                                   state.sim.substeps, state.sim.dt, state._stream())
     if status:
         N.check(status, EngineError)
@@ -807,7 +807,7 @@ def _step_host(state: BatchState, commands, width, ho):
     lib = N.load()
     if src is None:  # device commands with host result rows
         cmd = _commands(state, commands, width)
-        N.check(lib.uuv_step_dl(st._ctx, C.byref(st._cstate()), N.DLArg(cmd).ptr,
+        N.check(lib.uuv_step_dl(st._ctx, C.byref(st._cstate()), N.DLArg(cmd),
                                 st.sim.substeps, st.sim.dt, st._stream()), EngineError)
         torch.cuda.current_stream(st.device).synchronize()
         _copy_result(st, ho)
@@ -878,7 +878,7 @@ def _device_reset(state: BatchState, m, sampler: DeviceSampler):
         idx = torch.nonzero(m).flatten().cpu().tolist()
         for i in idx:
             state._host_overlays.pop(i, None)
-    N.check(N.load().uuv_reset_dl(state._ctx, C.byref(state._cstate()), N.DLArg(m).ptr,
+    N.check(N.load().uuv_reset_dl(state._ctx, C.byref(state._cstate()), N.DLArg(m),
                                   C.byref(packed), state.master_seed & M64, state._stream()),
             EngineError)
 

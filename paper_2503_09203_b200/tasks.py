@@ -422,8 +422,8 @@ class VecTaskEnv:
         # commands in and the next observation out cross the ABI as DLPack tensors
         _N.check(_N.load().uuv_task_step_dl(
             st._ctx, _C.byref(st._cstate()), _C.byref(self._task_c), _C.byref(self._sampler_c),
-            self.seed & ((1 << 64) - 1), _N.DLArg(u).ptr, self.sim.substeps, self.sim.dt,
-            _C.byref(self._io(None, term, rout, fout)), _N.DLArg(obs).ptr, st._stream()),
+            self.seed & ((1 << 64) - 1), _N.DLArg(u), self.sim.substeps, self.sim.dt,
+            _C.byref(self._io(None, term, rout, fout)), _N.DLArg(obs), st._stream()),
             TaskError)
         R = {k: rout[i, :n] for i, k in enumerate(_N.TR_NAMES)}
         F = {k: fout[i, :n].view(torch.bool) for i, k in enumerate(_N.TF_NAMES)}
@@ -439,18 +439,22 @@ class VecTaskEnv:
         return obs, R["reward"], F["terminated"], F["truncated"], info
 
     # -------------------------------------------------------------- rollout statistics
-    def rollout_stats(self, reset: bool = True, group=None) -> dict:
-        """Sums since the last call: reward, finished, success, failure, truncated,
-        metric over finished rows, diverged, frames — reduced on device in a fixed
-        order, then all-reduced over ``group`` (NCCL) when torch.distributed is up."""
+    def rollout_stats_tensor(self, reset: bool = True, group=None) -> torch.Tensor:
+        """``rollout_stats`` as a float64 device tensor in ``_N.ST_NAMES`` order, without a
+        host synchronisation (the reduction and the NCCL all-reduce are stream-ordered)."""
         out = torch.empty(len(_N.ST_NAMES), dtype=torch.float64, device=self.state.device)
         _N.check(_N.load().uuv_rollout_stats(self._stats.data_ptr(), self._stats.shape[0],
                                              out.data_ptr(), 1 if reset else 0,
                                              self.state._stream()), TaskError)
         from .distributed import allreduce_sum
 
-        out = allreduce_sum(out, group)
-        return dict(zip(_N.ST_NAMES, out.tolist()))
+        return allreduce_sum(out, group)
+
+    def rollout_stats(self, reset: bool = True, group=None) -> dict:
+        """Sums since the last call: reward, finished, success, failure, truncated,
+        metric over finished rows, diverged, frames — reduced on device in a fixed
+        order, then all-reduced over ``group`` (NCCL) when torch.distributed is up."""
+        return dict(zip(_N.ST_NAMES, self.rollout_stats_tensor(reset, group).tolist()))
 
 
 StationKeepingEnv = TrackingEnv = DockingEnv = VecTaskEnv

@@ -204,14 +204,14 @@ def test_dlpack_capsules_through_ctypes(dtype):
     for t in range(5):
         cmd = (torch.rand((n, a), device="cuda", generator=g) * 2 - 1).to(dtype)
         arg = N.DLArg(cmd)
-        assert lib.uuv_step_dl(ctx, C.byref(cst), arg.ptr, 1, 0.02, stream) == 0, last_error()
+        assert lib.uuv_step_dl(ctx, C.byref(cst), arg, 1, 0.02, stream) == 0, last_error()
         E.step_batch(ref, cmd)
     torch.cuda.synchronize()
     assert torch.equal(fields[0], ref.p) and torch.equal(fields[2], ref.nu)
     assert torch.equal(fields[5], ref.steps) and torch.equal(fields[6], ref.episodes)
 
     def err(cmd):
-        return lib.uuv_step_dl(ctx, C.byref(cst), N.DLArg(cmd).ptr, 1, 0.02, stream)
+        return lib.uuv_step_dl(ctx, C.byref(cst), N.DLArg(cmd), 1, 0.02, stream)
 
     other = torch.float64 if dtype == torch.float32 else torch.float32
     assert err(torch.zeros((n, a), dtype=other, device="cuda")) == 1
@@ -224,7 +224,7 @@ def test_dlpack_capsules_through_ctypes(dtype):
     wide = torch.zeros((n, 16), dtype=dtype, device="cuda")[:, :a]  # row stride 16: accepted
     assert err(wide) == 0
     bad_mask = torch.ones(n, dtype=torch.float32, device="cuda")
-    assert lib.uuv_reset_dl(ctx, C.byref(cst), N.DLArg(bad_mask).ptr, C.byref(smp), 0,
+    assert lib.uuv_reset_dl(ctx, C.byref(cst), N.DLArg(bad_mask), C.byref(smp), 0,
                             stream) == 1
     assert "bool or uint8" in last_error()
     lib.uuv_ctx_destroy(ctx)
@@ -274,8 +274,8 @@ def test_task_step_dl_writes_the_observation_tensor():
     bad = torch.empty((n, envs[0].obs_dim + 1), device="cuda")
     io = envs[0]._io(None)
     status = lib.uuv_task_step_dl(st._ctx, C.byref(st._cstate()), C.byref(envs[0]._task_c),
-                                  C.byref(envs[0]._sampler_c), 3, N.DLArg(u).ptr, 1, 0.02,
-                                  C.byref(io), N.DLArg(bad).ptr, st._stream())
+                                  C.byref(envs[0]._sampler_c), 3, N.DLArg(u), 1, 0.02,
+                                  C.byref(io), N.DLArg(bad), st._stream())
     assert status == 2 and "obs" in last_error()
 
 

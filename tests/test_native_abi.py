@@ -175,5 +175,28 @@ def test_dlarg_exports_the_tensor_layout():
     assert (t.strides[0], t.strides[1]) == (1, 64)
     assert (t.dtype.code, t.dtype.bits, t.dtype.lanes) == (2, 32, 1)
     assert t.device.device_type == 1  # kDLCPU
-    b = C.cast(N.DLArg(torch.zeros(4, dtype=torch.bool)).ptr, C.POINTER(N.DLTensor)).contents
+    barg = N.DLArg(torch.zeros(4, dtype=torch.bool))  # keep the capsule alive while reading
+    b = C.cast(barg.ptr, C.POINTER(N.DLTensor)).contents
     assert (b.dtype.code, b.dtype.bits) == (6, 8)
+
+
+def test_dlarg_is_passed_as_the_ctypes_argument():
+    """A temporary DLArg passed directly stays alive for the call (``_as_parameter_``): the C
+    side reads its DLTensor (here: refuses its CPU device) -- no GPU call is reached."""
+    import torch
+
+    lib = N.load()
+    h = pack_hull(pv.load_vehicle("bluerov"))
+    ctx = C.c_void_p()
+    assert lib.uuv_ctx_create(C.byref(h), 1, C.byref(ctx)) == 0
+    st = N.State()
+    st.dtype, st.a_max, st.n_envs, st.ld = 0, 6, 4, 32
+    for name in ("p", "q", "nu", "act", "steps", "episodes", "diverged"):
+        setattr(st, name, 256)  # never dereferenced: validation fails first
+    for k in range(N.OV_COUNT):
+        st.slot[k] = -1
+    status = lib.uuv_step_dl(ctx, C.byref(st), N.DLArg(torch.zeros((4, 6))), 1, 0.02, None)
+    assert status == N_ERR_ARG and b"commands: DLPack device type 1" in lib.uuv_last_error()
+    status = lib.uuv_step_dl(ctx, C.byref(st), N.DLArg(torch.zeros((5, 6))), 1, 0.02, None)
+    assert b"not CUDA" in lib.uuv_last_error()
+    lib.uuv_ctx_destroy(ctx)
