@@ -1,34 +1,39 @@
 """Benchmark: env frames/s of the batched 6-DOF Fossen step (hydro + thruster + integrate).
 
-Workload (BASELINE.json configs[1]): BlueROV2, 4096 envs per GPU, per-env
-domain-randomised mass / volume / damping / thruster gain ~ U[0.8, 1.2] drawn
-on device from the Philox stream keyed (seed 0, global env, episode 0),
-commands U(-1, 1).  A step is one control step (one ``uuv_step`` launch).
+Workload (BASELINE.json configs[1], the config quoted "on 1 B200"): BlueROV2,
+4096 envs per GPU, per-env domain-randomised mass / volume / damping / thruster
+gain ~ U[0.8, 1.2] drawn on device from the Philox stream keyed (seed 0, global
+env, episode 0), commands U(-1, 1).  A step is one control step of every env
+(``step_batch``: one ``uuv_step_dl`` launch).  N GPUs = N processes, one per
+GPU, each owning 4096 globally-indexed envs (weak scaling, no per-step
+collective); ``--gpus N`` without torchrun re-executes itself under
+``torch.distributed.run`` (NCCL, rendezvous on 127.0.0.1).
 
-* value — device-resident throughput: K steps replayed from a CUDA graph,
-  CUDA events on the launching stream, barrier + max over ranks.  Each step
-  reads a fresh command buffer from a ring larger than L2 (env state stays
-  resident, as in an RL loop); L2 is flushed once before the timed region.
+* value — device-resident throughput: K steps replayed from CUDA graphs, CUDA
+  events on the launching stream, barrier + max over ranks.  Each step reads a
+  fresh command buffer from a ring larger than L2 (env state stays resident, as
+  in an RL loop); L2 is flushed before the timed region.  The graphs are
+  submitted behind a short device-side spin (``torch.cuda._sleep``, before the
+  start event), so the GPU does not idle on host submission inside the region;
+  the host submission time is reported beside it.
 * e2e — the same metric through the public API with HOST buffers:
-  ``step_batch(state, pinned_host_commands, pose_out=pinned_host_pose)`` per
-  step: the step's commands go host->device and its p, q, nu rows
-  device->host, and the call returns when they are in host memory.  Two
-  paths are timed and the faster is reported (both in ``e2e.per_path``): one
-  launch per step whose kernel reads/writes the mapped pinned buffers over the
-  link (CUDA events), and the same calls inside ``engine.serve(state)``, where a
-  resident step kernel is driven by a doorbell in mapped pinned memory (no
-  launch, no stream sync per step; host clock around exactly K synchronous
-  steps).
+  ``step_batch(state, pinned_host_commands, out=HostStepOut)`` per step: the
+  step's commands go host->device and its whole result (p, q, nu, act, steps,
+  diverged -- what the reference's step_batch leaves in its numpy state) comes
+  back device->host; the call returns when it is in host memory.  Two paths are
+  timed and the faster is reported (both in ``e2e.per_path``): one launch per
+  step whose kernel reads/writes the mapped pinned buffers (CUDA events), and
+  the same calls inside ``engine.serve(state)`` (a resident step kernel rung by a
+  doorbell in mapped pinned memory; host clock around exactly K steps).
 * roofline — the step kernel's algorithmic bytes per launch / average launch
-  duration vs the measured HBM copy bandwidth (MEASURED_PEAKS.json).  At
-  4096 envs the step is launch/latency-bound, so ``roofline_at_scale`` also
-  reports the same kernel on 1,048,576 envs of the same workload (informational;
-  not the bench value).
-* cpu_baseline — the CPU oracle (numpy restatement of the reference) on the
-  same workload on this box's host cores (rank 0, N = 1 only).
+  duration vs the measured HBM copy bandwidth (MEASURED_PEAKS.json).
+* at_scale — the other BASELINE configs at their stated per-GPU sizes, each
+  device-timed the same way with its own per-step roofline (informational).
+* cpu_baseline — the reference's own CPU implementation (the unmodified
+  ``uuvsim`` from baseline/_ref when installed, else the oracle numpy port) on
+  the same workload on this box's host cores (rank 0, N = 1 only).
 
-``--impl reference`` runs the reference's CPU algorithm (the oracle port; the
-reference is pure numpy and cannot be installed here) on the same workload.
+``--impl reference`` runs that CPU implementation as the reference arm.
 """
 
 import argparse
@@ -50,12 +55,21 @@ DR_KEYS = ("damping*", "mass*", "thrust_coeff*", "volume*")
 METRIC = "env frames/sec (hydro+thruster+integrate)"
 WORKLOAD = ("cfg2: BlueROV2 station-keeping dynamics, 4096 envs/GPU, per-env DR "
             "mass/volume/damping/thrust_coeff ~ U[0.8,1.2] (Philox, device), cmds U(-1,1)")
+RING_BYTES = 160 << 20  # command rings larger than the 126 MB L2
 
 
-def algorithmic_bytes_per_frame(a=A_BLUEROV, n_dr=len(DR_KEYS), dtype_bytes=4):
+def bench_config(world):
+    """The config dict both arms print (identical, so the driver can pair them)."""
+    return {"workload": WORKLOAD, "global_batch": world * N_ENVS, "per_gpu_envs": N_ENVS,
+            "parallelism": f"env-shard x{world} (no per-step collective)"}
+
+
+def algorithmic_bytes_per_frame(a=A_BLUEROV, n_dr=len(DR_KEYS)):
     """state p,q,nu,act read+write, commands read, diverged r/w (1+1 B),
     steps r/w (4+4 B), plus the float64 DR record actually read (8 B per key)."""
-    return dtype_bytes * (2 * (13 + a) + a) + 2 + 8 + 8 * n_dr
+    from paper_2503_09203_b200.roofline import frame_bytes
+
+    return frame_bytes(a, n_dr)
 
 
 def dr_spec():
@@ -66,21 +80,25 @@ def dr_spec():
 
 def load_traffic():
     """DRAM bytes per launch of the step kernel from the committed ncu capture."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json")) as f:
-            t = json.load(f)
-        return t["dram_bytes_read"] + t["dram_bytes_write"]
-    except Exception:
-        return None
+    for rnd in ("r02", "r01"):
+        try:
+            with open(os.path.join(ROOT, "profiles", rnd, "ncu_traffic.json")) as f:
+                t = json.load(f)
+            return t["dram_bytes_read"] + t["dram_bytes_write"], f"profiles/{rnd}"
+        except Exception:
+            continue
+    return None, None
 
 
-def load_peaks():
+def cpu_model():
     try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            pk = json.load(f)
-        return float(pk["hbm_gbs"]), "measured"
-    except Exception:
-        return 6650.0, "fallback"
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 class ClockSampler:
@@ -113,7 +131,7 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
                 out, _ = self.proc.communicate()
-            self.lines = [l for l in out.splitlines() if l.strip()]
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
 
     def summary(self):
         sm, mx, reasons = [], None, set()
@@ -139,52 +157,112 @@ class ClockSampler:
 # ================================================================ reference (CPU) arm
 
 
-def cpu_probe(seconds=None, steps=None, warmup=3, workers=None):
-    """The oracle on the cfg2 workload: returns (frames/s, steps, elapsed, cores, reset_s)."""
-    from concurrent.futures import ThreadPoolExecutor
+def reference_modules():
+    """The unmodified reference (``pip install --target baseline/_ref``), or None."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "uuvsim")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import uuvsim.engine as RE
+        import uuvsim.randomization as RD
+        import uuvsim.vehicles as RV
+        from uuvsim.kinematics import Pose
+    except Exception:
+        return None
+    return RE, RD, RV, Pose
 
+
+def _reference_batch(workers):
+    """cfg2 in the reference itself: its make_batch / reset_envs (its own PCG64 streams,
+    sample_overlay draws, apply_overlay) / step_batch (engine.py:298, 487, 465)."""
+    RE, RD, RV, Pose = reference_modules()
+    veh = RV.load_vehicle("bluerov")
+    spec = RD.make_spec([RD.DRParameter(k, RD.Uniform(0.8, 1.2)) for k in DR_KEYS])
+    st = RE.make_batch(veh, RE.SimConfig(batch_size=N_ENVS, workers=workers), master_seed=0)
+    t0 = time.perf_counter()
+    RE.reset_envs(st, np.ones(N_ENVS, bool),
+                  lambda i, ep, rng: RE.EnvInit(pose=Pose(), overlay=RD.sample_overlay(spec, rng)))
+    return RE, st, time.perf_counter() - t0
+
+
+def _oracle_batch(workers):
     from oracle import uuv_oracle as O
     from paper_2503_09203_b200.vehicles import load_vehicle
 
-    workers = workers or os.cpu_count() or 1
-    veh = load_vehicle("bluerov")
     spec = dr_spec()
-    b = O.Batch(veh, N_ENVS, 0.02, 1, seed=0, workers=workers)
+    b = O.Batch(load_vehicle("bluerov"), N_ENVS, 0.02, 1, seed=0, workers=workers)
     t0 = time.perf_counter()
     b.reset(np.ones(N_ENVS, bool), lambda i, ep, r: O.Init(overlay=O.draw_overlay(spec, r)))
-    reset_s = time.perf_counter() - t0
+    return b, time.perf_counter() - t0
+
+
+def cpu_probe(seconds=None, steps=None, warmup=3):
+    """The reference's CPU path on the cfg2 workload, commands held fixed (BASELINE.md §3,
+    the throughput_probe protocol).  Worker count: the faster of 1 and all host threads
+    (the reference's thread pool gains nothing from more threads on small batches).
+    Returns (frames/s, steps, elapsed, workers, reset_s, kind)."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     cmds = np.random.default_rng(0).uniform(-1.0, 1.0, (N_ENVS, A_BLUEROV))
-    pool = ThreadPoolExecutor(max_workers=workers) if workers > 1 else None
-    for _ in range(warmup):
-        b.step(cmds, pool)
+    ncpu = os.cpu_count() or 1
+    if reference_modules() is not None:
+        kind = "reference"
+
+        def make(w):
+            RE, st, rs = _reference_batch(w)
+            return (lambda: RE.step_batch(st, cmds)), rs
+    else:
+        from concurrent.futures import ThreadPoolExecutor
+
+        kind = "port"
+        pools = {}
+
+        def make(w):
+            b, rs = _oracle_batch(w)
+            pool = pools.setdefault(w, ThreadPoolExecutor(max_workers=w) if w > 1 else None)
+            return (lambda: b.step(cmds, pool)), rs
+
+    best = None
+    for w in sorted({1, ncpu}):  # calibrate the worker count on a few steps
+        step, rs = make(w)
+        for _ in range(warmup):
+            step()
+        t0 = time.perf_counter()
+        for _ in range(3):
+            step()
+        rate = 3 / (time.perf_counter() - t0)
+        if best is None or rate > best[0]:
+            best = (rate, w, step, rs)
+    _, workers, step, reset_s = best
     k = 0
     t0 = time.perf_counter()
     while True:
-        b.step(cmds, pool)
+        step()
         k += 1
         el = time.perf_counter() - t0
         if (steps is not None and k >= steps) or (seconds is not None and el >= seconds):
             break
-    if pool is not None:
-        pool.shutdown()
-    return N_ENVS * k / el, k, el, workers, reset_s
+    return N_ENVS * k / el, k, el, workers, reset_s, kind
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    fps, k, el, cores, reset_s = cpu_probe(steps=args.steps, warmup=args.warmup)
-    sample = (f"full cfg2 workload ({N_ENVS} envs x {k} steps) on {cores} host threads; "
-              f"DR reset of {N_ENVS} envs took {reset_s:.2f} s (excluded)")
+    fps, k, el, workers, reset_s, kind = cpu_probe(steps=args.steps, warmup=args.warmup)
+    what = ("the unmodified reference uuvsim (baseline/_ref): make_batch / reset_envs / "
+            "step_batch" if kind == "reference" else "the oracle numpy port of the reference")
+    sample = (f"full cfg2 workload ({N_ENVS} envs x {k} steps, commands held fixed) through "
+              f"{what}, {workers} worker thread(s) (faster of 1 and {os.cpu_count()}); DR reset "
+              f"of {N_ENVS} envs took {reset_s:.2f} s (excluded)")
     line = {"metric": METRIC, "value": fps, "unit": "env-frames/s", "n_gpus": args.gpus,
             "steps": k, "warmup": args.warmup, "ms_per_step": 1e3 * el / k,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "impl": "reference",
-            "config": {"workload": WORKLOAD, "global_batch": N_ENVS, "parallelism": "cpu"},
-            "cpu_baseline": {"value": fps, "unit": "env-frames/s", "cores": cores,
-                             "kind": "port", "sample": sample},
+            "data": "synthetic", "impl": "reference", "config": bench_config(max(world, 1)),
+            "cpu_baseline": {"value": fps, "unit": "env-frames/s", "cores": workers,
+                             "host_threads": os.cpu_count(), "cpu_model": cpu_model(),
+                             "kind": kind, "sample": sample},
             "e2e": {"value": fps, "unit": "env-frames/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -194,30 +272,187 @@ def run_reference(args, rank, world):
 # ================================================================ B200 arm
 
 
-def run_b200(args, rank, world, local_rank):
+def command_ring(n, width, dev, gen, dtype=None):
+    import torch
+
+    per = n * width * 4
+    n_ring = max(2, -(-RING_BYTES // per))
+    ring = torch.rand((n_ring, n, width), device=dev, generator=gen) * 2 - 1
+    return ring if dtype is None else ring.to(dtype)
+
+
+class DeviceTimer:
+    """CUDA-event timing of graph replays on `stream`: L2 flushed first, the replays
+    enqueued behind a device-side spin so host submission is not inside the region."""
+
+    def __init__(self, dev, stream, barrier):
+        import torch
+
+        self.torch = torch
+        self.dev, self.stream, self.barrier = dev, stream, barrier
+        self.flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        self.e0 = torch.cuda.Event(enable_timing=True)
+        self.e1 = torch.cuda.Event(enable_timing=True)
+        self.gate_us = 200.0
+        self.submit_us = None
+        self.cycles_per_us = 1965.0  # B200 max SM clock: a spin of >= gate_us at any clock
+
+    def run(self, enqueue, gate=True):
+        torch = self.torch
+        with torch.cuda.stream(self.stream):
+            self.flush.fill_(1)
+        self.barrier()
+        torch.cuda.synchronize(self.dev)
+        with torch.cuda.stream(self.stream):
+            if gate:
+                torch.cuda._sleep(int(self.gate_us * self.cycles_per_us))
+            t0 = time.perf_counter()
+            self.e0.record(self.stream)
+            enqueue()
+            self.e1.record(self.stream)
+            sub = (time.perf_counter() - t0) * 1e6
+        torch.cuda.synchronize(self.dev)
+        self.barrier()
+        self.submit_us = sub
+        # keep the spin longer than the submission it hides (measured, with margin)
+        self.gate_us = max(self.gate_us, 3.0 * sub + 50.0)
+        return self.e0.elapsed_time(self.e1) / 1e3
+
+
+def capture_steps(step, k_total, stream, chunk=256):
+    """CUDA graphs of exactly k_total calls step(t) (chunks of <= chunk launches)."""
+    import torch
+
+    graphs, done = [], 0
+    while done < k_total:
+        c = min(chunk, k_total - done)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            with torch.cuda.graph(g, stream=stream):
+                for s in range(c):
+                    step(done + s)
+        graphs.append(g)
+        done += c
+    return graphs
+
+
+def at_scale_blocks(ctx, timer, stream, steps, gen):
+    """The other BASELINE configs at their per-GPU sizes (configs[2..4]); each block a
+    CUDA graph of `steps` control steps with fresh commands from a ring > L2."""
     import torch
 
     from paper_2503_09203_b200 import engine as E
-    from paper_2503_09203_b200.distributed import allreduce_max, shard_range
+    from paper_2503_09203_b200 import roofline as RF
+    from paper_2503_09203_b200.distributed import allreduce_max
+    from paper_2503_09203_b200.randomization import preset
+    from paper_2503_09203_b200.tasks import TaskConfig, make_env
+    from paper_2503_09203_b200.vehicles import BUILTIN_VEHICLES, load_vehicle
+
+    dev, rank = ctx.device, ctx.rank
+    out = {}
+
+    def measure(name, n, step_fn, warm_fn, bpf, fpf, desc, tail=None):
+        for t in range(3):
+            warm_fn(t)
+        torch.cuda.synchronize(dev)
+        graphs = capture_steps(step_fn, steps, stream)
+
+        def enqueue():
+            for g in graphs:
+                g.replay()
+            if tail is not None:
+                tail()
+
+        timer.run(enqueue)  # graph upload / first replay
+        el = allreduce_max(timer.run(enqueue), dev)
+        us = el / steps * 1e6
+        out[name] = {"workload": desc, "envs_per_gpu": n, "steps": steps, "us_per_step": us,
+                     "env_frames_per_s": ctx.world * n / (el / steps),
+                     "roofline": RF.roofline(us, n, bpf, fpf)}
+        del graphs
+        torch.cuda.empty_cache()
+
+    # cfg2 at 1M envs: the headline kernel where it is bandwidth-bound
+    n = 1 << 20
+    veh = load_vehicle("bluerov")
+    st = E.make_batch(veh, E.SimConfig(batch_size=n), master_seed=0, device=dev,
+                      env_offset=rank * n)
+    E.reset_envs(st, torch.ones(n, dtype=torch.bool, device=dev), E.spec_sampler(dr_spec()))
+    ring = command_ring(n, 6, dev, gen)
+    measure("cfg2_1m", n, lambda t: E.step_batch(st, ring[t % len(ring)]),
+            lambda t: E.step_batch(st, ring[t]), RF.frame_bytes(6, 4), RF.substep_flops("bluerov"),
+            "cfg2 workload at 1,048,576 envs/GPU")
+    del st, ring
+
+    # configs[2]: all five vehicles mixed, 262,144 envs (contiguous per-type runs)
+    n = 262_144
+    vehs = [load_vehicle(v) for v in BUILTIN_VEHICLES]
+    counts = [n // 5 + (1 if i < n % 5 else 0) for i in range(5)]
+    st = E.make_fleet_batch(vehs, counts, E.SimConfig(batch_size=n), device=dev,
+                            env_offset=rank * n)
+    E.reset_envs(st, torch.ones(n, dtype=torch.bool, device=dev))
+    ring = command_ring(n, st.a_max, dev, gen)
+    for v, s0, c in zip(vehs, np.concatenate([[0], np.cumsum(counts)[:-1]]), counts):
+        ring[:, int(s0):int(s0) + c, v.action_dim:] = 0.0  # padded command columns
+    a_mean = sum(v.action_dim * c for v, c in zip(vehs, counts)) / n
+    fpf = sum(RF.substep_flops(v.name) * c for v, c in zip(vehs, counts)) / n
+    measure("cfg3_mixed_262k", n, lambda t: E.step_batch(st, ring[t % len(ring)]),
+            lambda t: E.step_batch(st, ring[t]), RF.frame_bytes(a_mean, 0, mixed=True), fpf,
+            "configs[2]: five UUV models mixed (6/8/5/5/8 actuators), 262,144 envs/GPU")
+    del st, ring
+
+    # configs[3]: trajectory tracking, ocean current, 8 fused substeps, 1M envs (task step)
+    n = 1 << 20
+    env = make_env(TaskConfig(task="tracking", vehicle="bluerov", level="disturbed"),
+                   E.SimConfig(batch_size=n, substeps=8), seed=0, device=dev,
+                   env_offset=rank * n)
+    env.reset()
+    ring = command_ring(n, 6, dev, gen)
+    measure("cfg4_tracking_k8_1m", n, lambda t: env.step(ring[t % len(ring)]),
+            lambda t: env.step(ring[t]),
+            RF.frame_bytes(6, 0, True) + RF.task_bytes(6, env.obs_dim, True),
+            8 * RF.substep_flops("bluerov", current=True) + RF.TASK_FLOPS,
+            "configs[3]: tracking task, bluerov, level disturbed (current + payload), K=8, "
+            "1,048,576 envs/GPU, fused env.step")
+    del env, ring
+    torch.cuda.empty_cache()
+
+    # configs[4]: docking, train-preset DR, auto-reset, 1M envs per GPU, NCCL stats
+    env = make_env(TaskConfig(task="docking", vehicle="bluerov_heavy", level="disturbed_dr"),
+                   E.SimConfig(batch_size=n), seed=0, device=dev, env_offset=rank * n)
+    env.reset()
+    ring = command_ring(n, 8, dev, gen)
+    measure("cfg5_docking_1m", n, lambda t: env.step(ring[t % len(ring)]),
+            lambda t: env.step(ring[t]),
+            RF.frame_bytes(8, len(preset("train")) - 1, True) + RF.task_bytes(8, env.obs_dim,
+                                                                                False),
+            RF.substep_flops("bluerov_heavy", current=True, general=True) + RF.TASK_FLOPS,
+            "configs[4]: docking task, bluerov_heavy, level disturbed_dr (train preset), "
+            "auto-reset, 1,048,576 envs/GPU, rollout stats all-reduced once per rollout",
+            tail=lambda: env.rollout_stats_tensor())
+    out["cfg5_docking_1m"]["finished_per_frame"] = (
+        lambda s: s["finished"] / max(s["frames"], 1))(env.rollout_stats())
+    del env, ring
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_b200(args):
+    import torch
+
+    from paper_2503_09203_b200 import distributed as D
+    from paper_2503_09203_b200 import engine as E
+    from paper_2503_09203_b200 import roofline as RF
     from paper_2503_09203_b200.vehicles import load_vehicle
 
     # one process per GPU; UUV_BENCH_GPU_OVERRIDE=0 pins every rank to GPU 0 and
-    # UUV_DIST_BACKEND=gloo swaps NCCL for gloo (used to exercise the multi-rank
-    # path on a single-GPU box; the driver's runs use one GPU per rank over NCCL)
-    dev_index = int(os.environ.get("UUV_BENCH_GPU_OVERRIDE", local_rank))
-    dev = torch.device("cuda", dev_index)
-    torch.cuda.set_device(dev)
-    dist = world > 1
-    if dist:
-        backend = os.environ.get("UUV_DIST_BACKEND", "nccl")
-        if backend == "nccl":
-            torch.distributed.init_process_group("nccl", device_id=dev)
-        else:
-            torch.distributed.init_process_group(backend)
-
-    def barrier():
-        if dist:
-            torch.distributed.barrier()
+    # UUV_DIST_BACKEND=gloo swaps NCCL for gloo (exercises the multi-rank path on a
+    # single-GPU box; the driver's runs use one GPU per rank over NCCL)
+    override = os.environ.get("UUV_BENCH_GPU_OVERRIDE")
+    ctx = D.init(os.environ.get("UUV_DIST_BACKEND"),
+                 int(override) if override is not None else None)
+    dev, rank, world = ctx.device, ctx.rank, ctx.world
+    barrier = ctx.barrier
 
     veh = load_vehicle("bluerov")
     n = N_ENVS
@@ -226,87 +461,57 @@ def run_b200(args, rank, world, local_rank):
                       env_offset=offset)
     E.reset_envs(st, torch.ones(n, dtype=torch.bool, device=dev), E.spec_sampler(dr_spec()))
 
-    # command ring larger than L2 (126 MB): every timed step reads fresh inputs
-    ring_bytes = 160 << 20
-    per = n * A_BLUEROV * 4
-    n_ring = max(2, ring_bytes // per)
     gen = torch.Generator(device=dev).manual_seed(offset)
-    ring = torch.rand((n_ring, n, A_BLUEROV), device=dev, generator=gen) * 2 - 1
+    ring = command_ring(n, A_BLUEROV, dev, gen)
+    n_ring = len(ring)
     stream = torch.cuda.Stream(dev)
     k_total = args.steps
-
-    def capture(k, start):
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.stream(stream):
-            with torch.cuda.graph(g, stream=stream):
-                for s in range(k):
-                    E.step_batch(st, ring[(start + s) % n_ring])
-        return g
-
     torch.cuda.synchronize(dev)
-    # warmup (untimed), graph capture of exactly K steps in chunks
     with torch.cuda.stream(stream):
         for w in range(args.warmup):
             E.step_batch(st, ring[w % n_ring])
     torch.cuda.synchronize(dev)
-    chunk = 256
-    graphs, done = [], 0
-    while done < k_total:
-        c = min(chunk, k_total - done)
-        graphs.append(capture(c, args.warmup + done))
-        done += c
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    graphs = capture_steps(lambda s: E.step_batch(st, ring[(args.warmup + s) % n_ring]),
+                           k_total, stream)
+    timer = DeviceTimer(dev, stream, barrier)
 
-    def timed():
-        with torch.cuda.stream(stream):
-            flush.fill_(1)
-        barrier()
-        torch.cuda.synchronize(dev)
-        with torch.cuda.stream(stream):
-            e0.record(stream)
-            for g in graphs:
-                g.replay()
-            e1.record(stream)
-        torch.cuda.synchronize(dev)
-        barrier()
-        return e0.elapsed_time(e1) / 1e3
+    def enqueue():
+        for g in graphs:
+            g.replay()
 
-    timed()  # one untimed replay of the captured graphs (graph upload / first-run effects)
-    with ClockSampler(dev_index) as clk:
+    timer.run(enqueue)  # untimed: graph upload / first-run effects, gate calibration
+    with ClockSampler(dev.index) as clk:
         t0 = time.perf_counter()
-        el = timed()
-        # keep sampling clocks under the same load for >= 1 s
-        while time.perf_counter() - t0 < 1.0:
-            timed()
-    el_max = allreduce_max(el, dev)
+        el = timer.run(enqueue)
+        submit_us = timer.submit_us
+        while time.perf_counter() - t0 < 1.0:  # keep sampling clocks under the same load
+            timer.run(enqueue)
+    el_ungated = timer.run(enqueue, gate=False)  # for the record: host submission inside
+    el_max = D.allreduce_max(el, dev)
     frames = world * n * k_total
     value = frames / el_max
     ms_per_step = 1e3 * el_max / k_total
-    # roofline of the step kernel (the only kernel in the timed region)
     bpf = algorithmic_bytes_per_frame()
-    launch_s = el / k_total
-    achieved = n * bpf / launch_s / 1e9
-    peak, peak_kind = load_peaks()
+    us_launch = el / k_total * 1e6
+    roof = RF.roofline(us_launch, n, bpf, RF.substep_flops("bluerov"))
+    traffic, traffic_src = load_traffic()
+    roof.update(traffic=traffic, traffic_note=f"ncu dram bytes per launch (cold cache), "
+                f"{traffic_src}" if traffic_src else None,
+                kernel="k_step<float,1,DR,6,DM>")
 
-    # e2e through the public API with host buffers
-    # per-step commands from a ring of 64 pinned host buffers (fresh values every
-    # step, buffers reused as a host control loop reuses its staging buffers; a
-    # 1000-buffer ring adds ~3-5 us/step of GPU-side translation of never-seen
-    # host pages, scripts/probes/serve_overhead.py)
+    # e2e through the public API with host buffers: per-step commands from a ring of
+    # 64 pinned host buffers (fresh values every step, buffers reused as a host control
+    # loop reuses its staging buffers), the whole step result back in pinned buffers
     e2e_ring = min(64, k_total)
     host_cmds = torch.empty((e2e_ring, n, A_BLUEROV), dtype=torch.float32).pin_memory()
     host_cmds.copy_(torch.rand(e2e_ring, n, A_BLUEROV) * 2 - 1)
-    host_out = torch.empty((13, n), dtype=torch.float32).pin_memory()
+    res = E.HostStepOut(st)
     cur = torch.cuda.current_stream(dev)
 
     def e2e_step(t):
-        # public API, host buffers: pinned commands in, pinned (13, N) pose rows out;
-        # returns when the step's pose rows are in host memory
-        E.step_batch(st, host_cmds[t % e2e_ring], pose_out=host_out)
+        E.step_batch(st, host_cmds[t % e2e_ring], out=res)
 
-    # (1) launched path: one uuv_step_host call per step (kernel reads/writes the
-    # mapped pinned buffers), CUDA events on the launching stream
+    # (1) launched path: one uuv_step_host call per step, CUDA events on its stream
     for t in range(min(args.warmup, k_total)):
         e2e_step(t)
     barrier()
@@ -317,14 +522,12 @@ def run_b200(args, rank, world, local_rank):
         e2e_step(t)
     f1.record(cur)
     torch.cuda.synchronize(dev)
-    e2e_launch_el = allreduce_max(f0.elapsed_time(f1) / 1e3, dev)
-    # (2) the same calls inside engine.serve(): a resident step kernel driven by a
-    # doorbell in mapped pinned memory (no launch / stream sync per step); the
-    # steps are synchronous, so the host clock brackets exactly K of them
+    e2e_launch_el = D.allreduce_max(f0.elapsed_time(f1) / 1e3, dev)
+    # (2) the same calls inside engine.serve(); synchronous steps, host clock around K
     barrier()
     torch.cuda.synchronize(dev)
-    # under a kernel profiler (ncu serialises launches) a resident kernel would
-    # only wait out its idle timeout: skip the served path there
+    # under a kernel profiler (ncu serialises launches) a resident kernel would only
+    # wait out its idle timeout: skip the served path there
     profiled = args.no_serve or bool(os.environ.get("CUDA_INJECTION64_PATH"))
     e2e_serve_el = float("inf")
     if not profiled:
@@ -336,85 +539,56 @@ def run_b200(args, rank, world, local_rank):
                 e2e_step(t)
             e2e_serve_el = time.perf_counter() - t0
         torch.cuda.synchronize(dev)
-    e2e_serve_el = allreduce_max(e2e_serve_el, dev)
+    e2e_serve_el = D.allreduce_max(e2e_serve_el, dev)
     e2e_el = min(e2e_serve_el, e2e_launch_el)
-    e2e_path = ("step_batch inside engine.serve(): resident step kernel, doorbell in mapped "
-                "pinned memory" if e2e_el == e2e_serve_el else
-                "step_batch -> uuv_step_host (one launch per step, mapped pinned buffers)")
+    e2e_path = ("step_batch(host cmds, out=HostStepOut) inside engine.serve(): resident step "
+                "kernel, doorbell in mapped pinned memory" if e2e_el == e2e_serve_el else
+                "step_batch(host cmds, out=HostStepOut) -> uuv_step_host (one launch per step, "
+                "mapped pinned buffers)")
     barrier()
+    del graphs
+    torch.cuda.empty_cache()
 
-    # the same kernel at scale (informational): 1,048,576 envs of the same
-    # workload (state + DR record + commands ~ 230 MB >> L2), CUDA graph of 20
-    # steps, CUDA events -> achieved bandwidth of the step kernel where it is
-    # HBM-bound rather than launch/latency-bound
     scale = None
     if not args.no_scale:
-        n_big = 1 << 20
-        big = E.make_batch(veh, E.SimConfig(batch_size=n_big), master_seed=0, device=dev,
-                           env_offset=rank * n_big)
-        E.reset_envs(big, torch.ones(n_big, dtype=torch.bool, device=dev),
-                     E.spec_sampler(dr_spec()))
-        cmd_big = torch.rand((n_big, A_BLUEROV), device=dev, generator=gen) * 2 - 1
-        with torch.cuda.stream(stream):
-            for _ in range(3):
-                E.step_batch(big, cmd_big)
-        torch.cuda.synchronize(dev)
-        gb = torch.cuda.CUDAGraph()
-        with torch.cuda.stream(stream):
-            with torch.cuda.graph(gb, stream=stream):
-                for _ in range(20):
-                    E.step_batch(big, cmd_big)
-        torch.cuda.synchronize(dev)
-        with torch.cuda.stream(stream):
-            e0.record(stream)
-            gb.replay()
-            e1.record(stream)
-        torch.cuda.synchronize(dev)
-        t_big = e0.elapsed_time(e1) / 1e3 / 20
-        a_big = n_big * bpf / t_big / 1e9
-        scale = {"envs_per_gpu": n_big, "us_per_step": t_big * 1e6,
-                 "env_frames_per_s": n_big / t_big, "achieved": a_big, "peak": peak,
-                 "unit": "GB/s", "frac": a_big / peak}
-        del big, cmd_big, gb
-        torch.cuda.empty_cache()
+        scale = at_scale_blocks(ctx, timer, stream, 20, gen)
 
     if rank == 0:
+        cfg = bench_config(world)
         line = {
             "metric": METRIC, "value": value, "unit": "env-frames/s", "n_gpus": world,
             "steps": k_total, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic",
-            "config": {"workload": WORKLOAD, "global_batch": world * n, "per_gpu_envs": n,
-                       "parallelism": f"env-shard x{world} (no per-step collective)",
-                       "l2": "inputs larger than L2: per-step commands from a "
-                             f"{n_ring * per >> 20} MiB ring; L2 flushed before the timed region; "
-                             "env state resident",
-                       "launch": "CUDA graph of K uuv_step launches"},
+            "data": "synthetic", "config": cfg,
+            "timing": {"l2": f"inputs larger than L2: per-step commands from a "
+                             f"{n_ring * n * A_BLUEROV * 4 >> 20} MiB ring; L2 flushed before "
+                             "the timed region; env state resident",
+                       "launch": "CUDA graphs of K step_batch launches (uuv_step_dl), "
+                                 "programmatic dependent launch between steps",
+                       "host_submit_us": submit_us, "gate_us": timer.gate_us,
+                       "us_per_step_with_submit_inside": el_ungated / k_total * 1e6},
             "e2e": {"value": world * n * k_total / e2e_el, "unit": "env-frames/s",
-                    "h2d_bytes_per_step": n * A_BLUEROV * 4, "d2h_bytes_per_step": n * 13 * 4,
+                    "h2d_bytes_per_step": n * A_BLUEROV * 4, "d2h_bytes_per_step": res.nbytes,
                     "path": e2e_path,
                     "per_path": {"serve": (world * n * k_total / e2e_serve_el
                                            if e2e_serve_el != float("inf") else None),
                                  "launch_per_step": world * n * k_total / e2e_launch_el}},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak,
-                         "traffic": load_traffic(),
-                         "traffic_note": "ncu dram bytes per launch (cold cache), profiles/r01",
-                         "peak_source": peak_kind,
-                         "bytes_per_frame": bpf, "kernel": "k_step<float,1,DR=true>"},
-            "roofline_at_scale": scale,
+            "roofline": roof,
+            "at_scale": scale,
             "gpu_launches": k_total,
             "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu_baseline:
-            fps, k, cel, cores, reset_s = cpu_probe(seconds=args.cpu_seconds)
+            fps, k, cel, workers, reset_s, kind = cpu_probe(seconds=args.cpu_seconds)
+            what = "unmodified reference uuvsim (baseline/_ref)" if kind == "reference" else \
+                "oracle numpy port"
             line["cpu_baseline"] = {
-                "value": fps, "unit": "env-frames/s", "cores": cores, "kind": "port",
+                "value": fps, "unit": "env-frames/s", "cores": workers,
+                "host_threads": os.cpu_count(), "cpu_model": cpu_model(), "kind": kind,
                 "sample": f"{N_ENVS} envs x {k} steps ({cel:.1f} s) of the same workload, "
-                          f"oracle numpy port, {cores} threads"}
+                          f"{what}, {workers} worker thread(s)"}
         print(json.dumps(line), flush=True)
-    if dist:
-        torch.distributed.destroy_process_group()
+    D.finalize(ctx)
     return 0
 
 
@@ -429,16 +603,21 @@ def main():
     ap.add_argument("--no-serve", action="store_true",
                     help="time only the launched e2e path (for runs under a kernel profiler)")
     ap.add_argument("--no-scale", action="store_true",
-                    help="skip the informational 1M-env roofline_at_scale measurement")
+                    help="skip the informational at-scale blocks of the other configs")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
-        return run_reference(args, rank, world)
-    return run_b200(args, rank, world, local_rank)
+        return run_reference(args, rank, world if "WORLD_SIZE" in os.environ else args.gpus)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-execute under torch.distributed.run (NCCL)
+        from paper_2503_09203_b200.distributed import launch
+
+        return launch(os.path.abspath(__file__), sys.argv[1:], args.gpus,
+                      env={"NCCL_DEBUG": os.environ.get("NCCL_DEBUG", "INFO")})
+    return run_b200(args)
 
 
 if __name__ == "__main__":
