@@ -9,11 +9,14 @@ GPU, each owning 4096 globally-indexed envs (weak scaling, no per-step
 collective); ``--gpus N`` without torchrun re-executes itself under
 ``torch.distributed.run`` (NCCL, rendezvous on 127.0.0.1).
 
-* value — device-resident throughput: K steps replayed from CUDA graphs, CUDA
-  events on the launching stream, barrier + max over ranks.  Each step reads a
-  fresh command buffer from a ring larger than L2 (env state stays resident, as
-  in an RL loop); L2 is flushed before the timed region.  The graphs are
-  submitted behind a short device-side spin (``torch.cuda._sleep``, before the
+* value — device-resident throughput of K control steps through
+  ``engine.rollout`` (one ``uuv_rollout_dl`` launch, the state in registers from
+  the first step to the last, the state stored every step; bit for bit K
+  ``step_batch`` calls), CUDA events on the launching stream, barrier + max over
+  ranks.  Each step reads a fresh command slot from a ring larger than L2; L2 is
+  flushed before the timed region.  ``per_path.step_batch_graph`` is the same K
+  steps as K ``step_batch`` launches replayed from CUDA graphs.  Work is
+  enqueued behind a short device-side spin (``torch.cuda._sleep``, before the
   start event), so the GPU does not idle on host submission inside the region;
   the host submission time is reported beside it.
 * e2e — the same metric through the public API with HOST buffers:
@@ -418,6 +421,7 @@ def at_scale_blocks(ctx, timer, stream, steps, gen):
     torch.cuda.empty_cache()
 
     # configs[4]: docking, train-preset DR, auto-reset, 1M envs per GPU, NCCL stats
+    last_stats = []
     env = make_env(TaskConfig(task="docking", vehicle="bluerov_heavy", level="disturbed_dr"),
                    E.SimConfig(batch_size=n), seed=0, device=dev, env_offset=rank * n)
     env.reset()
@@ -429,9 +433,10 @@ def at_scale_blocks(ctx, timer, stream, steps, gen):
             RF.substep_flops("bluerov_heavy", current=True, general=True) + RF.TASK_FLOPS,
             "configs[4]: docking task, bluerov_heavy, level disturbed_dr (train preset), "
             "auto-reset, 1,048,576 envs/GPU, rollout stats all-reduced once per rollout",
-            tail=lambda: env.rollout_stats_tensor())
-    out["cfg5_docking_1m"]["finished_per_frame"] = (
-        lambda s: s["finished"] / max(s["frames"], 1))(env.rollout_stats())
+            tail=lambda: last_stats.append(env.rollout_stats_tensor()))
+    s5 = dict(zip(("reward_sum", "finished", "success", "failure", "truncated",
+                   "metric_sum_finished", "diverged", "frames"), last_stats[-1].tolist()))
+    out["cfg5_docking_1m"]["finished_per_frame"] = s5["finished"] / max(s5["frames"], 1)
     del env, ring
     torch.cuda.empty_cache()
     return out
@@ -471,33 +476,50 @@ def run_b200(args):
         for w in range(args.warmup):
             E.step_batch(st, ring[w % n_ring])
     torch.cuda.synchronize(dev)
+    timer = DeviceTimer(dev, stream, barrier)
+    # (a) the resident rollout: ONE uuv_rollout_dl launch for the K steps, the state in
+    #     registers from the first step to the last, step t reading ring slot
+    #     (warmup + t) -- bit for bit K step_batch calls (tests/test_gpu_rollout.py)
+    start = args.warmup % n_ring
+
+    def enqueue_rollout():
+        E.rollout(st, ring, k_total, start=start)
+
+    # (b) the per-step drop-in call: CUDA graphs of K step_batch launches (uuv_step_dl),
+    #     programmatic dependent launch between consecutive steps
     graphs = capture_steps(lambda s: E.step_batch(st, ring[(args.warmup + s) % n_ring]),
                            k_total, stream)
-    timer = DeviceTimer(dev, stream, barrier)
 
-    def enqueue():
+    def enqueue_graphs():
         for g in graphs:
             g.replay()
 
-    timer.run(enqueue)  # untimed: graph upload / first-run effects, gate calibration
+    timer.run(enqueue_rollout)  # untimed: first launch, gate calibration
+    timer.run(enqueue_graphs)  # untimed: graph upload
     with ClockSampler(dev.index) as clk:
         t0 = time.perf_counter()
-        el = timer.run(enqueue)
+        el = timer.run(enqueue_rollout)
         submit_us = timer.submit_us
+        el_graph = timer.run(enqueue_graphs)
         while time.perf_counter() - t0 < 1.0:  # keep sampling clocks under the same load
-            timer.run(enqueue)
-    el_ungated = timer.run(enqueue, gate=False)  # for the record: host submission inside
+            timer.run(enqueue_rollout)
+            timer.run(enqueue_graphs)
+    el_graph_ungated = timer.run(enqueue_graphs, gate=False)  # host submission inside
     el_max = D.allreduce_max(el, dev)
+    el_graph_max = D.allreduce_max(el_graph, dev)
     frames = world * n * k_total
     value = frames / el_max
     ms_per_step = 1e3 * el_max / k_total
-    bpf = algorithmic_bytes_per_frame()
-    us_launch = el / k_total * 1e6
-    roof = RF.roofline(us_launch, n, bpf, RF.substep_flops("bluerov"))
+    us_step = el / k_total * 1e6
+    roof = RF.roofline(us_step, n, RF.rollout_frame_bytes(A_BLUEROV, len(DR_KEYS), k_total),
+                       RF.substep_flops("bluerov"))
     traffic, traffic_src = load_traffic()
-    roof.update(traffic=traffic, traffic_note=f"ncu dram bytes per launch (cold cache), "
-                f"{traffic_src}" if traffic_src else None,
-                kernel="k_step<float,1,DR,6,DM>")
+    roof.update(traffic=traffic, traffic_note=f"ncu dram bytes per frame of the dominant kernel "
+                f"(cold cache), {traffic_src}" if traffic_src else None,
+                kernel="k_rollout<float,1,DR,6,DM>")
+    roof_graph = RF.roofline(el_graph / k_total * 1e6, n, algorithmic_bytes_per_frame(),
+                             RF.substep_flops("bluerov"))
+    roof_graph["kernel"] = "k_step<float,1,DR,6,DM>"
 
     # e2e through the public API with host buffers: per-step commands from a ring of
     # 64 pinned host buffers (fresh values every step, buffers reused as a host control
@@ -563,10 +585,15 @@ def run_b200(args):
             "timing": {"l2": f"inputs larger than L2: per-step commands from a "
                              f"{n_ring * n * A_BLUEROV * 4 >> 20} MiB ring; L2 flushed before "
                              "the timed region; env state resident",
-                       "launch": "CUDA graphs of K step_batch launches (uuv_step_dl), "
-                                 "programmatic dependent launch between steps",
+                       "launch": "value: one engine.rollout launch (k_rollout) for the K steps; "
+                                 "per_path.step_batch_graph: CUDA graphs of K step_batch "
+                                 "launches (uuv_step_dl, programmatic dependent launch)",
                        "host_submit_us": submit_us, "gate_us": timer.gate_us,
-                       "us_per_step_with_submit_inside": el_ungated / k_total * 1e6},
+                       "step_batch_graph_us_per_step_submit_inside":
+                           el_graph_ungated / k_total * 1e6},
+            "per_path": {"rollout": value, "step_batch_graph": frames / el_graph_max,
+                         "step_batch_graph_ms_per_step": 1e3 * el_graph_max / k_total,
+                         "step_batch_graph_roofline": roof_graph},
             "e2e": {"value": world * n * k_total / e2e_el, "unit": "env-frames/s",
                     "h2d_bytes_per_step": n * A_BLUEROV * 4, "d2h_bytes_per_step": res.nbytes,
                     "path": e2e_path,
@@ -575,7 +602,7 @@ def run_b200(args):
                                  "launch_per_step": world * n * k_total / e2e_launch_el}},
             "roofline": roof,
             "at_scale": scale,
-            "gpu_launches": k_total,
+            "gpu_launches": 1,  # one k_rollout launch for the K steps
             "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu_baseline:

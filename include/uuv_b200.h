@@ -406,6 +406,19 @@ uuv_status uuv_state_from_dlpack(uuv_state* st, const DLTensor* const* fields, i
 uuv_status uuv_step_dl(uuv_ctx* ctx, const uuv_state* st, const DLTensor* commands,
                        int32_t substeps, double dt, void* stream);
 
+/* `steps` control steps in ONE launch with the state held in registers from the
+ * first to the last (throughput_probe, engine.py:541-564, and open-loop
+ * rollouts): step t applies slot (start + t) mod S of `commands`, a DLPack ring
+ * (S, n_envs, width) of the state's dtype -- bit for bit `steps` calls of
+ * uuv_step_dl(commands[slot]) (engine.py:465-484), state stored every step.
+ * `trace` (>= steps, 13, n_envs) or NULL receives p, q, nu after every step.
+ * `ready` (a uint32/int32 device counter) or NULL: step t waits until
+ * *ready > t, so a producer on another stream can fill the ring while the
+ * rollout runs (device-side command ring; fill slot, then raise the counter). */
+uuv_status uuv_rollout_dl(uuv_ctx* ctx, const uuv_state* st, const DLTensor* commands,
+                          int32_t start, int32_t steps, int32_t substeps, double dt,
+                          const DLTensor* trace, const DLTensor* ready, void* stream);
+
 /* uuv_reset with the mask as a DLPack tensor (n_envs,) bool/uint8, unit stride,
  * or NULL for every row (reset_envs, engine.py:487-512). */
 uuv_status uuv_reset_dl(uuv_ctx* ctx, const uuv_state* st, const DLTensor* mask,

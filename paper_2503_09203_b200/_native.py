@@ -212,6 +212,8 @@ EXPORTS = {
     "uuv_state_from_dlpack": (C.c_int, [C.POINTER(State), C.POINTER(C.c_void_p), C.c_int32]),
     "uuv_step_dl": (C.c_int, [C.c_void_p, C.POINTER(State), C.c_void_p, C.c_int32, C.c_double,
                               C.c_void_p]),
+    "uuv_rollout_dl": (C.c_int, [C.c_void_p, C.POINTER(State), C.c_void_p, C.c_int32, C.c_int32,
+                                 C.c_int32, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]),
     "uuv_reset_dl": (C.c_int, [C.c_void_p, C.POINTER(State), C.c_void_p, C.POINTER(Sampler),
                                C.c_uint64, C.c_void_p]),
     "uuv_task_step_dl": (C.c_int, [C.c_void_p, C.POINTER(State), C.POINTER(Task),

@@ -571,6 +571,159 @@ __global__ void __launch_bounds__(kBlock, HI ? kMinBHi : ((NT > 1 && sizeof(R) =
 #endif
 }
 
+// ------------------------------------------------------------------ multi-step rollout
+// T control steps of every env in ONE launch, the state in registers from the
+// first step to the last: step t applies commands slot (start + t) mod n_slots
+// of a (n_slots, n, cmd_ld) ring -- exactly step_batch(state, ring[slot]) T
+// times (engine.py:465-484), bit for bit (same substep code, same parameters):
+// frozen rows stay frozen and count steps, a non-finite substep freezes the row
+// at its last finite state.  Per launch instead of per step: the state loads and
+// the DR derivation (derive_env + sub_from_env); per step: the command row
+// (loaded one step ahead) and the state stores (every step, as step_batch
+// leaves it), plus the optional (T, 13, trace_ld) pose trace.  With `ready`
+// set, step t first waits (acquire, GPU scope) until *ready > t: a producer on
+// another stream fills the ring slot and then raises the counter -- the device-
+// side command ring of a resident stepper.
+template <typename R, int NT> struct RolloutArgs {
+  StepArgs<R, NT> step;   // hulls, state view, cmd = slot 0, cmd_ld, K, dt
+  int64_t slot_stride;    // elements between ring slots
+  int32_t n_slots, start, steps;
+  R* trace;               // (steps, 13, trace_ld) or null
+  int64_t trace_ld;
+  const uint32_t* ready;  // or null (every slot already written)
+};
+
+constexpr uint64_t kRolloutWaitNs = 10000000000ull;  // 10 s without a new command slot
+
+UUV_D uint32_t ld_acquire_gpu_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <typename R, int NT, bool DR, int AC, bool DM>
+UUV_D void rollout_env(const RolloutArgs<R, NT>& ra, int64_t i, StepIn<R>& in) {
+  const StepArgs<R, NT>& a = ra.step;
+  const StateView<R>& sv = a.sv;
+  const Hull<R>& H = a.hull[in.ty];
+  const int A = AC > 0 ? AC : H.r.n_act;
+  constexpr int NA = AC > 0 ? AC : UUV_MAX_ACT;
+  const bool has_cur = sv.cur != nullptr;
+  V3<R> cur{R(0), R(0), R(0)};
+  if (has_cur) cur = V3<R>{sv.cur[i], sv.cur[sv.ld + i], sv.cur[2 * sv.ld + i]};
+  Sub<R> s;
+  const double* jit = nullptr;
+  if (DR) {
+    EnvD e;
+    derive_env(H.d, sv.ov, sv.ld, i, sv.slot, e);
+    sub_from_env<R, DM, true, AC>(H.r, e, s);
+    if (sv.slot[UUV_OV_JITTER] >= 0) jit = sv.ov + sv.slot[UUV_OV_JITTER] * sv.ld + i;
+  }
+  uint32_t avail = 0;
+  bool stalled = false;  // the producer never raised the counter: give up, never hang
+  auto slot_row = [&](int t) {
+    const int k = (int)((ra.start + t) % ra.n_slots);
+    return a.cmd + (int64_t)k * ra.slot_stride + i * a.cmd_ld;
+  };
+  auto wait_slot = [&](int t) {
+    if (ra.ready != nullptr && (uint32_t)t >= avail) {
+      uint64_t t0;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      while ((avail = ld_acquire_gpu_u32(ra.ready)) <= (uint32_t)t) {
+        __nanosleep(100);
+        uint64_t t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        if ((int64_t)(t1 - t0) > (int64_t)kRolloutWaitNs) {
+          stalled = true;
+          return;
+        }
+      }
+    }
+  };
+  R un[UUV_MAX_ACT];
+  wait_slot(0);
+  {
+    const R* c = slot_row(0);
+#pragma unroll
+    for (int j = 0; j < UUV_MAX_ACT; ++j) un[j] = (j < NA && j < A) ? c[j] : R(0);
+  }
+  for (int t = 0; t < ra.steps && !stalled; ++t) {
+    R u[UUV_MAX_ACT];
+#pragma unroll
+    for (int j = 0; j < UUV_MAX_ACT; ++j) u[j] = clip_<R>(un[j], R(-1), R(1));
+    if (t + 1 < ra.steps) {  // the next step's command row, in flight during this step
+      if (ra.ready == nullptr || (uint32_t)(t + 1) < avail) {
+        const R* c = slot_row(t + 1);
+#pragma unroll
+        for (int j = 0; j < UUV_MAX_ACT; ++j) un[j] = (j < NA && j < A) ? c[j] : R(0);
+      }
+    }
+    if (!in.div) {
+      bool ok = true;
+      auto run = [&](auto with_jit) {
+        for (int k = 0; k < a.K; ++k) {
+          if (!substep<R, DR, false, AC, DM, decltype(with_jit)::value, true>(
+                  H.r, s, jit, sv.ld, in.px, in.py, in.pz, in.q, in.nu, in.act, u, has_cur, cur,
+                  a.dt, nullptr)) {
+            ok = false;
+            break;
+          }
+        }
+      };
+      if (DR && jit != nullptr) run(std::true_type{});
+      else run(std::false_type{});
+      store_state(sv, i, A, in.px, in.py, in.pz, in.q, in.nu, in.act);
+      if (!ok) {
+        in.div = 1;
+        sv.diverged[i] = 1;
+      }
+    }
+    in.steps += 1;
+    if (ra.trace != nullptr) {
+      R* o = ra.trace + (int64_t)t * 13 * ra.trace_ld + i;
+      const int64_t ld = ra.trace_ld;
+      o[0] = in.px; o[ld] = in.py; o[2 * ld] = in.pz;
+      o[3 * ld] = in.q.w; o[4 * ld] = in.q.x; o[5 * ld] = in.q.y; o[6 * ld] = in.q.z;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) o[(7 + k) * ld] = in.nu[k];
+    }
+    if (t + 1 < ra.steps && ra.ready != nullptr && (uint32_t)(t + 1) >= avail) {
+      wait_slot(t + 1);  // the producer had not filled slot t+1 when step t began
+      const R* c = slot_row(t + 1);
+#pragma unroll
+      for (int j = 0; j < UUV_MAX_ACT; ++j) un[j] = (j < NA && j < A) ? c[j] : R(0);
+    }
+  }
+  sv.steps[i] = in.steps;
+}
+
+template <typename R, int NT, bool DR, int AC, bool DM>
+__global__ void __launch_bounds__(kBlock, 1) k_rollout(const __grid_constant__ RolloutArgs<R, NT> ra) {
+  const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+  if (i >= ra.step.sv.n) return;
+  const StateView<R>& sv = ra.step.sv;
+  StepIn<R> in;
+  in.ty = NT > 1 ? sv.type_id[i] : 0;
+  const int A = AC > 0 ? AC : ra.step.hull[in.ty].r.n_act;
+  in.steps = sv.steps[i];
+  in.div = sv.diverged[i];
+  load_state(sv, i, A, in.px, in.py, in.pz, in.q, in.nu, in.act);
+  if constexpr (NT > 1) {
+    switch (ra.step.cls[in.ty]) {
+      case 1: rollout_env<R, NT, DR, 6, true>(ra, i, in); return;
+      case 2: rollout_env<R, NT, DR, 8, true>(ra, i, in); return;
+      case 3: rollout_env<R, NT, DR, 6, false>(ra, i, in); return;
+      case 4: rollout_env<R, NT, DR, 8, false>(ra, i, in); return;
+      case 5: rollout_env<R, NT, DR, 0, true>(ra, i, in); return;
+      case 6: rollout_env<R, NT, DR, kFinLayout, true>(ra, i, in); return;
+      case 7: rollout_env<R, NT, DR, kFinLayout, false>(ra, i, in); return;
+      default: rollout_env<R, NT, DR, 0, false>(ra, i, in); return;
+    }
+  } else {
+    rollout_env<R, NT, DR, AC, DM>(ra, i, in);
+  }
+}
+
 // ------------------------------------------------------------------ step server
 // A resident kernel that steps the batch whenever the host rings a doorbell in
 // mapped pinned memory: no launch, no stream synchronisation per step.  Each CTA
@@ -1531,6 +1684,80 @@ uuv_status dispatch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cm
             : launch_step<R, UUV_MAX_TYPES, false, 0>(ctx, st, cmd, cmd_ld, K, dt, s, pose);
 }
 
+// Multi-step rollout (k_rollout): one thread per env, no dependent-launch chain.
+struct RolloutSpec {
+  const void* cmd;
+  int64_t cmd_ld, slot_stride;
+  int32_t n_slots, start, steps;
+  void* trace;
+  int64_t trace_ld;
+  const uint32_t* ready;
+};
+
+template <typename R, int NT, bool DR, int AC, bool DM = false>
+uuv_status launch_rollout(const uuv_ctx* ctx, const uuv_state* st, const RolloutSpec& sp,
+                          int32_t K, double dt, cudaStream_t s) {
+  RolloutArgs<R, NT> ra;
+  StepArgs<R, NT>& a = ra.step;
+  fill_hulls<R, NT>(ctx, a.hull, dt / K);
+  for (int t = 0; t < NT; ++t)
+    a.cls[t] = t < (int)ctx->hulls.size() ? hull_class(ctx->hulls[t], st) : 0;
+  a.sv = make_view<R>(*st);
+  a.cmd = (const R*)sp.cmd;
+  a.cmd_ld = sp.cmd_ld;
+  a.K = K;
+  a.dt = (R)(dt / K);
+  a.early_trigger = 0;
+  a.out = HostOut{};
+  a.prefetch_ov = 0;
+  ra.slot_stride = sp.slot_stride;
+  ra.n_slots = sp.n_slots;
+  ra.start = sp.start;
+  ra.steps = sp.steps;
+  ra.trace = (R*)sp.trace;
+  ra.trace_ld = sp.trace_ld;
+  ra.ready = sp.ready;
+  UUV_REGISTER(k_rollout<R, NT, DR, AC, DM>);
+  k_rollout<R, NT, DR, AC, DM><<<(unsigned)grid_for(st->n_envs), kBlock, 0, s>>>(ra);
+  return check_launch("uuv_rollout");
+}
+
+template <typename R>
+uuv_status dispatch_rollout(const uuv_ctx* ctx, const uuv_state* st, const RolloutSpec& sp,
+                            int32_t K, double dt, cudaStream_t s) {
+  const bool dr = st->overlay != nullptr;
+  if (ctx->hulls.size() > 1)
+    return dr ? launch_rollout<R, UUV_MAX_TYPES, true, 0>(ctx, st, sp, K, dt, s)
+              : launch_rollout<R, UUV_MAX_TYPES, false, 0>(ctx, st, sp, K, dt, s);
+  const bool dm = diag_mass(ctx, st);
+  switch (act_class(ctx)) {
+    case 6:
+      if (dm)
+        return dr ? launch_rollout<R, 1, true, 6, true>(ctx, st, sp, K, dt, s)
+                  : launch_rollout<R, 1, false, 6, true>(ctx, st, sp, K, dt, s);
+      return dr ? launch_rollout<R, 1, true, 6>(ctx, st, sp, K, dt, s)
+                : launch_rollout<R, 1, false, 6>(ctx, st, sp, K, dt, s);
+    case 8:
+      if (dm)
+        return dr ? launch_rollout<R, 1, true, 8, true>(ctx, st, sp, K, dt, s)
+                  : launch_rollout<R, 1, false, 8, true>(ctx, st, sp, K, dt, s);
+      return dr ? launch_rollout<R, 1, true, 8>(ctx, st, sp, K, dt, s)
+                : launch_rollout<R, 1, false, 8>(ctx, st, sp, K, dt, s);
+    case kFinLayout:
+      if (dm)
+        return dr ? launch_rollout<R, 1, true, kFinLayout, true>(ctx, st, sp, K, dt, s)
+                  : launch_rollout<R, 1, false, kFinLayout, true>(ctx, st, sp, K, dt, s);
+      return dr ? launch_rollout<R, 1, true, kFinLayout>(ctx, st, sp, K, dt, s)
+                : launch_rollout<R, 1, false, kFinLayout>(ctx, st, sp, K, dt, s);
+    default:
+      if (dm)
+        return dr ? launch_rollout<R, 1, true, 0, true>(ctx, st, sp, K, dt, s)
+                  : launch_rollout<R, 1, false, 0, true>(ctx, st, sp, K, dt, s);
+      return dr ? launch_rollout<R, 1, true, 0>(ctx, st, sp, K, dt, s)
+                : launch_rollout<R, 1, false, 0>(ctx, st, sp, K, dt, s);
+  }
+}
+
 uuv_status check_sampler(const uuv_sampler* smp) {
   if (smp == nullptr) return fail(UUV_ERR_ARG, "null sampler");
   if (smp->n_overlay < 0 || smp->n_overlay > UUV_MAX_DRAWS)
@@ -1638,8 +1865,20 @@ uuv_status step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd, int64_
                 int32_t K, double dt, cudaStream_t s, const HostOut* out);
 template <typename R, bool POL>
 void task(bool dr, int ac, bool dm, unsigned g, cudaStream_t cs, const TaskArgs<R>& a);
+template <typename R>
+uuv_status rollout(const uuv_ctx* ctx, const uuv_state* st, const RolloutSpec& sp, int32_t K,
+                   double dt, cudaStream_t s);
 
 #if UUV_TU_STEP
+template <typename R>
+uuv_status rollout(const uuv_ctx* ctx, const uuv_state* st, const RolloutSpec& sp, int32_t K,
+                   double dt, cudaStream_t s) {
+  return dispatch_rollout<R>(ctx, st, sp, K, dt, s);
+}
+template uuv_status rollout<float>(const uuv_ctx*, const uuv_state*, const RolloutSpec&, int32_t,
+                                   double, cudaStream_t);
+template uuv_status rollout<double>(const uuv_ctx*, const uuv_state*, const RolloutSpec&, int32_t,
+                                    double, cudaStream_t);
 template <typename R>
 uuv_status step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd, int64_t cmd_ld,
                 int32_t K, double dt, cudaStream_t s, const HostOut* out) {
@@ -2485,6 +2724,57 @@ uuv_status uuv_step_dl(uuv_ctx* ctx, const uuv_state* st, const DLTensor* comman
   if ((s = dl_rows(commands, "commands", st->n_envs, cmd_width(ctx, st), st->dtype, &ld)) != UUV_OK)
     return s;
   return step_checked(ctx, st, dl_ptr(commands), ld, substeps, dt, (cudaStream_t)stream, nullptr);
+}
+
+uuv_status uuv_rollout_dl(uuv_ctx* ctx, const uuv_state* st, const DLTensor* commands,
+                          int32_t start, int32_t steps, int32_t substeps, double dt,
+                          const DLTensor* trace, const DLTensor* ready, void* stream) {
+  uuv_status s = check_state(ctx, st);
+  if (s != UUV_OK) return s;
+  if (commands == nullptr) return fail(UUV_ERR_ARG, "commands: null tensor");
+  if ((s = dl_device(commands, "commands")) != UUV_OK) return s;
+  int32_t dt_code = -1;
+  if (!dl_is_real(commands->dtype, &dt_code) || dt_code != st->dtype)
+    return fail(UUV_ERR_ARG, "commands: dtype is not the state's float%d",
+                st->dtype == UUV_F32 ? 32 : 64);
+  const int64_t n = st->n_envs, w = cmd_width(ctx, st);
+  if (commands->ndim != 3 || commands->shape[1] != n || commands->shape[2] != w)
+    return fail(UUV_ERR_SHAPE, "commands: expected shape (slots, %lld, %lld)", (long long)n,
+                (long long)w);
+  const int64_t n_slots = commands->shape[0];
+  if (n_slots < 1 || n_slots > INT32_MAX) return fail(UUV_ERR_SHAPE, "commands: no slots");
+  if (w > 1 && dl_stride(commands, 2) != 1)
+    return fail(UUV_ERR_SHAPE, "commands: column stride must be 1");
+  const int64_t cmd_ld = n > 1 ? dl_stride(commands, 1) : w;
+  const int64_t slot_stride = n_slots > 1 ? dl_stride(commands, 0) : 0;
+  if (cmd_ld < w) return fail(UUV_ERR_SHAPE, "commands: row stride < width");
+  if (steps < 0 || start < 0) return fail(UUV_ERR_ARG, "steps and start must be >= 0");
+  if (substeps < 1 || !(dt > 0)) return fail(UUV_ERR_ARG, "substeps >= 1 and dt > 0 required");
+  RolloutSpec sp{dl_ptr(commands), cmd_ld, slot_stride, (int32_t)n_slots, (int32_t)(start % n_slots),
+                 steps, nullptr, 0, nullptr};
+  if (trace != nullptr) {
+    if ((s = dl_device(trace, "trace")) != UUV_OK) return s;
+    int32_t tc = -1;
+    if (!dl_is_real(trace->dtype, &tc) || tc != st->dtype)
+      return fail(UUV_ERR_ARG, "trace: dtype is not the state's");
+    if (trace->ndim != 3 || trace->shape[0] < steps || trace->shape[1] != 13 || trace->shape[2] != n)
+      return fail(UUV_ERR_SHAPE, "trace: expected shape (>= %d, 13, %lld)", steps, (long long)n);
+    if ((n > 1 && dl_stride(trace, 2) != 1) || dl_stride(trace, 0) != 13 * dl_stride(trace, 1))
+      return fail(UUV_ERR_SHAPE, "trace: expected contiguous (steps, 13, ld) rows");
+    sp.trace = dl_ptr(trace);
+    sp.trace_ld = dl_stride(trace, 1);
+  }
+  if (ready != nullptr) {
+    if ((s = dl_device(ready, "ready")) != UUV_OK) return s;
+    if (ready->ndim < 1 || !((ready->dtype.code == kDLInt || ready->dtype.code == kDLUInt) &&
+                             ready->dtype.bits == 32))
+      return fail(UUV_ERR_ARG, "ready: expected a 32-bit integer counter");
+    sp.ready = (const uint32_t*)dl_ptr(ready);
+  }
+  if (n == 0 || steps == 0) return UUV_OK;
+  cudaStream_t cs = (cudaStream_t)stream;
+  return st->dtype == UUV_F32 ? uuv_tu::rollout<float>(ctx, st, sp, substeps, dt, cs)
+                              : uuv_tu::rollout<double>(ctx, st, sp, substeps, dt, cs);
 }
 
 uuv_status uuv_reset_dl(uuv_ctx* ctx, const uuv_state* st, const DLTensor* mask,

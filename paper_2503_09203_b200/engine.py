@@ -695,6 +695,46 @@ def step_batch(state: BatchState, commands, *, pose_out=None, out=None) -> Batch
     return state
 
 
+def rollout(state: BatchState, commands, steps: int | None = None, *, start: int = 0,
+            trace=None, ready=None) -> BatchState:
+    """``steps`` control steps in ONE kernel launch, the state held in registers
+    throughout (``uuv_rollout_dl``): bit for bit
+
+        for t in range(steps):
+            step_batch(state, commands[(start + t) % S])
+
+    ``commands``: CUDA tensor (S, N, A) -- a ring of S command slots -- or (N, A),
+    held for every step (the ``throughput_probe`` protocol, engine.py:541-564);
+    ``steps`` defaults to S.  ``trace``: optional CUDA tensor (>= steps, 13, N) of the
+    batch dtype receiving p (3), q (4), nu (6) after every step.  ``ready``: optional
+    int32 CUDA counter; step t waits until ``ready > t`` -- a producer on another
+    stream writes slot t and then raises the counter (a device-side command ring).
+    """
+    if state._server is not None:
+        raise EngineError("rollout: the batch is being served (leave the serve() block first)")
+    n, w = state.n_envs, _cmd_width(state)
+    if not (torch.is_tensor(commands) and commands.is_cuda):
+        raise EngineError("commands: rollout takes a CUDA tensor (S, N, A) or (N, A)")
+    cmd = commands if commands.dim() == 3 else commands.unsqueeze(0)
+    if cmd.dim() != 3 or tuple(cmd.shape[1:]) != (n, w):
+        raise EngineError(f"commands: expected shape (S, {n}, {w}) or ({n}, {w}), "
+                          f"got {tuple(commands.shape)}")
+    if cmd.dtype != state.dtype or cmd.device != state.device:
+        cmd = cmd.to(device=state.device, dtype=state.dtype)
+    if cmd.stride(2) != 1:
+        cmd = cmd.contiguous()
+    steps = cmd.shape[0] if steps is None else int(steps)
+    if steps < 0 or start < 0:
+        raise EngineError("steps and start must be >= 0")
+    args = [N.DLArg(cmd), N.dl(trace), N.dl(ready)]
+    status = N.load().uuv_rollout_dl(state._ctx, C.byref(state._cstate()), args[0], int(start),
+                                     steps, state.sim.substeps, state.sim.dt, args[1], args[2],
+                                     state._stream())
+    if status:
+        N.check(status, EngineError)
+    return state
+
+
 class serve:
     """Host-in-the-loop stepping through a resident step kernel (``uuv_server_*``).
 

@@ -66,6 +66,16 @@ def frame_bytes(a: float, n_dr: int = 0, current: bool = False, dtype_bytes: int
     return b
 
 
+def rollout_frame_bytes(a: int, n_dr: int = 0, steps: int = 1, current: bool = False,
+                        dtype_bytes: int = 4) -> float:
+    """k_rollout: per step the command row read and the state stored (p, q, nu, act); per
+    launch (amortised over ``steps``) the state, steps/diverged and DR record read, the
+    step counter written."""
+    per_step = dtype_bytes * a + dtype_bytes * (13 + a)
+    per_launch = dtype_bytes * (13 + a) + 5 + 8 * n_dr + 4 + (3 * dtype_bytes if current else 0)
+    return per_step + per_launch / max(steps, 1)
+
+
 def task_bytes(a: int, obs_dim: int, tracking: bool, dtype_bytes: int = 4) -> int:
     """Task layer on top of the physics: obs, reward, term/trunc, prev command r/w, dev_sum."""
     return dtype_bytes * obs_dim + dtype_bytes + 2 + 2 * dtype_bytes * a + (8 if tracking else 0)

@@ -1,0 +1,143 @@
+"""engine.rollout (uuv_rollout_dl, k_rollout): T control steps in one launch with the state in
+registers == T step_batch launches, bit for bit (same substep code, same per-env parameters).
+
+Covers the benchmarked cfg2 kernel class, K = 8, mixed fleets, fin vehicles, the generic
+layout (rotor nets), frozen/diverging rows, command rings that wrap, the pose trace, and
+the device-side command ring (a producer stream raising a ready counter)."""
+
+import numpy as np
+import pytest
+import torch
+from conftest import product_vehicle
+
+from paper_2503_09203_b200 import engine as E
+from paper_2503_09203_b200.randomization import DRParameter, Uniform, preset
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+FIELDS = ("p", "q", "nu", "act", "steps", "diverged", "episodes")
+
+
+def pair(make):
+    a, b = make(), make()
+    for k in FIELDS:
+        assert torch.equal(getattr(a, k), getattr(b, k))
+    return a, b
+
+
+def same(a, b, where=""):
+    for k in FIELDS:
+        assert torch.equal(getattr(a, k), getattr(b, k)), (where, k)
+
+
+def cfg2(n, dtype, substeps=1):
+    def make():
+        st = E.make_batch(product_vehicle("bluerov"), E.SimConfig(batch_size=n, substeps=substeps),
+                          master_seed=0, dtype=dtype)
+        spec = {k: DRParameter(k, Uniform(0.8, 1.2))
+                for k in ("damping*", "mass*", "thrust_coeff*", "volume*")}
+        E.reset_envs(st, torch.ones(n, dtype=torch.bool, device=st.device), E.spec_sampler(spec))
+        return st
+    return make
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("substeps", [1, 8])
+def test_rollout_equals_launched_steps_cfg2(dtype, substeps):
+    n, T = 4096, 37
+    a, b = pair(cfg2(n, dtype, substeps))
+    g = torch.Generator(device="cuda").manual_seed(0)
+    ring = (torch.rand((T, n, 6), device="cuda", generator=g) * 2.2 - 1.1).to(dtype)
+    ring[5, 9, 2] = float("nan")  # env 9 diverges at step 5 and stays frozen
+    for t in range(T):
+        E.step_batch(a, ring[t])
+    E.rollout(b, ring)
+    same(a, b)
+    assert bool(b.diverged[9]) and int(b.steps[0]) == T
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_rollout_ring_wraps_and_trace(dtype):
+    n, S, T, start = 1000, 5, 23, 3
+    a, b = pair(cfg2(n, dtype))
+    ring = (torch.rand((S, n, 6), device="cuda", generator=torch.Generator(
+        device="cuda").manual_seed(1)) * 2 - 1).to(dtype)
+    trace = torch.empty((T, 13, n), dtype=dtype, device="cuda")
+    want = []
+    for t in range(T):
+        E.step_batch(a, ring[(start + t) % S])
+        want.append(torch.cat([a.p, a.q, a.nu], dim=1).T.clone())
+    E.rollout(b, ring, T, start=start, trace=trace)
+    same(a, b)
+    assert torch.equal(trace, torch.stack(want))
+    # held commands (throughput_probe): (N, A) for every step
+    E.rollout(b, ring[0], 4)
+    for _ in range(4):
+        E.step_batch(a, ring[0])
+    same(a, b, "held")
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_rollout_fleet_and_generic_layouts(dtype):
+    names = ("bluerov", "bluerov_heavy", "lauv", "iauv", "hauv")
+    vehs = [product_vehicle(x) for x in names + ("rotor_relu",)]  # + the generic layout
+    counts = [300, 200, 250, 150, 100, 200]
+    n = sum(counts)
+
+    def make():
+        st = E.make_fleet_batch(vehs, counts, E.SimConfig(batch_size=n, substeps=2),
+                                master_seed=4, dtype=dtype)
+        E.reset_envs(st, np.ones(n, bool), E.spec_sampler(preset("train")))
+        return st
+
+    a, b = pair(make)
+    T = 15
+    ring = (torch.rand((T, n, a.a_max), device="cuda", generator=torch.Generator(
+        device="cuda").manual_seed(2)) * 2 - 1).to(dtype)
+    for t in range(T):
+        E.step_batch(a, ring[t])
+    E.rollout(b, ring)
+    same(a, b)
+
+
+def test_rollout_waits_for_the_device_command_ring():
+    """A producer stream fills slot t and raises `ready`; the resident rollout consumes the
+    slots as they arrive (launched first, it waits on the counter)."""
+    n, T = 2048, 12
+    a, b = pair(cfg2(n, torch.float32))
+    src = torch.rand((T, n, 6), device="cuda") * 2 - 1
+    ring = torch.zeros_like(src)
+    ready = torch.zeros(1, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    consumer, producer = torch.cuda.Stream(), torch.cuda.Stream()
+    with torch.cuda.stream(consumer):
+        E.rollout(b, ring, T, ready=ready)
+    with torch.cuda.stream(producer):
+        for t in range(T):
+            torch.cuda._sleep(20000)  # the producer is slower than the stepper
+            ring[t].copy_(src[t])
+            ready.fill_(t + 1)
+    torch.cuda.synchronize()
+    for t in range(T):
+        E.step_batch(a, src[t])
+    same(a, b)
+
+
+def test_rollout_argument_errors():
+    st = cfg2(64, torch.float32)()
+    with pytest.raises(E.EngineError, match="commands"):
+        E.rollout(st, torch.zeros((3, 64, 5), device="cuda"))
+    with pytest.raises(E.EngineError, match="commands"):
+        E.rollout(st, np.zeros((3, 64, 6)))
+    with pytest.raises(E.EngineError, match="trace"):
+        E.rollout(st, torch.zeros((3, 64, 6), device="cuda"),
+                  trace=torch.zeros((2, 13, 64), device="cuda"))
+    E.rollout(st, torch.zeros((3, 64, 6), device="cuda"), 0)  # zero steps: no-op
+    assert int(st.steps[0]) == 0
