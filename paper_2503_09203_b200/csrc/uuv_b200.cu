@@ -584,6 +584,16 @@ __global__ void __launch_bounds__(kBlock, HI ? kMinBHi : ((NT > 1 && sizeof(R) =
 // set, step t first waits (acquire, GPU scope) until *ready > t: a producer on
 // another stream fills the ring slot and then raises the counter -- the device-
 // side command ring of a resident stepper.
+// Host-side description of one rollout (shared by the translation units).
+struct RolloutSpec {
+  const void* cmd;
+  int64_t cmd_ld, slot_stride;
+  int32_t n_slots, start, steps;
+  void* trace;
+  int64_t trace_ld;
+  const uint32_t* ready;
+};
+
 template <typename R, int NT> struct RolloutArgs {
   StepArgs<R, NT> step;   // hulls, state view, cmd = slot 0, cmd_ld, K, dt
   int64_t slot_stride;    // elements between ring slots
@@ -1683,16 +1693,6 @@ uuv_status dispatch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cm
   return dr ? launch_step<R, UUV_MAX_TYPES, true, 0>(ctx, st, cmd, cmd_ld, K, dt, s, pose)
             : launch_step<R, UUV_MAX_TYPES, false, 0>(ctx, st, cmd, cmd_ld, K, dt, s, pose);
 }
-
-// Multi-step rollout (k_rollout): one thread per env, no dependent-launch chain.
-struct RolloutSpec {
-  const void* cmd;
-  int64_t cmd_ld, slot_stride;
-  int32_t n_slots, start, steps;
-  void* trace;
-  int64_t trace_ld;
-  const uint32_t* ready;
-};
 
 template <typename R, int NT, bool DR, int AC, bool DM = false>
 uuv_status launch_rollout(const uuv_ctx* ctx, const uuv_state* st, const RolloutSpec& sp,
