@@ -709,6 +709,9 @@ def rollout(state: BatchState, commands, steps: int | None = None, *, start: int
     batch dtype receiving p (3), q (4), nu (6) after every step.  ``ready``: optional
     int32 CUDA counter; step t waits until ``ready > t`` -- a producer on another
     stream writes slot t and then raises the counter (a device-side command ring).
+    The producer's kernels must already be loaded (under CUDA lazy loading a first
+    launch waits for the device, i.e. for the waiting rollout); a rollout that sees
+    no new slot for 10 s stops instead of hanging.
     """
     if state._server is not None:
         raise EngineError("rollout: the batch is being served (leave the serve() block first)")

@@ -1,6 +1,6 @@
 """Small fixed workload for ncu: a few direct launches of the step kernel.
 
-    python scripts/profile_step.py [--n 4096] [--case cfg2] [--steps 20]
+    python scripts/profile_step.py [--n 4096] [--case cfg2] [--steps 20] [--rollout 20]
 """
 
 import argparse
@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--n", type=int, default=4096)
     ap.add_argument("--case", default="cfg2")
     ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--rollout", type=int, default=0,
+                    help="after the launched steps, one engine.rollout launch of this many steps")
     args = ap.parse_args()
     if args.case.startswith("task_") or args.case == "policy":
         return task_case(args)
@@ -30,6 +32,9 @@ def main():
     cmds = torch.rand((args.n, width), device=st.device) * 2 - 1
     for _ in range(args.steps):
         E.step_batch(st, cmds)
+    if args.rollout:
+        ring = torch.rand((args.rollout, args.n, width), device=st.device) * 2 - 1
+        E.rollout(st, ring)
     torch.cuda.synchronize()
     print("ok", args.case, args.n, int(st.diverged.sum().item()))
 

@@ -250,7 +250,7 @@ def test_dlpack_state_layout_is_validated():
     f2[7] = torch.zeros(n + 1, dtype=torch.bool, device="cuda")
     assert bind(f2)[0] == 2 and "diverged" in last_error()
     f2 = list(f)
-    f2[4] = torch.zeros((3, 128), device="cuda")[:, :n].t()  # current_ned, other ld
+    f2[4] = torch.zeros((3, 256), device="cuda")[:, :n].t()  # current_ned, other ld
     assert bind(f2)[0] == 2 and "current_ned" in last_error()
 
 

@@ -104,7 +104,19 @@ def test_rollout_fleet_and_generic_layouts(dtype):
     for t in range(T):
         E.step_batch(a, ring[t])
     E.rollout(b, ring)
-    same(a, b)
+    # the mixed-fleet kernels: the same per-type code compiled into two different kernels may
+    # contract multiply-adds differently (as the per-run fleet dispatch), so the bar is the
+    # parity tolerance; counters and flags exact
+    for k in ("steps", "diverged", "episodes"):
+        assert torch.equal(getattr(a, k), getattr(b, k)), k
+    rtol, atol = (1e-5, 1e-6) if dtype == torch.float32 else (1e-12, 1e-14)
+    for k in ("p", "q", "nu", "act"):
+        x, y = getattr(a, k).double(), getattr(b, k).double()
+        scale = x.abs().amax(dim=1)
+        if k == "act":
+            scale = scale.clamp(min=100.0)
+        err = (x - y).abs().amax(dim=1)
+        assert bool((err <= rtol * scale + atol).all()), (k, float((err / scale).max()))
 
 
 def test_rollout_waits_for_the_device_command_ring():
@@ -115,8 +127,15 @@ def test_rollout_waits_for_the_device_command_ring():
     src = torch.rand((T, n, 6), device="cuda") * 2 - 1
     ring = torch.zeros_like(src)
     ready = torch.zeros(1, dtype=torch.int32, device="cuda")
-    torch.cuda.synchronize()
     consumer, producer = torch.cuda.Stream(), torch.cuda.Stream()
+    # the producer's kernels are loaded first: under CUDA lazy loading a kernel's first
+    # launch waits for the device, i.e. for the waiting rollout (it would give up after 10 s)
+    with torch.cuda.stream(producer):
+        torch.cuda._sleep(100)
+        ring[0].copy_(src[0])
+        ready.fill_(0)
+        ring[0].zero_()
+    torch.cuda.synchronize()
     with torch.cuda.stream(consumer):
         E.rollout(b, ring, T, ready=ready)
     with torch.cuda.stream(producer):
