@@ -127,9 +127,15 @@ def dist_ready(group=None) -> bool:
 
 def allreduce_sum(t: torch.Tensor, group=None) -> torch.Tensor:
     """Sum ``t`` over the process group in place (no-op when not distributed);
-    stream-ordered on the current stream for NCCL, no host synchronisation."""
+    stream-ordered on the current stream for NCCL, no host synchronisation.  A CUDA
+    tensor under gloo (the multi-rank tests on one GPU) is reduced through the host."""
     if dist_ready(group):
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.SUM, group=group)
+        if t.is_cuda and torch.distributed.get_backend(group) == "gloo":
+            h = t.cpu()
+            torch.distributed.all_reduce(h, op=torch.distributed.ReduceOp.SUM, group=group)
+            t.copy_(h)
+        else:
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.SUM, group=group)
     return t
 
 
