@@ -317,8 +317,9 @@ class DeviceTimer:
         torch.cuda.synchronize(self.dev)
         self.barrier()
         self.submit_us = sub
-        # keep the spin longer than the submission it hides (measured, with margin)
-        self.gate_us = max(self.gate_us, 3.0 * sub + 50.0)
+        # keep the spin longer than the submission it hides (measured, with margin; capped
+        # so a slow host -- or a profiler -- cannot stretch it without bound)
+        self.gate_us = min(max(self.gate_us, 3.0 * sub + 50.0), 5000.0)
         return self.e0.elapsed_time(self.e1) / 1e3
 
 

@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "uuv_task.cuh"
+#include "uuv_bulk.cuh"
 
 using namespace uuv;
 
@@ -1054,6 +1055,180 @@ UUV_D void policy_command(const TaskArgs<R>& a, int A, int od, int64_t i, const 
   }
 }
 
+// Inputs of one env's task step, loaded from global memory or a staged slab.
+template <typename R> struct TaskIn {
+  R raw[UUV_MAX_ACT];  // commands as given (unclipped; recorded in the trace)
+  R pu[UUV_MAX_ACT];   // previous clipped command (tasks/core.py:333-335)
+  R px, py, pz, nu[6], act[UUV_MAX_ACT];
+  Q4<R> q;
+  R dev;               // tracking deviation accumulator
+  V3<R> cur;
+  int32_t steps;
+  bool div, has_cur;
+};
+
+template <typename R>
+UUV_D void task_in_global(const TaskArgs<R>& a, int64_t i, bool load_cmd, TaskIn<R>& in) {
+  const StateView<R>& sv = a.sv;
+  const int A = a.hull[0].r.n_act;
+  const int64_t ld = sv.ld;
+  if (load_cmd) {  // command loads first: they are the longest-latency inputs
+    const R* crow = a.cmd + i * a.cmd_ld;
+#pragma unroll
+    for (int j = 0; j < UUV_MAX_ACT; ++j) in.raw[j] = j < A ? crow[j] : R(0);
+  }
+  in.steps = sv.steps[i];
+  in.div = sv.diverged[i] != 0;
+  load_state(sv, i, A, in.px, in.py, in.pz, in.q, in.nu, in.act);
+#pragma unroll
+  for (int j = 0; j < UUV_MAX_ACT; ++j) in.pu[j] = j < A ? a.prev_u[j * ld + i] : R(0);
+  in.dev = a.dev_sum != nullptr ? a.dev_sum[i] : R(0);
+  in.has_cur = sv.cur != nullptr;
+  in.cur = V3<R>{R(0), R(0), R(0)};
+  if (in.has_cur) in.cur = V3<R>{sv.cur[i], sv.cur[ld + i], sv.cur[2 * ld + i]};
+}
+
+// One env of VecTaskEnv.step (tasks/core.py:328-370): clip, physics (K substeps),
+// reward / termination / info, auto-reset, next observation (staged at srow),
+// state / prev_u / dev_sum stores, trace record, statistics into st.  The DR
+// record is read at (ov, ov_ld, ov_i): global memory or a staged slab.
+template <typename R, bool DR, int AC, bool DM, bool POL>
+UUV_D void task_env(const TaskArgs<R>& a, int64_t i, TaskIn<R>& in, const double* ov,
+                    int64_t ov_ld, int64_t ov_i, R* srow, double* st, bool& live) {
+  const StateView<R>& sv = a.sv;
+  const Hull<R>& H = a.hull[0];
+  const TaskR<R>& T = a.task;
+  const int A = H.r.n_act;
+  const int64_t ld = sv.ld;
+  if constexpr (POL) {
+    // the observation the last step returned, recomputed from the stored state
+    observe_row<R>(T, A, in.px, in.py, in.pz, in.q, in.nu, in.pu, in.steps, a.dt, srow, nullptr);
+    policy_command<R>(a, A, T.obs_dim, i, srow, in.raw);
+  }
+  // u = clip(commands); du = u - prev_u; prev_u = u  (tasks/core.py:329-335)
+  R u[UUV_MAX_ACT], du[UUV_MAX_ACT];
+#pragma unroll
+  for (int j = 0; j < UUV_MAX_ACT; ++j) {
+    if (j < A) {
+      u[j] = clip_<R>(in.raw[j], R(-1), R(1));
+      du[j] = u[j] - in.pu[j];
+    } else {
+      u[j] = R(0);
+      du[j] = R(0);
+    }
+  }
+  R px = in.px, py = in.py, pz = in.pz;
+  Q4<R> q = in.q;
+  R* nu = in.nu;
+  R* act = in.act;
+  bool div = in.div;
+  int32_t steps = in.steps;
+  if (!div)
+    div = physics_at<R, DR, AC, DM>(H, sv, i, ov, ov_ld, ov_i, in.has_cur, in.cur, a.K, a.dt_sub,
+                                    u, px, py, pz, q, nu, act);
+  steps += 1;
+  R dev = in.dev;
+  TaskOut<R> o;
+  task_eval<R>(T, A, px, py, pz, q, nu, du, steps, div, a.dt, &dev, o);
+  if (a.rout != nullptr) {
+    a.rout[UUV_TR_REWARD * ld + i] = o.reward;
+    a.rout[UUV_TR_POS_ERR * ld + i] = o.pos_err;
+    a.rout[UUV_TR_ATT_ERR * ld + i] = o.att_err;
+    a.rout[UUV_TR_METRIC * ld + i] = o.metric;
+    a.rout[UUV_TR_TIME * ld + i] = o.time;
+    if (T.kind == UUV_TASK_DOCKING) {
+      a.rout[UUV_TR_CONTACT_DIST * ld + i] = o.c_dist;
+      a.rout[UUV_TR_CONTACT_SPEED * ld + i] = o.c_speed;
+      a.rout[UUV_TR_CONTACT_ATT * ld + i] = o.c_att;
+    }
+  }
+  if (a.fout != nullptr) {
+    a.fout[UUV_TF_TERMINATED * ld + i] = o.terminated;
+    a.fout[UUV_TF_TRUNCATED * ld + i] = o.truncated;
+    a.fout[UUV_TF_FINISHED * ld + i] = o.finished;
+    a.fout[UUV_TF_FAILURE * ld + i] = o.failure;
+    a.fout[UUV_TF_SUCCESS * ld + i] = o.success;
+    a.fout[UUV_TF_DIVERGED * ld + i] = div;
+    a.fout[UUV_TF_CONTACT * ld + i] = o.contact;
+  }
+  if constexpr (POL) {
+    if (a.ep_ret != nullptr && a.ep_pending[i]) {  // _rollout_returns (baseline.py:116-123)
+      a.ep_ret[i] += (double)o.reward;
+      if (o.finished) {
+        a.ep_metric[i] = o.metric;
+        a.ep_success[i] = o.success;
+        a.ep_pending[i] = 0;
+      } else {
+        live = true;
+      }
+    }
+  }
+  st[UUV_ST_REWARD] += (double)o.reward;
+  st[UUV_ST_FINISHED] += o.finished;
+  st[UUV_ST_SUCCESS] += o.success;
+  st[UUV_ST_FAILURE] += o.failure;
+  st[UUV_ST_TRUNCATED] += o.truncated;
+  st[UUV_ST_METRIC_FINISHED] += o.finished ? (double)o.metric : 0.0;
+  st[UUV_ST_DIVERGED] += div;
+  st[UUV_ST_FRAMES] += 1.0;
+  if (o.finished) {
+    if (a.term_obs != nullptr)  // final observation of the ended episode
+      observe_row<R>(T, A, px, py, pz, q, nu, u, steps, a.dt, a.term_obs + i * a.obs_ld, nullptr);
+    V3<R> cur;
+    reset_env<R>(sv, i, a.smp, a.seed, px, py, pz, q, nu, cur);
+#pragma unroll
+    for (int j = 0; j < UUV_MAX_ACT; ++j) { act[j] = R(0); u[j] = R(0); }
+    steps = 0;
+    div = false;
+    dev = R(0);
+  }
+  // (the policy episode loop passes no obs buffer: its next launch recomputes
+  // the observation from the stored state)
+  if (a.obs != nullptr) observe_row<R>(T, A, px, py, pz, q, nu, u, steps, a.dt, srow, nullptr);
+  store_state(sv, i, A, px, py, pz, q, nu, act);
+  sv.steps[i] = steps;
+  sv.diverged[i] = div ? 1 : 0;
+#pragma unroll
+  for (int j = 0; j < UUV_MAX_ACT; ++j)
+    if (j < A) a.prev_u[j * ld + i] = u[j];
+  if (a.dev_sum != nullptr) a.dev_sum[i] = dev;
+  if (a.trace != nullptr) {  // rollout record (cli.py:277-287), coalesced SoA rows
+    R* tr = a.trace + i;
+    const int64_t tl = a.trace_ld;
+    tr[(UUV_TRACE_P + 0) * tl] = px;
+    tr[(UUV_TRACE_P + 1) * tl] = py;
+    tr[(UUV_TRACE_P + 2) * tl] = pz;
+    tr[(UUV_TRACE_Q + 0) * tl] = q.w;
+    tr[(UUV_TRACE_Q + 1) * tl] = q.x;
+    tr[(UUV_TRACE_Q + 2) * tl] = q.y;
+    tr[(UUV_TRACE_Q + 3) * tl] = q.z;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) tr[(UUV_TRACE_NU + k) * tl] = nu[k];
+    tr[UUV_TRACE_REWARD * tl] = o.reward;
+    tr[UUV_TRACE_T * tl] = (R)(__dmul_rn((double)steps, a.dt64));
+    for (int j = 0; j < A; ++j) tr[(UUV_TRACE_CMD + j) * tl] = in.raw[j];
+  }
+}
+
+// Deterministic CTA reduction of the per-thread statistics (fixed shuffle tree, then
+// warps in order) added to this CTA's slot.
+UUV_D void cta_stats(const double* st, double (*s_red)[UUV_ST_COUNT], double* slot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < UUV_ST_COUNT; ++k) {
+    double v = st[k];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+    if (lane == 0) s_red[warp][k] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < UUV_ST_COUNT) {
+    double v = 0.0;
+    for (int w = 0; w < kBlock / 32; ++w) v += s_red[w][threadIdx.x];
+    slot[threadIdx.x] += v;
+  }
+}
+
 template <typename R, bool DR, int AC, bool DM, bool POL = false>
 __global__ void __launch_bounds__(kBlock, MinBTask<R>::value) k_task_step(const __grid_constant__ TaskArgs<R> a) {
   __shared__ __align__(16) R s_obs[kBlock * kObsMax];
@@ -1063,130 +1238,14 @@ __global__ void __launch_bounds__(kBlock, MinBTask<R>::value) k_task_step(const 
   const int64_t row0 = (int64_t)blockIdx.x * kBlock;
   const int64_t i = row0 + threadIdx.x;
   const StateView<R>& sv = a.sv;
-  const Hull<R>& H = a.hull[0];
-  const TaskR<R>& T = a.task;
-  const int A = H.r.n_act;
-  const int od = T.obs_dim;
-  const int64_t ld = sv.ld;
+  const int od = a.task.obs_dim;
   double st[UUV_ST_COUNT];
 #pragma unroll
   for (int k = 0; k < UUV_ST_COUNT; ++k) st[k] = 0.0;
   if (i < sv.n) {
-    // u = clip(commands); du = u - prev_u; prev_u = u  (tasks/core.py:329-335)
-    R u[UUV_MAX_ACT], du[UUV_MAX_ACT], raw[UUV_MAX_ACT];
-    if constexpr (!POL) {  // command loads first: they are the longest-latency inputs
-      const R* crow = a.cmd + i * a.cmd_ld;
-#pragma unroll
-      for (int j = 0; j < UUV_MAX_ACT; ++j) raw[j] = j < A ? crow[j] : R(0);
-    }
-    int32_t steps = sv.steps[i];
-    bool div = sv.diverged[i] != 0;
-    R px, py, pz, nu[6], act[UUV_MAX_ACT];
-    Q4<R> q;
-    load_state(sv, i, A, px, py, pz, q, nu, act);
-    if constexpr (POL) {
-      // the observation the last step returned, recomputed from the stored state
-      R pu[UUV_MAX_ACT];
-#pragma unroll
-      for (int j = 0; j < UUV_MAX_ACT; ++j) pu[j] = j < A ? a.prev_u[j * ld + i] : R(0);
-      R* orow = s_obs + threadIdx.x * od;
-      observe_row<R>(T, A, px, py, pz, q, nu, pu, steps, a.dt, orow, nullptr);
-      policy_command<R>(a, A, od, i, orow, raw);
-    }
-#pragma unroll
-    for (int j = 0; j < UUV_MAX_ACT; ++j) {
-      if (j < A) {
-        u[j] = clip_<R>(raw[j], R(-1), R(1));
-        du[j] = u[j] - a.prev_u[j * ld + i];
-      } else {
-        u[j] = R(0);
-        du[j] = R(0);
-      }
-    }
-    if (!div) div = physics<R, DR, AC, DM>(H, sv, i, a.K, a.dt_sub, u, px, py, pz, q, nu, act);
-    steps += 1;
-    R dev = a.dev_sum != nullptr ? a.dev_sum[i] : R(0);
-    TaskOut<R> o;
-    task_eval<R>(T, A, px, py, pz, q, nu, du, steps, div, a.dt, &dev, o);
-    if (a.rout != nullptr) {
-      a.rout[UUV_TR_REWARD * ld + i] = o.reward;
-      a.rout[UUV_TR_POS_ERR * ld + i] = o.pos_err;
-      a.rout[UUV_TR_ATT_ERR * ld + i] = o.att_err;
-      a.rout[UUV_TR_METRIC * ld + i] = o.metric;
-      a.rout[UUV_TR_TIME * ld + i] = o.time;
-      if (T.kind == UUV_TASK_DOCKING) {
-        a.rout[UUV_TR_CONTACT_DIST * ld + i] = o.c_dist;
-        a.rout[UUV_TR_CONTACT_SPEED * ld + i] = o.c_speed;
-        a.rout[UUV_TR_CONTACT_ATT * ld + i] = o.c_att;
-      }
-    }
-    if (a.fout != nullptr) {
-      a.fout[UUV_TF_TERMINATED * ld + i] = o.terminated;
-      a.fout[UUV_TF_TRUNCATED * ld + i] = o.truncated;
-      a.fout[UUV_TF_FINISHED * ld + i] = o.finished;
-      a.fout[UUV_TF_FAILURE * ld + i] = o.failure;
-      a.fout[UUV_TF_SUCCESS * ld + i] = o.success;
-      a.fout[UUV_TF_DIVERGED * ld + i] = div;
-      a.fout[UUV_TF_CONTACT * ld + i] = o.contact;
-    }
-    if constexpr (POL) {
-      if (a.ep_ret != nullptr && a.ep_pending[i]) {  // _rollout_returns (baseline.py:116-123)
-        a.ep_ret[i] += (double)o.reward;
-        if (o.finished) {
-          a.ep_metric[i] = o.metric;
-          a.ep_success[i] = o.success;
-          a.ep_pending[i] = 0;
-        } else {
-          live = true;
-        }
-      }
-    }
-    st[UUV_ST_REWARD] = (double)o.reward;
-    st[UUV_ST_FINISHED] = o.finished;
-    st[UUV_ST_SUCCESS] = o.success;
-    st[UUV_ST_FAILURE] = o.failure;
-    st[UUV_ST_TRUNCATED] = o.truncated;
-    st[UUV_ST_METRIC_FINISHED] = o.finished ? (double)o.metric : 0.0;
-    st[UUV_ST_DIVERGED] = div;
-    st[UUV_ST_FRAMES] = 1.0;
-    R* srow = s_obs + threadIdx.x * od;
-    if (o.finished) {
-      if (a.term_obs != nullptr)  // final observation of the ended episode
-        observe_row<R>(T, A, px, py, pz, q, nu, u, steps, a.dt, a.term_obs + i * a.obs_ld, nullptr);
-      V3<R> cur;
-      reset_env<R>(sv, i, a.smp, a.seed, px, py, pz, q, nu, cur);
-#pragma unroll
-      for (int j = 0; j < UUV_MAX_ACT; ++j) { act[j] = R(0); u[j] = R(0); }
-      steps = 0;
-      div = false;
-      dev = R(0);
-    }
-    // (the policy episode loop passes no obs buffer: its next launch recomputes
-    // the observation from the stored state)
-    if (a.obs != nullptr) observe_row<R>(T, A, px, py, pz, q, nu, u, steps, a.dt, srow, nullptr);
-    store_state(sv, i, A, px, py, pz, q, nu, act);
-    sv.steps[i] = steps;
-    sv.diverged[i] = div ? 1 : 0;
-#pragma unroll
-    for (int j = 0; j < UUV_MAX_ACT; ++j)
-      if (j < A) a.prev_u[j * ld + i] = u[j];
-    if (a.dev_sum != nullptr) a.dev_sum[i] = dev;
-    if (a.trace != nullptr) {  // rollout record (cli.py:277-287), coalesced SoA rows
-      R* tr = a.trace + i;
-      const int64_t tl = a.trace_ld;
-      tr[(UUV_TRACE_P + 0) * tl] = px;
-      tr[(UUV_TRACE_P + 1) * tl] = py;
-      tr[(UUV_TRACE_P + 2) * tl] = pz;
-      tr[(UUV_TRACE_Q + 0) * tl] = q.w;
-      tr[(UUV_TRACE_Q + 1) * tl] = q.x;
-      tr[(UUV_TRACE_Q + 2) * tl] = q.y;
-      tr[(UUV_TRACE_Q + 3) * tl] = q.z;
-#pragma unroll
-      for (int k = 0; k < 6; ++k) tr[(UUV_TRACE_NU + k) * tl] = nu[k];
-      tr[UUV_TRACE_REWARD * tl] = o.reward;
-      tr[UUV_TRACE_T * tl] = (R)(__dmul_rn((double)steps, a.dt64));
-      for (int j = 0; j < A; ++j) tr[(UUV_TRACE_CMD + j) * tl] = raw[j];
-    }
+    TaskIn<R> in;
+    task_in_global<R>(a, i, !POL, in);
+    task_env<R, DR, AC, DM, POL>(a, i, in, sv.ov, sv.ld, i, s_obs + threadIdx.x * od, st, live);
   }
   if constexpr (POL) {
     if (a.ep_live != nullptr) {
@@ -1196,23 +1255,185 @@ __global__ void __launch_bounds__(kBlock, MinBTask<R>::value) k_task_step(const 
   }
   __syncthreads();
   if (a.obs != nullptr) flush_obs<R>(s_obs, a.obs, a.obs_ld, od, row0, sv.n);
-  if (a.stats != nullptr) {
-    // deterministic CTA reduction: fixed shuffle tree, then warps in order
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int k = 0; k < UUV_ST_COUNT; ++k) {
-      double v = st[k];
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
-      if (lane == 0) s_red[warp][k] = v;
-    }
-    __syncthreads();
-    if (threadIdx.x < UUV_ST_COUNT) {
-      double v = 0.0;
-      for (int w = 0; w < kBlock / 32; ++w) v += s_red[w][threadIdx.x];
-      a.stats[blockIdx.x * UUV_ST_COUNT + threadIdx.x] += v;
-    }
+  if (a.stats != nullptr) cta_stats(st, s_red, a.stats + blockIdx.x * UUV_ST_COUNT);
+}
+
+// ------------------------------------------------------------------ staged task step
+// Large batches: a persistent grid (one wave) walks 128-env tiles.  While a CTA
+// computes tile k, the TMA engine (cp.async.bulk, completion counted in bytes on
+// an mbarrier) copies tile k + grid's input rows -- state, previous command,
+// current, counters, DR record, the tile's command span -- into the other half of
+// a double-buffered shared-memory slab, so HBM reads overlap the physics instead
+// of stalling every warp at the start of its env.  Each thread reads its own
+// column (element t of every row: conflict-free); the dead input half then
+// stages the observation rows for the coalesced flush.  Same per-env code as
+// k_task_step (task_env), so results are identical.
+struct TaskSlab {   // layout of one slab half (host-computed, bytes)
+  uint32_t bytes;
+  uint32_t off_state, off_pu, off_cur, off_dev, off_steps, off_div, off_ov, off_cmd;
+  int32_t n_ov;     // staged DR-record rows (float64; the jitter rows stay in global memory)
+  int32_t cmd_bulk; // full tiles copy their command span (16-byte aligned commands)
+};
+
+// Input row r of a tile starting at env row0 with `rows` envs: global source, slab
+// offset and byte count (0 past the last row).
+template <typename R>
+UUV_D uint32_t task_row(const TaskArgs<R>& a, const TaskSlab& L, int r, int64_t row0, int rows,
+                        const char** src, uint32_t* dst) {
+  const StateView<R>& sv = a.sv;
+  const int A = a.hull[0].r.n_act;
+  const int64_t ld = sv.ld;
+  constexpr uint32_t es = sizeof(R);
+  auto rb = [&](uint32_t elem) { return ((uint32_t)rows * elem + 15u) & ~15u; };
+  if (r < 13 + A) {
+    const R* base = r < 3 ? sv.p + r * ld : r < 7 ? sv.q + (r - 3) * ld
+                  : r < 13 ? sv.nu + (r - 7) * ld : sv.act + (r - 13) * ld;
+    *src = (const char*)(base + row0);
+    *dst = L.off_state + (uint32_t)r * kBlock * es;
+    return rb(es);
   }
+  r -= 13 + A;
+  if (r < A) {
+    *src = (const char*)(a.prev_u + r * ld + row0);
+    *dst = L.off_pu + (uint32_t)r * kBlock * es;
+    return rb(es);
+  }
+  r -= A;
+  const int nc = sv.cur != nullptr ? 3 : 0;
+  if (r < nc) {
+    *src = (const char*)(sv.cur + r * ld + row0);
+    *dst = L.off_cur + (uint32_t)r * kBlock * es;
+    return rb(es);
+  }
+  r -= nc;
+  if (a.dev_sum != nullptr) {
+    if (r == 0) {
+      *src = (const char*)(a.dev_sum + row0);
+      *dst = L.off_dev;
+      return rb(es);
+    }
+    r -= 1;
+  }
+  if (r == 0) { *src = (const char*)(sv.steps + row0); *dst = L.off_steps; return rb(4); }
+  if (r == 1) { *src = (const char*)(sv.diverged + row0); *dst = L.off_div; return rb(1); }
+  r -= 2;
+  if (r < L.n_ov) {
+    *src = (const char*)(sv.ov + r * ld + row0);
+    *dst = L.off_ov + (uint32_t)r * kBlock * 8u;
+    return rb(8);
+  }
+  r -= L.n_ov;
+  if (r == 0 && L.cmd_bulk && rows == kBlock) {
+    *src = (const char*)(a.cmd + row0 * a.cmd_ld);
+    *dst = L.off_cmd;
+    return (uint32_t)(kBlock * a.cmd_ld) * es;
+  }
+  return 0;
+}
+
+template <typename R>
+UUV_D void task_issue(const TaskArgs<R>& a, const TaskSlab& L, int64_t tile, unsigned char* S,
+                      uint64_t* bar) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row0 = tile * kBlock;
+  const int rows = (int)min((int64_t)kBlock, a.sv.n - row0);
+  const int n_rows = 2 * a.hull[0].r.n_act + 13 + (a.sv.cur ? 3 : 0) + (a.dev_sum ? 1 : 0) + 2 +
+                     L.n_ov + 1;
+  if (lane == 0) {
+    uint32_t total = 0;
+    for (int r = 0; r < n_rows; ++r) {
+      const char* src;
+      uint32_t dst;
+      total += task_row(a, L, r, row0, rows, &src, &dst);
+    }
+    mbar_arrive_expect_tx(bar, total);
+  }
+  __syncwarp();
+  for (int r = lane; r < n_rows; r += 32) {
+    const char* src;
+    uint32_t dst;
+    const uint32_t bytes = task_row(a, L, r, row0, rows, &src, &dst);
+    if (bytes) bulk_g2s(S + dst, src, bytes, bar);
+  }
+}
+
+template <typename R, bool DR, int AC, bool DM>
+__global__ void __launch_bounds__(kBlock, 3)
+    k_task_step_staged(const __grid_constant__ TaskArgs<R> a, const __grid_constant__ TaskSlab L) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ double s_red[kBlock / 32][UUV_ST_COUNT];
+  const StateView<R>& sv = a.sv;
+  const int A = a.hull[0].r.n_act;
+  const int od = a.task.obs_dim;
+  const int t = threadIdx.x;
+  const int64_t n = sv.n, n_tiles = (n + kBlock - 1) / kBlock;
+  if (t == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  int64_t tile = blockIdx.x;
+  if (tile < n_tiles && t < 32) task_issue(a, L, tile, smem, &bars[0]);
+  double st[UUV_ST_COUNT];
+#pragma unroll
+  for (int k = 0; k < UUV_ST_COUNT; ++k) st[k] = 0.0;
+  uint32_t phase = 0;  // bit b: parity of slab b's next completion
+  bool live = false;
+  for (int b = 0; tile < n_tiles; tile += gridDim.x, b ^= 1) {
+    unsigned char* S = smem + b * L.bytes;
+    mbar_wait(&bars[b], (phase >> b) & 1u);
+    phase ^= 1u << b;
+    const int64_t row0 = tile * kBlock;
+    const int64_t i = row0 + t;
+    const bool on = i < n;
+    const bool full = n - row0 >= kBlock;
+    TaskIn<R> in;
+    if (on) {
+      const R* Sr = (const R*)(S + L.off_state);
+      if (L.cmd_bulk && full) {
+        const R* c = (const R*)(S + L.off_cmd) + t * a.cmd_ld;
+#pragma unroll
+        for (int j = 0; j < UUV_MAX_ACT; ++j) in.raw[j] = j < A ? c[j] : R(0);
+      } else {
+        const R* c = a.cmd + i * a.cmd_ld;
+#pragma unroll
+        for (int j = 0; j < UUV_MAX_ACT; ++j) in.raw[j] = j < A ? c[j] : R(0);
+      }
+      in.px = Sr[t]; in.py = Sr[kBlock + t]; in.pz = Sr[2 * kBlock + t];
+      in.q = Q4<R>{Sr[3 * kBlock + t], Sr[4 * kBlock + t], Sr[5 * kBlock + t], Sr[6 * kBlock + t]};
+#pragma unroll
+      for (int k = 0; k < 6; ++k) in.nu[k] = Sr[(7 + k) * kBlock + t];
+      const R* Sp = (const R*)(S + L.off_pu);
+#pragma unroll
+      for (int j = 0; j < UUV_MAX_ACT; ++j) {
+        in.act[j] = j < A ? Sr[(13 + j) * kBlock + t] : R(0);
+        in.pu[j] = j < A ? Sp[j * kBlock + t] : R(0);
+      }
+      in.has_cur = sv.cur != nullptr;
+      in.cur = V3<R>{R(0), R(0), R(0)};
+      if (in.has_cur) {
+        const R* Sc = (const R*)(S + L.off_cur);
+        in.cur = V3<R>{Sc[t], Sc[kBlock + t], Sc[2 * kBlock + t]};
+      }
+      in.dev = a.dev_sum != nullptr ? ((const R*)(S + L.off_dev))[t] : R(0);
+      in.steps = ((const int32_t*)(S + L.off_steps))[t];
+      in.div = ((const uint8_t*)(S + L.off_div))[t] != 0;
+    }
+    __syncthreads();  // slab b read by every thread; slab b^1's last flush is done
+    const int64_t nt = tile + gridDim.x;
+    if (nt < n_tiles && t < 32) task_issue(a, L, nt, smem + (b ^ 1) * L.bytes, &bars[b ^ 1]);
+    if (on) {
+      // the staged DR record (rows < n_ov) at (slab, kBlock, t); jitter stays global
+      task_env<R, DR, AC, DM, false>(a, i, in, (const double*)(S + L.off_ov), kBlock, t,
+                                     (R*)S + t * od, st, live);
+    }
+    fence_proxy_async_smem();  // the observation rows written into slab b precede its next TMA fill
+    __syncthreads();
+    if (a.obs != nullptr) flush_obs<R>((const R*)S, a.obs, a.obs_ld, od, row0, n);
+  }
+  if (a.stats != nullptr) cta_stats(st, s_red, a.stats + blockIdx.x * UUV_ST_COUNT);
 }
 
 // Task reset (mode 1: masked rows reset, prev_u / dev_sum cleared) + observe all rows.
@@ -1815,8 +2036,79 @@ void fill_task_args(const uuv_ctx* ctx, const uuv_state* st, const uuv_task* tas
   a.cmd_ld = 0;
 }
 
+// Staged task kernel (k_task_step_staged) from this batch size (float32, no policy);
+// UUV_TASK_STAGED_MIN_ENVS overrides (0 = never).
+int64_t task_staged_min_envs() {
+  static const int64_t v = [] {
+    const char* e = getenv("UUV_TASK_STAGED_MIN_ENVS");
+    return e ? (int64_t)atoll(e) : (int64_t)262144;
+  }();
+  return v;
+}
+
+// Slab layout for the staged task kernel; false if the inputs cannot be bulk-copied.
+template <typename R>
+bool task_slab(const TaskArgs<R>& a, TaskSlab& L) {
+  const StateView<R>& sv = a.sv;
+  const int A = a.hull[0].r.n_act;
+  auto al16 = [](const void* p) { return p == nullptr || ((uintptr_t)p & 15u) == 0; };
+  if (!al16(sv.p) || !al16(sv.q) || !al16(sv.nu) || !al16(sv.act) || !al16(sv.cur) ||
+      !al16(a.prev_u) || !al16(a.dev_sum) || !al16(sv.steps) || !al16(sv.diverged) ||
+      !al16(sv.ov) || (sv.ld % 32) != 0)
+    return false;
+  const uint32_t es = sizeof(R), row = kBlock * es;
+  uint32_t off = 0;
+  L.off_state = off; off += (13 + A) * row;
+  L.off_pu = off; off += A * row;
+  L.off_cur = off; if (sv.cur) off += 3 * row;
+  L.off_dev = off; if (a.dev_sum) off += row;
+  L.off_steps = off; off += kBlock * 4;
+  L.off_div = off; off += kBlock;
+  off = (off + 127u) & ~127u;
+  L.n_ov = 0;
+  if (sv.ov != nullptr) L.n_ov = sv.slot[UUV_OV_JITTER] >= 0 ? sv.slot[UUV_OV_JITTER] : sv.n_slots;
+  L.off_ov = off; off += (uint32_t)L.n_ov * kBlock * 8u;
+  L.cmd_bulk = ((uintptr_t)a.cmd & 15u) == 0 && ((a.cmd_ld * es) % 16) == 0;
+  L.off_cmd = off; if (L.cmd_bulk) off += (uint32_t)(kBlock * a.cmd_ld) * es;
+  off = std::max<uint32_t>(off, (uint32_t)(kBlock * a.task.obs_dim) * es);  // obs staging
+  L.bytes = (off + 127u) & ~127u;
+  return 2 * L.bytes <= 200u * 1024u;
+}
+
+template <typename R, bool DR, int AC, bool DM>
+bool launch_task_staged(unsigned g, cudaStream_t cs, const TaskArgs<R>& a) {
+  if (sizeof(R) != 4 || a.sv.n < task_staged_min_envs() || task_staged_min_envs() <= 0) return false;
+  TaskSlab L;
+  if (!task_slab(a, L)) return false;
+  auto kern = k_task_step_staged<R, DR, AC, DM>;
+  UUV_REGISTER(k_task_step_staged<R, DR, AC, DM>);
+  const int smem = (int)(2 * L.bytes);
+  static thread_local std::map<const void*, int> smem_set;
+  int& have = smem_set[(const void*)kern];
+  if (smem > have) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    have = smem;
+  }
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem);
+  if (per_sm < 1) return false;
+  const unsigned grid = (unsigned)std::min<int64_t>(g, (int64_t)sms * per_sm);
+  kern<<<grid, kBlock, smem, cs>>>(a, L);
+  return true;
+}
+
 template <typename R, int AC, bool DM, bool POL>
 void launch_task_dr(bool dr, unsigned g, cudaStream_t cs, const TaskArgs<R>& a) {
+  if constexpr (!POL && sizeof(R) == 4) {
+    if (dr ? launch_task_staged<R, true, AC, DM>(g, cs, a)
+           : launch_task_staged<R, false, AC, DM>(g, cs, a))
+      return;
+  }
   UUV_REGISTER(k_task_step<R, true, AC, DM, POL>);
   UUV_REGISTER(k_task_step<R, false, AC, DM, POL>);
   if (dr) k_task_step<R, true, AC, DM, POL><<<g, kBlock, 0, cs>>>(a);
