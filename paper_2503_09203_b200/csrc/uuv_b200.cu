@@ -1080,19 +1080,16 @@ UUV_D void task_in_global(const TaskArgs<R>& a, int64_t i, bool load_cmd, TaskIn
   in.steps = sv.steps[i];
   in.div = sv.diverged[i] != 0;
   load_state(sv, i, A, in.px, in.py, in.pz, in.q, in.nu, in.act);
-#pragma unroll
-  for (int j = 0; j < UUV_MAX_ACT; ++j) in.pu[j] = j < A ? a.prev_u[j * ld + i] : R(0);
-  in.dev = a.dev_sum != nullptr ? a.dev_sum[i] : R(0);
-  in.has_cur = sv.cur != nullptr;
-  in.cur = V3<R>{R(0), R(0), R(0)};
-  if (in.has_cur) in.cur = V3<R>{sv.cur[i], sv.cur[ld + i], sv.cur[2 * ld + i]};
+  (void)ld;  // prev_u, dev_sum and the current are read where they are used (task_env)
 }
 
 // One env of VecTaskEnv.step (tasks/core.py:328-370): clip, physics (K substeps),
 // reward / termination / info, auto-reset, next observation (staged at srow),
 // state / prev_u / dev_sum stores, trace record, statistics into st.  The DR
-// record is read at (ov, ov_ld, ov_i): global memory or a staged slab.
-template <typename R, bool DR, int AC, bool DM, bool POL>
+// record is read at (ov, ov_ld, ov_i): global memory or a staged slab.  STAGED:
+// previous command, current and deviation sum come from `in` (the slab); else they
+// are loaded from global memory where they are used (shorter live ranges).
+template <typename R, bool DR, int AC, bool DM, bool POL, bool STAGED = false>
 UUV_D void task_env(const TaskArgs<R>& a, int64_t i, TaskIn<R>& in, const double* ov,
                     int64_t ov_ld, int64_t ov_i, R* srow, double* st, bool& live) {
   const StateView<R>& sv = a.sv;
@@ -1102,7 +1099,10 @@ UUV_D void task_env(const TaskArgs<R>& a, int64_t i, TaskIn<R>& in, const double
   const int64_t ld = sv.ld;
   if constexpr (POL) {
     // the observation the last step returned, recomputed from the stored state
-    observe_row<R>(T, A, in.px, in.py, in.pz, in.q, in.nu, in.pu, in.steps, a.dt, srow, nullptr);
+    R pu[UUV_MAX_ACT];
+#pragma unroll
+    for (int j = 0; j < UUV_MAX_ACT; ++j) pu[j] = j < A ? a.prev_u[j * ld + i] : R(0);
+    observe_row<R>(T, A, in.px, in.py, in.pz, in.q, in.nu, pu, in.steps, a.dt, srow, nullptr);
     policy_command<R>(a, A, T.obs_dim, i, srow, in.raw);
   }
   // u = clip(commands); du = u - prev_u; prev_u = u  (tasks/core.py:329-335)
@@ -1111,7 +1111,7 @@ UUV_D void task_env(const TaskArgs<R>& a, int64_t i, TaskIn<R>& in, const double
   for (int j = 0; j < UUV_MAX_ACT; ++j) {
     if (j < A) {
       u[j] = clip_<R>(in.raw[j], R(-1), R(1));
-      du[j] = u[j] - in.pu[j];
+      du[j] = u[j] - (STAGED ? in.pu[j] : a.prev_u[j * ld + i]);
     } else {
       u[j] = R(0);
       du[j] = R(0);
@@ -1123,11 +1123,15 @@ UUV_D void task_env(const TaskArgs<R>& a, int64_t i, TaskIn<R>& in, const double
   R* act = in.act;
   bool div = in.div;
   int32_t steps = in.steps;
-  if (!div)
-    div = physics_at<R, DR, AC, DM>(H, sv, i, ov, ov_ld, ov_i, in.has_cur, in.cur, a.K, a.dt_sub,
-                                    u, px, py, pz, q, nu, act);
+  if (!div) {
+    if (STAGED)
+      div = physics_at<R, DR, AC, DM>(H, sv, i, ov, ov_ld, ov_i, in.has_cur, in.cur, a.K,
+                                      a.dt_sub, u, px, py, pz, q, nu, act);
+    else
+      div = physics<R, DR, AC, DM>(H, sv, i, a.K, a.dt_sub, u, px, py, pz, q, nu, act);
+  }
   steps += 1;
-  R dev = in.dev;
+  R dev = STAGED ? in.dev : (a.dev_sum != nullptr ? a.dev_sum[i] : R(0));
   TaskOut<R> o;
   task_eval<R>(T, A, px, py, pz, q, nu, du, steps, div, a.dt, &dev, o);
   if (a.rout != nullptr) {
@@ -1163,14 +1167,13 @@ UUV_D void task_env(const TaskArgs<R>& a, int64_t i, TaskIn<R>& in, const double
       }
     }
   }
-  st[UUV_ST_REWARD] += (double)o.reward;
-  st[UUV_ST_FINISHED] += o.finished;
-  st[UUV_ST_SUCCESS] += o.success;
-  st[UUV_ST_FAILURE] += o.failure;
-  st[UUV_ST_TRUNCATED] += o.truncated;
-  st[UUV_ST_METRIC_FINISHED] += o.finished ? (double)o.metric : 0.0;
-  st[UUV_ST_DIVERGED] += div;
-  st[UUV_ST_FRAMES] += 1.0;
+  {  // statistics: one env per thread sets them, the staged (persistent) kernel sums its envs
+    const double v[UUV_ST_COUNT] = {(double)o.reward, (double)o.finished, (double)o.success,
+                                    (double)o.failure, (double)o.truncated,
+                                    o.finished ? (double)o.metric : 0.0, (double)div, 1.0};
+#pragma unroll
+    for (int k = 0; k < UUV_ST_COUNT; ++k) st[k] = STAGED ? st[k] + v[k] : v[k];
+  }
   if (o.finished) {
     if (a.term_obs != nullptr)  // final observation of the ended episode
       observe_row<R>(T, A, px, py, pz, q, nu, u, steps, a.dt, a.term_obs + i * a.obs_ld, nullptr);
@@ -1268,93 +1271,47 @@ __global__ void __launch_bounds__(kBlock, MinBTask<R>::value) k_task_step(const 
 // column (element t of every row: conflict-free); the dead input half then
 // stages the observation rows for the coalesced flush.  Same per-env code as
 // k_task_step (task_env), so results are identical.
-struct TaskSlab {   // layout of one slab half (host-computed, bytes)
-  uint32_t bytes;
+constexpr int kSlabRows = 64;
+struct SlabRow {    // one input row of a tile: global base (env 0), slab offset, bytes per env
+  const char* g;
+  uint32_t dst, elem;
+};
+struct TaskSlab {   // layout of one slab half (host-computed)
+  uint32_t bytes;   // slab half size
+  uint32_t full_tx; // bytes one full tile copies
   uint32_t off_state, off_pu, off_cur, off_dev, off_steps, off_div, off_ov, off_cmd;
   int32_t n_ov;     // staged DR-record rows (float64; the jitter rows stay in global memory)
-  int32_t cmd_bulk; // full tiles copy their command span (16-byte aligned commands)
+  int32_t cmd_bulk; // full tiles copy their command span (the last descriptor row)
+  int32_t n_rows;
+  SlabRow row[kSlabRows];
 };
 
-// Input row r of a tile starting at env row0 with `rows` envs: global source, slab
-// offset and byte count (0 past the last row).
-template <typename R>
-UUV_D uint32_t task_row(const TaskArgs<R>& a, const TaskSlab& L, int r, int64_t row0, int rows,
-                        const char** src, uint32_t* dst) {
-  const StateView<R>& sv = a.sv;
-  const int A = a.hull[0].r.n_act;
-  const int64_t ld = sv.ld;
-  constexpr uint32_t es = sizeof(R);
-  auto rb = [&](uint32_t elem) { return ((uint32_t)rows * elem + 15u) & ~15u; };
-  if (r < 13 + A) {
-    const R* base = r < 3 ? sv.p + r * ld : r < 7 ? sv.q + (r - 3) * ld
-                  : r < 13 ? sv.nu + (r - 7) * ld : sv.act + (r - 13) * ld;
-    *src = (const char*)(base + row0);
-    *dst = L.off_state + (uint32_t)r * kBlock * es;
-    return rb(es);
-  }
-  r -= 13 + A;
-  if (r < A) {
-    *src = (const char*)(a.prev_u + r * ld + row0);
-    *dst = L.off_pu + (uint32_t)r * kBlock * es;
-    return rb(es);
-  }
-  r -= A;
-  const int nc = sv.cur != nullptr ? 3 : 0;
-  if (r < nc) {
-    *src = (const char*)(sv.cur + r * ld + row0);
-    *dst = L.off_cur + (uint32_t)r * kBlock * es;
-    return rb(es);
-  }
-  r -= nc;
-  if (a.dev_sum != nullptr) {
-    if (r == 0) {
-      *src = (const char*)(a.dev_sum + row0);
-      *dst = L.off_dev;
-      return rb(es);
-    }
-    r -= 1;
-  }
-  if (r == 0) { *src = (const char*)(sv.steps + row0); *dst = L.off_steps; return rb(4); }
-  if (r == 1) { *src = (const char*)(sv.diverged + row0); *dst = L.off_div; return rb(1); }
-  r -= 2;
-  if (r < L.n_ov) {
-    *src = (const char*)(sv.ov + r * ld + row0);
-    *dst = L.off_ov + (uint32_t)r * kBlock * 8u;
-    return rb(8);
-  }
-  r -= L.n_ov;
-  if (r == 0 && L.cmd_bulk && rows == kBlock) {
-    *src = (const char*)(a.cmd + row0 * a.cmd_ld);
-    *dst = L.off_cmd;
-    return (uint32_t)(kBlock * a.cmd_ld) * es;
-  }
-  return 0;
-}
-
+// Warp 0 fills slab S with the input rows of `tile`: lane r issues the bulk copies of
+// rows r, r + 32, ...; the byte count of a full tile is precomputed, a ragged last
+// tile sums its rows with a warp reduction.  (The command span is staged only for
+// full tiles; a ragged tile's threads read their command rows directly.)
 template <typename R>
 UUV_D void task_issue(const TaskArgs<R>& a, const TaskSlab& L, int64_t tile, unsigned char* S,
                       uint64_t* bar) {
   const int lane = threadIdx.x & 31;
   const int64_t row0 = tile * kBlock;
   const int rows = (int)min((int64_t)kBlock, a.sv.n - row0);
-  const int n_rows = 2 * a.hull[0].r.n_act + 13 + (a.sv.cur ? 3 : 0) + (a.dev_sum ? 1 : 0) + 2 +
-                     L.n_ov + 1;
-  if (lane == 0) {
-    uint32_t total = 0;
-    for (int r = 0; r < n_rows; ++r) {
-      const char* src;
-      uint32_t dst;
-      total += task_row(a, L, r, row0, rows, &src, &dst);
-    }
-    mbar_arrive_expect_tx(bar, total);
+  const bool full = rows == kBlock;
+  const int n_rows = L.n_rows - ((L.cmd_bulk && !full) ? 1 : 0);
+  auto bytes_of = [&](int r) {
+    return r == L.n_rows - 1 && L.cmd_bulk ? (uint32_t)kBlock * L.row[r].elem
+                                           : ((uint32_t)rows * L.row[r].elem + 15u) & ~15u;
+  };
+  uint32_t tx = L.full_tx;
+  if (!full) {
+    uint32_t part = 0;
+    for (int r = lane; r < n_rows; r += 32) part += bytes_of(r);
+    tx = __reduce_add_sync(0xffffffffu, part);
   }
+  if (lane == 0) mbar_arrive_expect_tx(bar, tx);
   __syncwarp();
-  for (int r = lane; r < n_rows; r += 32) {
-    const char* src;
-    uint32_t dst;
-    const uint32_t bytes = task_row(a, L, r, row0, rows, &src, &dst);
-    if (bytes) bulk_g2s(S + dst, src, bytes, bar);
-  }
+  for (int r = lane; r < n_rows; r += 32)
+    bulk_g2s(S + L.row[r].dst, L.row[r].g + row0 * L.row[r].elem, bytes_of(r), bar);
 }
 
 template <typename R, bool DR, int AC, bool DM>
@@ -1426,8 +1383,8 @@ __global__ void __launch_bounds__(kBlock, 3)
     if (nt < n_tiles && t < 32) task_issue(a, L, nt, smem + (b ^ 1) * L.bytes, &bars[b ^ 1]);
     if (on) {
       // the staged DR record (rows < n_ov) at (slab, kBlock, t); jitter stays global
-      task_env<R, DR, AC, DM, false>(a, i, in, (const double*)(S + L.off_ov), kBlock, t,
-                                     (R*)S + t * od, st, live);
+      task_env<R, DR, AC, DM, false, true>(a, i, in, (const double*)(S + L.off_ov), kBlock, t,
+                                           (R*)S + t * od, st, live);
     }
     fence_proxy_async_smem();  // the observation rows written into slab b precede its next TMA fill
     __syncthreads();
@@ -2046,7 +2003,8 @@ int64_t task_staged_min_envs() {
   return v;
 }
 
-// Slab layout for the staged task kernel; false if the inputs cannot be bulk-copied.
+// Slab layout and row descriptors for the staged task kernel; false if the inputs
+// cannot be bulk-copied (16-byte alignment) or do not fit.
 template <typename R>
 bool task_slab(const TaskArgs<R>& a, TaskSlab& L) {
   const StateView<R>& sv = a.sv;
@@ -2056,22 +2014,48 @@ bool task_slab(const TaskArgs<R>& a, TaskSlab& L) {
       !al16(a.prev_u) || !al16(a.dev_sum) || !al16(sv.steps) || !al16(sv.diverged) ||
       !al16(sv.ov) || (sv.ld % 32) != 0)
     return false;
-  const uint32_t es = sizeof(R), row = kBlock * es;
+  const uint32_t es = sizeof(R), rowb = kBlock * es;
+  const int64_t ld = sv.ld;
+  int nr = 0;
   uint32_t off = 0;
-  L.off_state = off; off += (13 + A) * row;
-  L.off_pu = off; off += A * row;
-  L.off_cur = off; if (sv.cur) off += 3 * row;
-  L.off_dev = off; if (a.dev_sum) off += row;
-  L.off_steps = off; off += kBlock * 4;
-  L.off_div = off; off += kBlock;
+  auto add = [&](const void* g, uint32_t elem) {
+    L.row[nr++] = SlabRow{(const char*)g, off, elem};
+    off += ((uint32_t)kBlock * elem + 15u) & ~15u;
+  };
+  L.off_state = off;
+  for (int r = 0; r < 3; ++r) add(sv.p + r * ld, es);
+  for (int r = 0; r < 4; ++r) add(sv.q + r * ld, es);
+  for (int r = 0; r < 6; ++r) add(sv.nu + r * ld, es);
+  for (int r = 0; r < A; ++r) add(sv.act + r * ld, es);
+  L.off_pu = off;
+  for (int r = 0; r < A; ++r) add(a.prev_u + r * ld, es);
+  L.off_cur = off;
+  if (sv.cur != nullptr)
+    for (int r = 0; r < 3; ++r) add(sv.cur + r * ld, es);
+  L.off_dev = off;
+  if (a.dev_sum != nullptr) add(a.dev_sum, es);
+  L.off_steps = off;
+  add(sv.steps, 4);
+  L.off_div = off;
+  add(sv.diverged, 1);
   off = (off + 127u) & ~127u;
   L.n_ov = 0;
   if (sv.ov != nullptr) L.n_ov = sv.slot[UUV_OV_JITTER] >= 0 ? sv.slot[UUV_OV_JITTER] : sv.n_slots;
-  L.off_ov = off; off += (uint32_t)L.n_ov * kBlock * 8u;
+  L.off_ov = off;
+  for (int r = 0; r < L.n_ov; ++r) add(sv.ov + r * ld, 8);
   L.cmd_bulk = ((uintptr_t)a.cmd & 15u) == 0 && ((a.cmd_ld * es) % 16) == 0;
-  L.off_cmd = off; if (L.cmd_bulk) off += (uint32_t)(kBlock * a.cmd_ld) * es;
+  off = (off + 127u) & ~127u;
+  L.off_cmd = off;
+  if (L.cmd_bulk) add(a.cmd, (uint32_t)(a.cmd_ld * es));
+  if (nr > kSlabRows) return false;
+  L.n_rows = nr;
+  L.full_tx = 0;
+  for (int r = 0; r < nr; ++r)
+    L.full_tx += (r == nr - 1 && L.cmd_bulk) ? (uint32_t)kBlock * L.row[r].elem
+                                              : (((uint32_t)kBlock * L.row[r].elem + 15u) & ~15u);
   off = std::max<uint32_t>(off, (uint32_t)(kBlock * a.task.obs_dim) * es);  // obs staging
   L.bytes = (off + 127u) & ~127u;
+  (void)rowb;
   return 2 * L.bytes <= 200u * 1024u;
 }
 
