@@ -23,7 +23,6 @@
 #include <vector>
 
 #include "uuv_task.cuh"
-#include "uuv_bulk.cuh"
 
 using namespace uuv;
 
@@ -1261,136 +1260,138 @@ __global__ void __launch_bounds__(kBlock, MinBTask<R>::value) k_task_step(const 
   if (a.stats != nullptr) cta_stats(st, s_red, a.stats + blockIdx.x * UUV_ST_COUNT);
 }
 
-// ------------------------------------------------------------------ staged task step
-// Large batches: a persistent grid (one wave) walks 128-env tiles.  While a CTA
-// computes tile k, the TMA engine (cp.async.bulk, completion counted in bytes on
-// an mbarrier) copies tile k + grid's input rows -- state, previous command,
-// current, counters, DR record, the tile's command span -- into the other half of
-// a double-buffered shared-memory slab, so HBM reads overlap the physics instead
-// of stalling every warp at the start of its env.  Each thread reads its own
-// column (element t of every row: conflict-free); the dead input half then
-// stages the observation rows for the coalesced flush.  Same per-env code as
-// k_task_step (task_env), so results are identical.
-constexpr int kSlabRows = 64;
-struct SlabRow {    // one input row of a tile: global base (env 0), slab offset, bytes per env
+// ------------------------------------------------------------------ pipelined task step
+// Large batches: a persistent grid where every WARP walks its own 32-env tiles and
+// software-pipelines them: before computing tile k, each lane issues asynchronous
+// copies (cp.async, LDGSTS) of its env's inputs for tile k + (warps in the grid) --
+// state, previous command, current, counters, DR record, command row -- into the
+// other half of the warp's double-buffered shared-memory slab, so the HBM reads of
+// the next tile overlap this tile's physics instead of stalling the warp at the
+// start of every env.  Lanes read only their own elements (cp.async.wait_group is
+// per thread), so the loop has no CTA barrier -- only __syncwarp around the warp's
+// observation staging, which reuses the consumed half for a coalesced flush.  Same
+// per-env code as k_task_step (task_env), so results are identical.
+constexpr int kPipeRows = 64;
+constexpr int kWarpTile = 32;
+struct PipeRow {     // one input row: global address of env 0, bytes between envs, copy size
   const char* g;
-  uint32_t dst, elem;
+  uint32_t stride;   // bytes from env i to env i + 1
+  uint32_t size;     // 4 or 8 (the diverged byte row is copied as its aligned 4-byte word)
+  uint32_t dst;      // offset of the row inside a half slab (32 elements of `size` bytes)
 };
-struct TaskSlab {   // layout of one slab half (host-computed)
-  uint32_t bytes;   // slab half size
-  uint32_t full_tx; // bytes one full tile copies
+struct TaskPipe {    // layout of one half slab of one warp (host-computed)
+  uint32_t half;     // bytes of one half
   uint32_t off_state, off_pu, off_cur, off_dev, off_steps, off_div, off_ov, off_cmd;
-  int32_t n_ov;     // staged DR-record rows (float64; the jitter rows stay in global memory)
-  int32_t cmd_bulk; // full tiles copy their command span (the last descriptor row)
   int32_t n_rows;
-  SlabRow row[kSlabRows];
+  PipeRow row[kPipeRows];
 };
 
-// Warp 0 fills slab S with the input rows of `tile`: lane r issues the bulk copies of
-// rows r, r + 32, ...; the byte count of a full tile is precomputed, a ragged last
-// tile sums its rows with a warp reduction.  (The command span is staged only for
-// full tiles; a ragged tile's threads read their command rows directly.)
+UUV_D uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+UUV_D void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+UUV_D void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+UUV_D void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+UUV_D void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
 template <typename R>
-UUV_D void task_issue(const TaskArgs<R>& a, const TaskSlab& L, int64_t tile, unsigned char* S,
-                      uint64_t* bar) {
-  const int lane = threadIdx.x & 31;
-  const int64_t row0 = tile * kBlock;
-  const int rows = (int)min((int64_t)kBlock, a.sv.n - row0);
-  const bool full = rows == kBlock;
-  const int n_rows = L.n_rows - ((L.cmd_bulk && !full) ? 1 : 0);
-  auto bytes_of = [&](int r) {
-    return r == L.n_rows - 1 && L.cmd_bulk ? (uint32_t)kBlock * L.row[r].elem
-                                           : ((uint32_t)rows * L.row[r].elem + 15u) & ~15u;
-  };
-  uint32_t tx = L.full_tx;
-  if (!full) {
-    uint32_t part = 0;
-    for (int r = lane; r < n_rows; r += 32) part += bytes_of(r);
-    tx = __reduce_add_sync(0xffffffffu, part);
+UUV_D void pipe_issue(const TaskPipe& L, int64_t i, bool on, unsigned char* H, int lane) {
+  if (on) {
+    for (int r = 0; r < L.n_rows; ++r) {
+      const PipeRow& d = L.row[r];
+      const char* src = d.g + i * d.stride;
+      unsigned char* dst = H + d.dst + lane * d.size;
+      if (d.size == 8) cp_async8(dst, src);
+      else if (d.stride == 1) cp_async4(dst, (const char*)((uintptr_t)src & ~(uintptr_t)3));
+      else cp_async4(dst, src);
+    }
   }
-  if (lane == 0) mbar_arrive_expect_tx(bar, tx);
-  __syncwarp();
-  for (int r = lane; r < n_rows; r += 32)
-    bulk_g2s(S + L.row[r].dst, L.row[r].g + row0 * L.row[r].elem, bytes_of(r), bar);
+  cp_async_commit();  // an empty group for idle lanes keeps the group count uniform
 }
 
+#ifndef UUV_MINB_PIPE
+#define UUV_MINB_PIPE 4
+#endif
 template <typename R, bool DR, int AC, bool DM>
-__global__ void __launch_bounds__(kBlock, 3)
-    k_task_step_staged(const __grid_constant__ TaskArgs<R> a, const __grid_constant__ TaskSlab L) {
+__global__ void __launch_bounds__(kBlock, UUV_MINB_PIPE)
+    k_task_step_pipe(const __grid_constant__ TaskArgs<R> a, const __grid_constant__ TaskPipe L) {
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bars[2];
   __shared__ double s_red[kBlock / 32][UUV_ST_COUNT];
   const StateView<R>& sv = a.sv;
   const int A = a.hull[0].r.n_act;
   const int od = a.task.obs_dim;
-  const int t = threadIdx.x;
-  const int64_t n = sv.n, n_tiles = (n + kBlock - 1) / kBlock;
-  if (t == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  int64_t tile = blockIdx.x;
-  if (tile < n_tiles && t < 32) task_issue(a, L, tile, smem, &bars[0]);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t n = sv.n, n_tiles = (n + kWarpTile - 1) / kWarpTile;
+  const int64_t stride = (int64_t)gridDim.x * (kBlock / 32);
+  unsigned char* W = smem + (size_t)warp * 2 * L.half;  // this warp's two halves
   double st[UUV_ST_COUNT];
 #pragma unroll
   for (int k = 0; k < UUV_ST_COUNT; ++k) st[k] = 0.0;
-  uint32_t phase = 0;  // bit b: parity of slab b's next completion
   bool live = false;
-  for (int b = 0; tile < n_tiles; tile += gridDim.x, b ^= 1) {
-    unsigned char* S = smem + b * L.bytes;
-    mbar_wait(&bars[b], (phase >> b) & 1u);
-    phase ^= 1u << b;
-    const int64_t row0 = tile * kBlock;
-    const int64_t i = row0 + t;
+  int64_t tile = (int64_t)blockIdx.x * (kBlock / 32) + warp;
+  if (tile < n_tiles) pipe_issue<R>(L, tile * kWarpTile + lane, tile * kWarpTile + lane < n, W, lane);
+  for (int b = 0; tile < n_tiles; tile += stride, b ^= 1) {
+    unsigned char* H = W + b * L.half;
+    const int64_t nt = tile + stride;
+    pipe_issue<R>(L, nt * kWarpTile + lane, nt < n_tiles && nt * kWarpTile + lane < n,
+                  W + (b ^ 1) * L.half, lane);
+    cp_async_wait_prev();  // this lane's copies of the current tile have landed
+    const int64_t row0 = tile * kWarpTile;
+    const int64_t i = row0 + lane;
     const bool on = i < n;
-    const bool full = n - row0 >= kBlock;
     TaskIn<R> in;
     if (on) {
-      const R* Sr = (const R*)(S + L.off_state);
-      if (L.cmd_bulk && full) {
-        const R* c = (const R*)(S + L.off_cmd) + t * a.cmd_ld;
-#pragma unroll
-        for (int j = 0; j < UUV_MAX_ACT; ++j) in.raw[j] = j < A ? c[j] : R(0);
-      } else {
-        const R* c = a.cmd + i * a.cmd_ld;
-#pragma unroll
-        for (int j = 0; j < UUV_MAX_ACT; ++j) in.raw[j] = j < A ? c[j] : R(0);
-      }
-      in.px = Sr[t]; in.py = Sr[kBlock + t]; in.pz = Sr[2 * kBlock + t];
-      in.q = Q4<R>{Sr[3 * kBlock + t], Sr[4 * kBlock + t], Sr[5 * kBlock + t], Sr[6 * kBlock + t]};
-#pragma unroll
-      for (int k = 0; k < 6; ++k) in.nu[k] = Sr[(7 + k) * kBlock + t];
-      const R* Sp = (const R*)(S + L.off_pu);
+      const R* Sr = (const R*)(H + L.off_state);
+      const R* Sc = (const R*)(H + L.off_cmd);
+      const R* Sp = (const R*)(H + L.off_pu);
 #pragma unroll
       for (int j = 0; j < UUV_MAX_ACT; ++j) {
-        in.act[j] = j < A ? Sr[(13 + j) * kBlock + t] : R(0);
-        in.pu[j] = j < A ? Sp[j * kBlock + t] : R(0);
+        in.raw[j] = j < A ? Sc[j * kWarpTile + lane] : R(0);
+        in.act[j] = j < A ? Sr[(13 + j) * kWarpTile + lane] : R(0);
+        in.pu[j] = j < A ? Sp[j * kWarpTile + lane] : R(0);
       }
+      in.px = Sr[lane]; in.py = Sr[kWarpTile + lane]; in.pz = Sr[2 * kWarpTile + lane];
+      in.q = Q4<R>{Sr[3 * kWarpTile + lane], Sr[4 * kWarpTile + lane], Sr[5 * kWarpTile + lane],
+                   Sr[6 * kWarpTile + lane]};
+#pragma unroll
+      for (int k = 0; k < 6; ++k) in.nu[k] = Sr[(7 + k) * kWarpTile + lane];
       in.has_cur = sv.cur != nullptr;
       in.cur = V3<R>{R(0), R(0), R(0)};
       if (in.has_cur) {
-        const R* Sc = (const R*)(S + L.off_cur);
-        in.cur = V3<R>{Sc[t], Sc[kBlock + t], Sc[2 * kBlock + t]};
+        const R* Su = (const R*)(H + L.off_cur);
+        in.cur = V3<R>{Su[lane], Su[kWarpTile + lane], Su[2 * kWarpTile + lane]};
       }
-      in.dev = a.dev_sum != nullptr ? ((const R*)(S + L.off_dev))[t] : R(0);
-      in.steps = ((const int32_t*)(S + L.off_steps))[t];
-      in.div = ((const uint8_t*)(S + L.off_div))[t] != 0;
+      in.dev = a.dev_sum != nullptr ? ((const R*)(H + L.off_dev))[lane] : R(0);
+      in.steps = ((const int32_t*)(H + L.off_steps))[lane];
+      const uint32_t dw = ((const uint32_t*)(H + L.off_div))[lane];
+      in.div = ((dw >> (8 * (uint32_t)(((uintptr_t)(sv.diverged + i)) & 3u))) & 0xffu) != 0;
     }
-    __syncthreads();  // slab b read by every thread; slab b^1's last flush is done
-    const int64_t nt = tile + gridDim.x;
-    if (nt < n_tiles && t < 32) task_issue(a, L, nt, smem + (b ^ 1) * L.bytes, &bars[b ^ 1]);
-    if (on) {
-      // the staged DR record (rows < n_ov) at (slab, kBlock, t); jitter stays global
-      task_env<R, DR, AC, DM, false, true>(a, i, in, (const double*)(S + L.off_ov), kBlock, t,
-                                           (R*)S + t * od, st, live);
+    __syncwarp();  // every lane has read its inputs: the half may now stage observations
+    if (on)
+      task_env<R, DR, AC, DM, false, true>(a, i, in, (const double*)(H + L.off_ov), kWarpTile,
+                                           lane, (R*)H + lane * od, st, live);
+    __syncwarp();
+    if (a.obs != nullptr) {  // the warp's rows are one contiguous span of the (n, od) obs
+      const int rows = (int)min((int64_t)kWarpTile, n - row0);
+      const R* src = (const R*)H;
+      if (a.obs_ld == od) {
+        R* dst = a.obs + row0 * od;
+        for (int e = lane; e < rows * od; e += 32) dst[e] = src[e];
+      } else {
+        for (int e = lane; e < rows * od; e += 32) {
+          const int r = e / od, c = e - r * od;
+          a.obs[(row0 + r) * a.obs_ld + c] = src[e];
+        }
+      }
     }
-    fence_proxy_async_smem();  // the observation rows written into slab b precede its next TMA fill
-    __syncthreads();
-    if (a.obs != nullptr) flush_obs<R>((const R*)S, a.obs, a.obs_ld, od, row0, n);
+    __syncwarp();  // the half is read before it receives the tile after next
   }
-  if (a.stats != nullptr) cta_stats(st, s_red, a.stats + blockIdx.x * UUV_ST_COUNT);
+  if (a.stats != nullptr) {
+    __syncthreads();
+    cta_stats(st, s_red, a.stats + blockIdx.x * UUV_ST_COUNT);
+  }
 }
 
 // Task reset (mode 1: masked rows reset, prev_u / dev_sum cleared) + observe all rows.
@@ -1993,80 +1994,71 @@ void fill_task_args(const uuv_ctx* ctx, const uuv_state* st, const uuv_task* tas
   a.cmd_ld = 0;
 }
 
-// Staged task kernel (k_task_step_staged) from this batch size (float32, no policy);
-// UUV_TASK_STAGED_MIN_ENVS overrides (0 = never).
-int64_t task_staged_min_envs() {
+// Pipelined task kernel (k_task_step_pipe) from this batch size (float32, no policy);
+// UUV_TASK_PIPE_MIN_ENVS overrides (0 = never).
+int64_t task_pipe_min_envs() {
   static const int64_t v = [] {
-    const char* e = getenv("UUV_TASK_STAGED_MIN_ENVS");
+    const char* e = getenv("UUV_TASK_PIPE_MIN_ENVS");
     return e ? (int64_t)atoll(e) : (int64_t)262144;
   }();
   return v;
 }
 
-// Slab layout and row descriptors for the staged task kernel; false if the inputs
-// cannot be bulk-copied (16-byte alignment) or do not fit.
+// Half-slab layout and row descriptors of the pipelined task kernel.
 template <typename R>
-bool task_slab(const TaskArgs<R>& a, TaskSlab& L) {
+bool task_pipe(const TaskArgs<R>& a, TaskPipe& L) {
   const StateView<R>& sv = a.sv;
   const int A = a.hull[0].r.n_act;
-  auto al16 = [](const void* p) { return p == nullptr || ((uintptr_t)p & 15u) == 0; };
-  if (!al16(sv.p) || !al16(sv.q) || !al16(sv.nu) || !al16(sv.act) || !al16(sv.cur) ||
-      !al16(a.prev_u) || !al16(a.dev_sum) || !al16(sv.steps) || !al16(sv.diverged) ||
-      !al16(sv.ov) || (sv.ld % 32) != 0)
-    return false;
-  const uint32_t es = sizeof(R), rowb = kBlock * es;
+  const uint32_t es = sizeof(R);
   const int64_t ld = sv.ld;
   int nr = 0;
   uint32_t off = 0;
-  auto add = [&](const void* g, uint32_t elem) {
-    L.row[nr++] = SlabRow{(const char*)g, off, elem};
-    off += ((uint32_t)kBlock * elem + 15u) & ~15u;
+  auto add = [&](const void* g, uint32_t stride, uint32_t size) {
+    if (nr < kPipeRows) L.row[nr] = PipeRow{(const char*)g, stride, size, off};
+    ++nr;
+    off += kWarpTile * size;
   };
   L.off_state = off;
-  for (int r = 0; r < 3; ++r) add(sv.p + r * ld, es);
-  for (int r = 0; r < 4; ++r) add(sv.q + r * ld, es);
-  for (int r = 0; r < 6; ++r) add(sv.nu + r * ld, es);
-  for (int r = 0; r < A; ++r) add(sv.act + r * ld, es);
+  for (int r = 0; r < 3; ++r) add(sv.p + r * ld, es, es);
+  for (int r = 0; r < 4; ++r) add(sv.q + r * ld, es, es);
+  for (int r = 0; r < 6; ++r) add(sv.nu + r * ld, es, es);
+  for (int r = 0; r < A; ++r) add(sv.act + r * ld, es, es);
   L.off_pu = off;
-  for (int r = 0; r < A; ++r) add(a.prev_u + r * ld, es);
+  for (int r = 0; r < A; ++r) add(a.prev_u + r * ld, es, es);
+  L.off_cmd = off;
+  for (int r = 0; r < A; ++r) add(a.cmd + r, (uint32_t)(a.cmd_ld * es), es);
   L.off_cur = off;
   if (sv.cur != nullptr)
-    for (int r = 0; r < 3; ++r) add(sv.cur + r * ld, es);
+    for (int r = 0; r < 3; ++r) add(sv.cur + r * ld, es, es);
   L.off_dev = off;
-  if (a.dev_sum != nullptr) add(a.dev_sum, es);
+  if (a.dev_sum != nullptr) add(a.dev_sum, es, es);
   L.off_steps = off;
-  add(sv.steps, 4);
+  add(sv.steps, 4, 4);
   L.off_div = off;
-  add(sv.diverged, 1);
-  off = (off + 127u) & ~127u;
-  L.n_ov = 0;
-  if (sv.ov != nullptr) L.n_ov = sv.slot[UUV_OV_JITTER] >= 0 ? sv.slot[UUV_OV_JITTER] : sv.n_slots;
+  add(sv.diverged, 1, 4);
+  const int n_ov = sv.ov == nullptr ? 0
+                   : (sv.slot[UUV_OV_JITTER] >= 0 ? sv.slot[UUV_OV_JITTER] : sv.n_slots);
+  off = (off + 7u) & ~7u;
   L.off_ov = off;
-  for (int r = 0; r < L.n_ov; ++r) add(sv.ov + r * ld, 8);
-  L.cmd_bulk = ((uintptr_t)a.cmd & 15u) == 0 && ((a.cmd_ld * es) % 16) == 0;
-  off = (off + 127u) & ~127u;
-  L.off_cmd = off;
-  if (L.cmd_bulk) add(a.cmd, (uint32_t)(a.cmd_ld * es));
-  if (nr > kSlabRows) return false;
+  for (int r = 0; r < n_ov; ++r) add(sv.ov + r * ld, 8, 8);
+  if (nr > kPipeRows) return false;
   L.n_rows = nr;
-  L.full_tx = 0;
+  off = std::max<uint32_t>(off, (uint32_t)(kWarpTile * a.task.obs_dim) * es);  // obs staging
+  L.half = (off + 127u) & ~127u;
+  // 4-byte elements need 4-byte aligned rows; the float64 record 8-byte aligned
   for (int r = 0; r < nr; ++r)
-    L.full_tx += (r == nr - 1 && L.cmd_bulk) ? (uint32_t)kBlock * L.row[r].elem
-                                              : (((uint32_t)kBlock * L.row[r].elem + 15u) & ~15u);
-  off = std::max<uint32_t>(off, (uint32_t)(kBlock * a.task.obs_dim) * es);  // obs staging
-  L.bytes = (off + 127u) & ~127u;
-  (void)rowb;
-  return 2 * L.bytes <= 200u * 1024u;
+    if (((uintptr_t)L.row[r].g % L.row[r].size) != 0 && L.row[r].stride != 1) return false;
+  return true;
 }
 
 template <typename R, bool DR, int AC, bool DM>
-bool launch_task_staged(unsigned g, cudaStream_t cs, const TaskArgs<R>& a) {
-  if (sizeof(R) != 4 || a.sv.n < task_staged_min_envs() || task_staged_min_envs() <= 0) return false;
-  TaskSlab L;
-  if (!task_slab(a, L)) return false;
-  auto kern = k_task_step_staged<R, DR, AC, DM>;
-  UUV_REGISTER(k_task_step_staged<R, DR, AC, DM>);
-  const int smem = (int)(2 * L.bytes);
+bool launch_task_pipe(unsigned g, cudaStream_t cs, const TaskArgs<R>& a) {
+  if (sizeof(R) != 4 || task_pipe_min_envs() <= 0 || a.sv.n < task_pipe_min_envs()) return false;
+  TaskPipe L;
+  if (!task_pipe(a, L)) return false;
+  auto kern = k_task_step_pipe<R, DR, AC, DM>;
+  UUV_REGISTER(k_task_step_pipe<R, DR, AC, DM>);
+  const int smem = (int)(2 * L.half * (kBlock / 32));
   static thread_local std::map<const void*, int> smem_set;
   int& have = smem_set[(const void*)kern];
   if (smem > have) {
@@ -2089,8 +2081,8 @@ bool launch_task_staged(unsigned g, cudaStream_t cs, const TaskArgs<R>& a) {
 template <typename R, int AC, bool DM, bool POL>
 void launch_task_dr(bool dr, unsigned g, cudaStream_t cs, const TaskArgs<R>& a) {
   if constexpr (!POL && sizeof(R) == 4) {
-    if (dr ? launch_task_staged<R, true, AC, DM>(g, cs, a)
-           : launch_task_staged<R, false, AC, DM>(g, cs, a))
+    if (dr ? launch_task_pipe<R, true, AC, DM>(g, cs, a)
+           : launch_task_pipe<R, false, AC, DM>(g, cs, a))
       return;
   }
   UUV_REGISTER(k_task_step<R, true, AC, DM, POL>);

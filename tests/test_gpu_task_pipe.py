@@ -1,9 +1,9 @@
-"""The staged task kernel (k_task_step_staged: persistent grid, TMA bulk copies of the next
-128-env tile into a double-buffered shared-memory slab) == the per-env kernel (k_task_step),
-bit for bit: the same per-env code (task_env) on staged inputs.  The staged kernel serves
-float32 batches from UUV_TASK_STAGED_MIN_ENVS envs (default 262,144); a subprocess with the
-threshold at 1 runs it on small batches with ragged last tiles, auto-resets, DR, currents
-and every task kind."""
+"""The pipelined task kernel (k_task_step_pipe: persistent grid, every warp prefetching its
+next 32-env tile with cp.async into a double-buffered shared-memory slab) == the per-env
+kernel (k_task_step), bit for bit: the same per-env code (task_env) on staged inputs.  The
+pipelined kernel serves float32 batches from UUV_TASK_PIPE_MIN_ENVS envs (default 262,144);
+a subprocess with the threshold at 1 runs it on small batches with ragged last tiles,
+auto-resets, DR, currents and every task kind."""
 
 import os
 import subprocess
@@ -49,19 +49,19 @@ np.savez(sys.argv[2], **out)
 
 def run(tmp_path, threshold):
     path = tmp_path / f"out_{threshold}.npz"
-    env = dict(os.environ, UUV_TASK_STAGED_MIN_ENVS=str(threshold))
+    env = dict(os.environ, UUV_TASK_PIPE_MIN_ENVS=str(threshold))
     r = subprocess.run([sys.executable, "-c", RUN, ROOT, str(path)], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     return np.load(path)
 
 
-def test_staged_task_kernel_equals_per_env_kernel(tmp_path):
+def test_pipelined_task_kernel_equals_per_env_kernel(tmp_path):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    staged, plain = run(tmp_path, 1), run(tmp_path, 0)
-    assert set(staged.files) == set(plain.files)
+    piped, plain = run(tmp_path, 1), run(tmp_path, 0)
+    assert set(piped.files) == set(plain.files)
     for k in plain.files:
-        assert np.array_equal(staged[k], plain[k], equal_nan=True), k
+        assert np.array_equal(piped[k], plain[k], equal_nan=True), k
     # auto-resets happened (episode_length 7 over 20 steps)
     assert plain["docking_bluerov_heavy_episodes"].max() >= 2
