@@ -1000,6 +1000,7 @@ template <typename R> struct TaskArgs {
   int32_t ep_t;
   const uint8_t* mask;  // task reset only
   int32_t mode;         // task reset kernel: 0 observe only, 1 reset masked then observe
+  int32_t prefetch;     // batch beyond L2: hint the late-read rows into L2 at kernel entry
 };
 
 // Write the CTA's staged observation rows out with coalesced stores.
@@ -1244,6 +1245,18 @@ __global__ void __launch_bounds__(kBlock, MinBTask<R>::value) k_task_step(const 
   double st[UUV_ST_COUNT];
 #pragma unroll
   for (int k = 0; k < UUV_ST_COUNT; ++k) st[k] = 0.0;
+  if (a.prefetch && i < sv.n) {
+    // rows read only after the diverged-flag branch (DR record, current) or late
+    // (previous command, deviation sum): start their DRAM reads into L2 now, so
+    // those loads hit L2 instead of adding a second DRAM round trip per env
+    prefetch_overlay_l2(sv, i);
+    const int64_t ld = sv.ld;
+    if (sv.cur != nullptr)
+      for (int c = 0; c < 3; ++c) asm volatile("prefetch.global.L2 [%0];" ::"l"(sv.cur + c * ld + i));
+    for (int j = 0; j < a.hull[0].r.n_act; ++j)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.prev_u + j * ld + i));
+    if (a.dev_sum != nullptr) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.dev_sum + i));
+  }
   if (i < sv.n) {
     TaskIn<R> in;
     task_in_global<R>(a, i, !POL, in);
@@ -1258,140 +1271,6 @@ __global__ void __launch_bounds__(kBlock, MinBTask<R>::value) k_task_step(const 
   __syncthreads();
   if (a.obs != nullptr) flush_obs<R>(s_obs, a.obs, a.obs_ld, od, row0, sv.n);
   if (a.stats != nullptr) cta_stats(st, s_red, a.stats + blockIdx.x * UUV_ST_COUNT);
-}
-
-// ------------------------------------------------------------------ pipelined task step
-// Large batches: a persistent grid where every WARP walks its own 32-env tiles and
-// software-pipelines them: before computing tile k, each lane issues asynchronous
-// copies (cp.async, LDGSTS) of its env's inputs for tile k + (warps in the grid) --
-// state, previous command, current, counters, DR record, command row -- into the
-// other half of the warp's double-buffered shared-memory slab, so the HBM reads of
-// the next tile overlap this tile's physics instead of stalling the warp at the
-// start of every env.  Lanes read only their own elements (cp.async.wait_group is
-// per thread), so the loop has no CTA barrier -- only __syncwarp around the warp's
-// observation staging, which reuses the consumed half for a coalesced flush.  Same
-// per-env code as k_task_step (task_env), so results are identical.
-constexpr int kPipeRows = 64;
-constexpr int kWarpTile = 32;
-struct PipeRow {     // one input row: global address of env 0, bytes between envs, copy size
-  const char* g;
-  uint32_t stride;   // bytes from env i to env i + 1
-  uint32_t size;     // 4 or 8 (the diverged byte row is copied as its aligned 4-byte word)
-  uint32_t dst;      // offset of the row inside a half slab (32 elements of `size` bytes)
-};
-struct TaskPipe {    // layout of one half slab of one warp (host-computed)
-  uint32_t half;     // bytes of one half
-  uint32_t off_state, off_pu, off_cur, off_dev, off_steps, off_div, off_ov, off_cmd;
-  int32_t n_rows;
-  PipeRow row[kPipeRows];
-};
-
-UUV_D uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-UUV_D void cp_async4(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-UUV_D void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-UUV_D void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-UUV_D void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-
-template <typename R>
-UUV_D void pipe_issue(const TaskPipe& L, int64_t i, bool on, unsigned char* H, int lane) {
-  if (on) {
-    for (int r = 0; r < L.n_rows; ++r) {
-      const PipeRow& d = L.row[r];
-      const char* src = d.g + i * d.stride;
-      unsigned char* dst = H + d.dst + lane * d.size;
-      if (d.size == 8) cp_async8(dst, src);
-      else if (d.stride == 1) cp_async4(dst, (const char*)((uintptr_t)src & ~(uintptr_t)3));
-      else cp_async4(dst, src);
-    }
-  }
-  cp_async_commit();  // an empty group for idle lanes keeps the group count uniform
-}
-
-#ifndef UUV_MINB_PIPE
-#define UUV_MINB_PIPE 4
-#endif
-template <typename R, bool DR, int AC, bool DM>
-__global__ void __launch_bounds__(kBlock, UUV_MINB_PIPE)
-    k_task_step_pipe(const __grid_constant__ TaskArgs<R> a, const __grid_constant__ TaskPipe L) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ double s_red[kBlock / 32][UUV_ST_COUNT];
-  const StateView<R>& sv = a.sv;
-  const int A = a.hull[0].r.n_act;
-  const int od = a.task.obs_dim;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t n = sv.n, n_tiles = (n + kWarpTile - 1) / kWarpTile;
-  const int64_t stride = (int64_t)gridDim.x * (kBlock / 32);
-  unsigned char* W = smem + (size_t)warp * 2 * L.half;  // this warp's two halves
-  double st[UUV_ST_COUNT];
-#pragma unroll
-  for (int k = 0; k < UUV_ST_COUNT; ++k) st[k] = 0.0;
-  bool live = false;
-  int64_t tile = (int64_t)blockIdx.x * (kBlock / 32) + warp;
-  if (tile < n_tiles) pipe_issue<R>(L, tile * kWarpTile + lane, tile * kWarpTile + lane < n, W, lane);
-  for (int b = 0; tile < n_tiles; tile += stride, b ^= 1) {
-    unsigned char* H = W + b * L.half;
-    const int64_t nt = tile + stride;
-    pipe_issue<R>(L, nt * kWarpTile + lane, nt < n_tiles && nt * kWarpTile + lane < n,
-                  W + (b ^ 1) * L.half, lane);
-    cp_async_wait_prev();  // this lane's copies of the current tile have landed
-    const int64_t row0 = tile * kWarpTile;
-    const int64_t i = row0 + lane;
-    const bool on = i < n;
-    TaskIn<R> in;
-    if (on) {
-      const R* Sr = (const R*)(H + L.off_state);
-      const R* Sc = (const R*)(H + L.off_cmd);
-      const R* Sp = (const R*)(H + L.off_pu);
-#pragma unroll
-      for (int j = 0; j < UUV_MAX_ACT; ++j) {
-        in.raw[j] = j < A ? Sc[j * kWarpTile + lane] : R(0);
-        in.act[j] = j < A ? Sr[(13 + j) * kWarpTile + lane] : R(0);
-        in.pu[j] = j < A ? Sp[j * kWarpTile + lane] : R(0);
-      }
-      in.px = Sr[lane]; in.py = Sr[kWarpTile + lane]; in.pz = Sr[2 * kWarpTile + lane];
-      in.q = Q4<R>{Sr[3 * kWarpTile + lane], Sr[4 * kWarpTile + lane], Sr[5 * kWarpTile + lane],
-                   Sr[6 * kWarpTile + lane]};
-#pragma unroll
-      for (int k = 0; k < 6; ++k) in.nu[k] = Sr[(7 + k) * kWarpTile + lane];
-      in.has_cur = sv.cur != nullptr;
-      in.cur = V3<R>{R(0), R(0), R(0)};
-      if (in.has_cur) {
-        const R* Su = (const R*)(H + L.off_cur);
-        in.cur = V3<R>{Su[lane], Su[kWarpTile + lane], Su[2 * kWarpTile + lane]};
-      }
-      in.dev = a.dev_sum != nullptr ? ((const R*)(H + L.off_dev))[lane] : R(0);
-      in.steps = ((const int32_t*)(H + L.off_steps))[lane];
-      const uint32_t dw = ((const uint32_t*)(H + L.off_div))[lane];
-      in.div = ((dw >> (8 * (uint32_t)(((uintptr_t)(sv.diverged + i)) & 3u))) & 0xffu) != 0;
-    }
-    __syncwarp();  // every lane has read its inputs: the half may now stage observations
-    if (on)
-      task_env<R, DR, AC, DM, false, true>(a, i, in, (const double*)(H + L.off_ov), kWarpTile,
-                                           lane, (R*)H + lane * od, st, live);
-    __syncwarp();
-    if (a.obs != nullptr) {  // the warp's rows are one contiguous span of the (n, od) obs
-      const int rows = (int)min((int64_t)kWarpTile, n - row0);
-      const R* src = (const R*)H;
-      if (a.obs_ld == od) {
-        R* dst = a.obs + row0 * od;
-        for (int e = lane; e < rows * od; e += 32) dst[e] = src[e];
-      } else {
-        for (int e = lane; e < rows * od; e += 32) {
-          const int r = e / od, c = e - r * od;
-          a.obs[(row0 + r) * a.obs_ld + c] = src[e];
-        }
-      }
-    }
-    __syncwarp();  // the half is read before it receives the tile after next
-  }
-  if (a.stats != nullptr) {
-    __syncthreads();
-    cta_stats(st, s_red, a.stats + blockIdx.x * UUV_ST_COUNT);
-  }
 }
 
 // Task reset (mode 1: masked rows reset, prev_u / dev_sum cleared) + observe all rows.
@@ -1992,99 +1871,11 @@ void fill_task_args(const uuv_ctx* ctx, const uuv_state* st, const uuv_task* tas
   a.mode = 0;
   a.cmd = nullptr;
   a.cmd_ld = 0;
-}
-
-// Pipelined task kernel (k_task_step_pipe) from this batch size (float32, no policy);
-// UUV_TASK_PIPE_MIN_ENVS overrides (0 = never).
-int64_t task_pipe_min_envs() {
-  static const int64_t v = [] {
-    const char* e = getenv("UUV_TASK_PIPE_MIN_ENVS");
-    return e ? (int64_t)atoll(e) : (int64_t)262144;
-  }();
-  return v;
-}
-
-// Half-slab layout and row descriptors of the pipelined task kernel.
-template <typename R>
-bool task_pipe(const TaskArgs<R>& a, TaskPipe& L) {
-  const StateView<R>& sv = a.sv;
-  const int A = a.hull[0].r.n_act;
-  const uint32_t es = sizeof(R);
-  const int64_t ld = sv.ld;
-  int nr = 0;
-  uint32_t off = 0;
-  auto add = [&](const void* g, uint32_t stride, uint32_t size) {
-    if (nr < kPipeRows) L.row[nr] = PipeRow{(const char*)g, stride, size, off};
-    ++nr;
-    off += kWarpTile * size;
-  };
-  L.off_state = off;
-  for (int r = 0; r < 3; ++r) add(sv.p + r * ld, es, es);
-  for (int r = 0; r < 4; ++r) add(sv.q + r * ld, es, es);
-  for (int r = 0; r < 6; ++r) add(sv.nu + r * ld, es, es);
-  for (int r = 0; r < A; ++r) add(sv.act + r * ld, es, es);
-  L.off_pu = off;
-  for (int r = 0; r < A; ++r) add(a.prev_u + r * ld, es, es);
-  L.off_cmd = off;
-  for (int r = 0; r < A; ++r) add(a.cmd + r, (uint32_t)(a.cmd_ld * es), es);
-  L.off_cur = off;
-  if (sv.cur != nullptr)
-    for (int r = 0; r < 3; ++r) add(sv.cur + r * ld, es, es);
-  L.off_dev = off;
-  if (a.dev_sum != nullptr) add(a.dev_sum, es, es);
-  L.off_steps = off;
-  add(sv.steps, 4, 4);
-  L.off_div = off;
-  add(sv.diverged, 1, 4);
-  const int n_ov = sv.ov == nullptr ? 0
-                   : (sv.slot[UUV_OV_JITTER] >= 0 ? sv.slot[UUV_OV_JITTER] : sv.n_slots);
-  off = (off + 7u) & ~7u;
-  L.off_ov = off;
-  for (int r = 0; r < n_ov; ++r) add(sv.ov + r * ld, 8, 8);
-  if (nr > kPipeRows) return false;
-  L.n_rows = nr;
-  off = std::max<uint32_t>(off, (uint32_t)(kWarpTile * a.task.obs_dim) * es);  // obs staging
-  L.half = (off + 127u) & ~127u;
-  // 4-byte elements need 4-byte aligned rows; the float64 record 8-byte aligned
-  for (int r = 0; r < nr; ++r)
-    if (((uintptr_t)L.row[r].g % L.row[r].size) != 0 && L.row[r].stride != 1) return false;
-  return true;
-}
-
-template <typename R, bool DR, int AC, bool DM>
-bool launch_task_pipe(unsigned g, cudaStream_t cs, const TaskArgs<R>& a) {
-  if (sizeof(R) != 4 || task_pipe_min_envs() <= 0 || a.sv.n < task_pipe_min_envs()) return false;
-  TaskPipe L;
-  if (!task_pipe(a, L)) return false;
-  auto kern = k_task_step_pipe<R, DR, AC, DM>;
-  UUV_REGISTER(k_task_step_pipe<R, DR, AC, DM>);
-  const int smem = (int)(2 * L.half * (kBlock / 32));
-  static thread_local std::map<const void*, int> smem_set;
-  int& have = smem_set[(const void*)kern];
-  if (smem > have) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
-      cudaGetLastError();
-      return false;
-    }
-    have = smem;
-  }
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem);
-  if (per_sm < 1) return false;
-  const unsigned grid = (unsigned)std::min<int64_t>(g, (int64_t)sms * per_sm);
-  kern<<<grid, kBlock, smem, cs>>>(a, L);
-  return true;
+  a.prefetch = st->n_envs >= ((int64_t)1 << 19);
 }
 
 template <typename R, int AC, bool DM, bool POL>
 void launch_task_dr(bool dr, unsigned g, cudaStream_t cs, const TaskArgs<R>& a) {
-  if constexpr (!POL && sizeof(R) == 4) {
-    if (dr ? launch_task_pipe<R, true, AC, DM>(g, cs, a)
-           : launch_task_pipe<R, false, AC, DM>(g, cs, a))
-      return;
-  }
   UUV_REGISTER(k_task_step<R, true, AC, DM, POL>);
   UUV_REGISTER(k_task_step<R, false, AC, DM, POL>);
   if (dr) k_task_step<R, true, AC, DM, POL><<<g, kBlock, 0, cs>>>(a);
