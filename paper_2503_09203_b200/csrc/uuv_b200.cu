@@ -577,10 +577,11 @@ __global__ void __launch_bounds__(kBlock, HI ? kMinBHi : ((NT > 1 && sizeof(R) =
 // of a (n_slots, n, cmd_ld) ring -- exactly step_batch(state, ring[slot]) T
 // times (engine.py:465-484), bit for bit (same substep code, same parameters):
 // frozen rows stay frozen and count steps, a non-finite substep freezes the row
-// at its last finite state.  Per launch instead of per step: the state loads and
-// the DR derivation (derive_env + sub_from_env); per step: the command row
-// (loaded one step ahead) and the state stores (every step, as step_batch
-// leaves it), plus the optional (T, 13, trace_ld) pose trace.  With `ready`
+// at its last finite state.  Per launch instead of per step: the state loads,
+// the DR derivation (derive_env + sub_from_env) and the state stores (the states
+// between the first and the last step are dead stores, as the substeps' are in
+// k_step); per step: the command row (loaded one step ahead) and the optional
+// (T, 13, trace_ld) pose trace.  With `ready`
 // set, step t first waits (acquire, GPU scope) until *ready > t: a producer on
 // another stream fills the ring slot and then raises the counter -- the device-
 // side command ring of a resident stepper.
@@ -682,11 +683,7 @@ UUV_D void rollout_env(const RolloutArgs<R, NT>& ra, int64_t i, StepIn<R>& in) {
       };
       if (DR && jit != nullptr) run(std::true_type{});
       else run(std::false_type{});
-      store_state(sv, i, A, in.px, in.py, in.pz, in.q, in.nu, in.act);
-      if (!ok) {
-        in.div = 1;
-        sv.diverged[i] = 1;
-      }
+      if (!ok) in.div = 1;  // frozen from here on at its last finite state
     }
     in.steps += 1;
     if (ra.trace != nullptr) {
@@ -704,6 +701,10 @@ UUV_D void rollout_env(const RolloutArgs<R, NT>& ra, int64_t i, StepIn<R>& in) {
       for (int j = 0; j < UUV_MAX_ACT; ++j) un[j] = (j < NA && j < A) ? c[j] : R(0);
     }
   }
+  // the state after the last step: intermediate states live only in registers (and the
+  // optional trace), as the substeps of one step do in k_step
+  store_state(sv, i, A, in.px, in.py, in.pz, in.q, in.nu, in.act);
+  sv.diverged[i] = in.div;
   sv.steps[i] = in.steps;
 }
 

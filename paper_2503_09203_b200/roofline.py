@@ -68,11 +68,12 @@ def frame_bytes(a: float, n_dr: int = 0, current: bool = False, dtype_bytes: int
 
 def rollout_frame_bytes(a: int, n_dr: int = 0, steps: int = 1, current: bool = False,
                         dtype_bytes: int = 4) -> float:
-    """k_rollout: per step the command row read and the state stored (p, q, nu, act); per
-    launch (amortised over ``steps``) the state, steps/diverged and DR record read, the
-    step counter written."""
-    per_step = dtype_bytes * a + dtype_bytes * (13 + a)
-    per_launch = dtype_bytes * (13 + a) + 5 + 8 * n_dr + 4 + (3 * dtype_bytes if current else 0)
+    """k_rollout: per step the command row read; per launch (amortised over ``steps``) the
+    state, steps/diverged and DR record read and the state, steps, diverged written (the
+    states between the first and the last step never leave registers)."""
+    per_step = dtype_bytes * a
+    state = dtype_bytes * (13 + a) + 4 + 1
+    per_launch = 2 * state + 8 * n_dr + (3 * dtype_bytes if current else 0)
     return per_step + per_launch / max(steps, 1)
 
 
