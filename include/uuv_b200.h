@@ -3,15 +3,20 @@
  *
  * Drop-in boundary for the reference hot path (Python `uuvsim`, /root/reference):
  *
- *   uuv_step        replaces uuvsim/engine.py:465-484 step_batch
+ *   uuv_state_from_dlpack  binds the BatchState fields (engine.py:269-295)
+ *                   given as DLPack tensors (validated in C)
+ *   uuv_step_dl / uuv_step  replace uuvsim/engine.py:465-484 step_batch
  *                   (and its callees _step_slice 405-418, _substeps 421-449,
  *                    _advance_rotors 335-352, _actuator_wrench_batch 355-402,
  *                    hydrodynamics.py:125-197, kinematics.py:245-266)
- *   uuv_reset       replaces uuvsim/engine.py:487-512 reset_envs for declarative
+ *   uuv_rollout_dl  step_batch T times with known commands in one launch
+ *                   (throughput_probe engine.py:541-564)
+ *   uuv_step_host   step_batch on host arrays, whole result back (uuv_host_out)
+ *   uuv_reset(_dl) replaces uuvsim/engine.py:487-512 reset_envs for declarative
  *                   samplers (default_sampler 265-266; the task samplers
  *                   tasks/core.py:282-289 + 402-407/454-460/503-507; DR draws
  *                   randomization.py:213-234; overlay math vehicles/__init__.py:418-505)
- *   uuv_task_step   replaces uuvsim/tasks/core.py:328-370 VecTaskEnv.step
+ *   uuv_task_step(_dl) replaces uuvsim/tasks/core.py:328-370 VecTaskEnv.step
  *                   (physics + observe 316-321 + rewards 170-214 + auto-reset)
  *   uuv_task_reset  replaces uuvsim/tasks/core.py:294-301 VecTaskEnv.reset
  *   uuv_observe     replaces uuvsim/tasks/core.py:316-321 VecTaskEnv.observe
@@ -20,9 +25,10 @@
  *
  * Conventions
  *  - Every array is DEVICE memory owned by the caller and borrowed for the
- *    call; nothing is retained and nothing is allocated inside uuv_step /
- *    uuv_task_step.  All work is enqueued on `stream` (a cudaStream_t, NULL =
- *    legacy default stream); no call synchronises the host.
+ *    call (plain pointers, or DLPack tensors in the *_dl entry points); nothing
+ *    is retained and nothing is allocated inside uuv_step / uuv_task_step.
+ *    All work is enqueued on `stream` (a cudaStream_t, NULL = legacy default
+ *    stream); only the host-buffer entry points (sync != 0) synchronise.
  *  - Per-env state is struct-of-arrays: component c of env i lives at
  *    base[c * ld + i] (ld >= n_envs).  Commands and observations are
  *    row-major (n_envs, width) with an explicit row stride.

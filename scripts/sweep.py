@@ -23,29 +23,13 @@ from paper_2503_09203_b200 import engine as E  # noqa: E402
 from paper_2503_09203_b200.randomization import DRParameter, Uniform, preset  # noqa: E402
 from paper_2503_09203_b200.vehicles import BUILTIN_VEHICLES, load_vehicle  # noqa: E402
 
-PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
-    if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
-# FP32 side of the per-step roofline: the FFMA-chain measurement of this pool's
-# B200s (scripts/probes/fp32_peak.cu -> profiles/r01/fp32_peak.json); else the
-# nominal 148 SM x 128 lanes x 2 flops x 1.965 GHz.
-_FP32 = os.path.join(ROOT, "profiles", "r01", "fp32_peak.json")
-FP32_TFLOPS, FP32_SOURCE = (json.load(open(_FP32))["fp32_tflops"], "measured") \
-    if os.path.exists(_FP32) else (74.4, "nominal")
+from paper_2503_09203_b200 import roofline as RF  # noqa: E402
 
-# Executed flops per substep (SURVEY.md §8(d) counting: +,-,x,/ = 1, FMA = 2,
-# sqrt/sin/cos/atan2 = 1, clamps 0): 5A + 16P + 87F + 6(A-1) + C with C = 332 on
-# the diagonal-hull, r_g = 0 path the kernel specialises (bluerov, bluerov_heavy,
-# lauv) and 638 for the general formulation (iauv, hauv: r_g != 0); + 33 for the
-# current-relative velocity R(q)^T c.  Task layer (obs, reward, termination):
-# ~250 per frame (SURVEY's upper estimate).
-FLEET_SHAPE = {"bluerov": (6, 6, 0, True), "bluerov_heavy": (8, 8, 0, True),
-               "lauv": (5, 1, 4, True), "iauv": (5, 1, 4, False), "hauv": (8, 8, 0, False)}
-TASK_FLOPS = 250
-
-
-def substep_flops(vehicle, current=False):
-    a, p, f, dm = FLEET_SHAPE[vehicle]
-    return 5 * a + 16 * p + 87 * f + 6 * (a - 1) + (332 if dm else 638) + (33 if current else 0)
+PEAK = RF.hbm_peak()[0]
+FP32_TFLOPS, FP32_SOURCE = RF.fp32_peak()
+TASK_FLOPS = RF.TASK_FLOPS
+substep_flops = RF.substep_flops
+frame_bytes = RF.frame_bytes
 
 
 def roofline(us_per_step, n, bpf, fpf):
@@ -58,15 +42,6 @@ def roofline(us_per_step, n, bpf, fpf):
             "bound": "hbm" if t_hbm >= t_fp else "fp32",
             "frac_roofline": max(t_hbm, t_fp) / us_per_step,
             "fp32_peak_tflops": FP32_TFLOPS, "fp32_peak_source": FP32_SOURCE}
-
-
-def frame_bytes(a, n_dr, cur, dtype_bytes=4, mixed=False):
-    b = dtype_bytes * (2 * (13 + a) + a) + 2 + 8 + 8 * n_dr
-    if cur:
-        b += 3 * dtype_bytes
-    if mixed:
-        b += 1
-    return b
 
 
 def make_case(name, n):
@@ -106,7 +81,7 @@ def make_case(name, n):
         width = 8
         bpf = frame_bytes(8, 7, True)
         # payload / cobm draws move r_g: counted with the general formulation
-        fpf = 5 * 8 + 16 * 8 + 6 * 7 + 638 + 33
+        fpf = substep_flops("bluerov_heavy", current=True, general=True)
     else:
         raise ValueError(name)
     return st, width, bpf, fpf
@@ -132,7 +107,7 @@ def measure_task(name, n, steps):
         # physics 278 B (train DR: 7 ratios + current) + obs 4*(12+8+1), reward 4,
         # term/trunc 2, prev_u 8*8
         bpf = frame_bytes(8, 7, True) + 4 * (12 + 8 + 1) + 4 + 2 + 8 * 8
-        fpf = 5 * 8 + 16 * 8 + 6 * 7 + 638 + 33 + TASK_FLOPS
+        fpf = substep_flops("bluerov_heavy", current=True, general=True) + TASK_FLOPS
     env.reset()
     cmds = torch.rand((n, a), device=dev) * 2 - 1
     s = torch.cuda.Stream(dev)
