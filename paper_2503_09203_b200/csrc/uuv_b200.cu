@@ -622,6 +622,14 @@ UUV_D void rollout_env(const RolloutArgs<R, NT>& ra, int64_t i, StepIn<R>& in) {
   const bool has_cur = sv.cur != nullptr;
   V3<R> cur{R(0), R(0), R(0)};
   if (has_cur) cur = V3<R>{sv.cur[i], sv.cur[sv.ld + i], sv.cur[2 * sv.ld + i]};
+  Sub<R> s;
+  const double* jit = nullptr;
+  if (DR) {
+    EnvD e;
+    derive_env(H.d, sv.ov, sv.ld, i, sv.slot, e);
+    sub_from_env<R, DM, true, AC>(H.r, e, s);
+    if (sv.slot[UUV_OV_JITTER] >= 0) jit = sv.ov + sv.slot[UUV_OV_JITTER] * sv.ld + i;
+  }
   uint32_t avail = 0;
   bool stalled = false;  // the producer never raised the counter: give up, never hang
   auto slot_row = [&](int t) {
@@ -645,18 +653,10 @@ UUV_D void rollout_env(const RolloutArgs<R, NT>& ra, int64_t i, StepIn<R>& in) {
   };
   R un[UUV_MAX_ACT];
   wait_slot(0);
-  {  // the first command row is in flight with the state and DR-record loads
+  {
     const R* c = slot_row(0);
 #pragma unroll
     for (int j = 0; j < UUV_MAX_ACT; ++j) un[j] = (j < NA && j < A) ? c[j] : R(0);
-  }
-  Sub<R> s;  // per-env parameters, derived once for all the steps
-  const double* jit = nullptr;
-  if (DR) {
-    EnvD e;
-    derive_env(H.d, sv.ov, sv.ld, i, sv.slot, e);
-    sub_from_env<R, DM, true, AC>(H.r, e, s);
-    if (sv.slot[UUV_OV_JITTER] >= 0) jit = sv.ov + sv.slot[UUV_OV_JITTER] * sv.ld + i;
   }
   for (int t = 0; t < ra.steps && !stalled; ++t) {
     R u[UUV_MAX_ACT];
