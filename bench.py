@@ -515,8 +515,10 @@ def run_b200(args):
     roof = RF.roofline(us_step, n, RF.rollout_frame_bytes(A_BLUEROV, len(DR_KEYS), k_total),
                        RF.substep_flops("bluerov"))
     traffic, traffic_src = load_traffic()
-    roof.update(traffic=traffic, traffic_note=f"ncu dram bytes per frame of the dominant kernel "
-                f"(cold cache), {traffic_src}" if traffic_src else None,
+    roof.update(traffic=traffic, traffic_note=f"ncu dram bytes read + written by one launch of the "
+                f"dominant kernel ({traffic_src}/ncu_traffic.json: 20 steps, cold cache)"
+                if traffic_src else None,
+                algorithmic_bytes_per_launch=n * k_total * roof["bytes_per_frame"],
                 kernel="k_rollout<float,1,DR,6,DM>")
     roof_graph = RF.roofline(el_graph / k_total * 1e6, n, algorithmic_bytes_per_frame(),
                              RF.substep_flops("bluerov"))

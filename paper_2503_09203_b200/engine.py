@@ -1033,13 +1033,18 @@ class ThroughputReport:
 
 def throughput_probe(sim: SimConfig, vehicle: VehicleConfig, duration: float = 2.0,
                      warmup_steps: int = 20, seed: int = 0, *, dtype=torch.float32,
-                     device=None, graph: bool = True) -> ThroughputReport:
+                     device=None, mode: str = "rollout") -> ThroughputReport:
     """Stepping rate with active rotors (engine.py:541-564), device-timed.
 
     Commands are ``default_rng(seed).uniform(-1, 1, (N, A))`` held fixed, as in
-    the reference; steps are replayed from a captured CUDA graph of 100 launches
-    (``graph=False`` launches from Python) and timed with CUDA events.
+    the reference.  ``mode``: ``"rollout"`` runs chunks of 100 steps as one
+    ``rollout`` launch each (the state held in registers, bit for bit 100
+    ``step_batch`` calls); ``"graph"`` replays a captured CUDA graph of 100
+    ``step_batch`` launches; ``"launch"`` launches every step from Python.
+    Timed with CUDA events.
     """
+    if mode not in ("rollout", "graph", "launch"):
+        raise EngineError(f"mode must be rollout, graph or launch, got {mode!r}")
     st = make_batch(vehicle, sim, master_seed=seed, device=device, dtype=dtype)
     reset_envs(st, np.ones(sim.batch_size, bool))
     cmds = torch.from_numpy(np.random.default_rng(seed).uniform(
@@ -1047,8 +1052,10 @@ def throughput_probe(sim: SimConfig, vehicle: VehicleConfig, duration: float = 2
     for _ in range(warmup_steps):
         step_batch(st, cmds)
     chunk = 100
-    run = (lambda: [step_batch(st, cmds) for _ in range(chunk)])
-    if graph:
+    if mode == "rollout":
+        def run():
+            rollout(st, cmds, chunk)
+    elif mode == "graph":
         s = torch.cuda.Stream(st.device)
         s.wait_stream(torch.cuda.current_stream(st.device))
         g = torch.cuda.CUDAGraph()
@@ -1059,6 +1066,10 @@ def throughput_probe(sim: SimConfig, vehicle: VehicleConfig, duration: float = 2
                     step_batch(st, cmds)
         torch.cuda.current_stream(st.device).wait_stream(s)
         run = g.replay
+    else:
+        def run():
+            for _ in range(chunk):
+                step_batch(st, cmds)
     torch.cuda.synchronize(st.device)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     n_steps, t_wall = 0, time.perf_counter()

@@ -19,16 +19,16 @@ for n in (256, 4096):
     st = E.make_batch(load_vehicle("bluerov"), E.SimConfig(batch_size=n), master_seed=4)
     E.reset_envs(st, np.ones(n, bool))
     cmd = (torch.rand((n, 6)) * 2 - 1).pin_memory()
-    out = torch.empty((13, n)).pin_memory()
+    out = E.HostStepOut(st)  # the whole step result (p, q, nu, act, steps, diverged)
     rows = []
     with E.serve(st, idle_timeout_ms=2000) as srv:
         for t in range(300):
-            E.step_batch(st, cmd, pose_out=out if t % 2 else None)
+            E.step_batch(st, cmd, out=out if t % 2 else None)
             b = (ctypes.c_uint64 * 8)()
             N.load().uuv_server_stamps(srv._h, b)
             rows.append([int(b[k]) for k in range(8)])
     r = np.array(rows[20:], dtype=np.int64)
-    for label, sel in (("with pose", r[1::2]), ("no pose", r[0::2])):
+    for label, sel in (("with result", r[1::2]), ("no result", r[0::2])):
         rel = sel[:, [0, 1, 2, 3, 4, 5, 7]] - sel[:, [6]]
         print(n, label, "median ns from host ring: seen, published, cmds, physics, counted, released, host-done:",
               np.median(rel, axis=0).astype(int).tolist(), "total", int(np.median(sel[:, 7] - sel[:, 6])))

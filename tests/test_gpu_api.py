@@ -111,12 +111,15 @@ def test_current_rotates_into_body_frame():
     assert np.abs(nu_c.numpy() - np.array([0, -1, 0, 0, 0, 0])).max() < 1e-12
 
 
-def test_throughput_probe_reports():
+@pytest.mark.parametrize("mode", ["rollout", "graph", "launch"])
+def test_throughput_probe_reports(mode):
     rep = E.throughput_probe(E.SimConfig(batch_size=16), load_vehicle("bluerov"), duration=0.05,
-                             warmup_steps=2, seed=0)
+                             warmup_steps=2, seed=0, mode=mode)
     assert rep.batch_size == 16 and rep.n_steps > 0
     assert rep.aggregate_steps_per_s == pytest.approx(16 * rep.n_steps / rep.elapsed_s)
     assert rep.diverged_envs == 0
+    with pytest.raises(E.EngineError):
+        E.throughput_probe(E.SimConfig(batch_size=16), load_vehicle("bluerov"), mode="other")
 
 
 def test_write_row_gives_one_env_new_parameters():
