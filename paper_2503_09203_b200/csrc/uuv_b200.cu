@@ -352,14 +352,7 @@ UUV_D bool physics_at(const Hull<R>& H, const StateView<R>& sv, int64_t i, const
   const double* jit = nullptr;
   if (DR) {
     EnvD e;
-#ifdef UUV_EXP_NODERIVE  // diagnostic build only (scripts/gpu_ab_exp.sh): hull values, no record reads
-    {
-      const int32_t none[UUV_OV_COUNT] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
-      derive_env(H.d, ov, ov_ld, ov_i, none, e);
-    }
-#else
     derive_env(H.d, ov, ov_ld, ov_i, sv.slot, e);
-#endif
     sub_from_env<R, DM, PRE, AC>(H.r, e, s);
     if (sv.slot[UUV_OV_JITTER] >= 0) jit = sv.ov + sv.slot[UUV_OV_JITTER] * sv.ld + i;
   }
@@ -390,8 +383,7 @@ UUV_D bool physics(const Hull<R>& H, const StateView<R>& sv, int64_t i, int K, R
                                    q, nu, act);
 }
 
-// Inputs of one env's step, loaded ahead of use so that a persistent thread can
-// have env k+1's loads in flight while it computes env k.
+// Inputs of one env's step, all loaded before any arithmetic (one memory round trip).
 template <typename R> struct StepIn {
   R px, py, pz;
   Q4<R> q;
@@ -499,9 +491,6 @@ UUV_D void step_any(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in) {
   }
 }
 
-// One env per thread; when the grid is smaller than the batch (persistent mode)
-// each thread walks envs with stride gridDim * kBlock and prefetches the next
-// env's inputs into registers before computing the current one.
 // L2 prefetch of the DR-record slots the per-launch derivation reads (keys up to
 // and including payload_position); issued before the dependent-launch wait.
 template <typename R>
@@ -541,34 +530,15 @@ __global__ void __launch_bounds__(kBlock, HI ? kMinBHi : ((NT > 1 && sizeof(R) =
       if (on) pdl_trigger();
     }
   } exit_trigger{a.early_trigger == 2};
-  const int64_t stride = (int64_t)gridDim.x * kBlock;
-  int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
-  const int64_t n = a.sv.n;
-  if (i >= n) return;
+  const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+  if (i >= a.sv.n) return;
   StepIn<R> cur;
   load_in<R, NT, AC>(a, i, cur);
   // mode 3: release the next step once this step's loads are issued -- it is
   // already past its own wait here, so at most two grids are in flight, and the
   // next step's command prefetch overlaps this step's compute
   if (a.early_trigger == 3) pdl_trigger();
-#if UUV_PERSISTENT_STEP
-  while (true) {
-    const int64_t nx = i + stride;
-    if (nx < n) {
-      StepIn<R> nxt;
-      load_in<R, NT, AC>(a, nx, nxt);
-      step_any<R, NT, DR, AC, DM, !HI>(a, i, cur);
-      cur = nxt;
-      i = nx;
-    } else {
-      step_any<R, NT, DR, AC, DM, !HI>(a, i, cur);
-      break;
-    }
-  }
-#else
-  (void)stride;
   step_any<R, NT, DR, AC, DM, !HI>(a, i, cur);
-#endif
 }
 
 // ------------------------------------------------------------------ multi-step rollout
@@ -1555,18 +1525,6 @@ void fill_hulls(const uuv_ctx* ctx, Hull<R>* dst, double dt_sub, int first = 0) 
   }
 }
 
-#ifndef UUV_PERSISTENT_STEP
-#define UUV_PERSISTENT_STEP 0
-#endif
-int64_t step_waves() {
-  if (!UUV_PERSISTENT_STEP) return INT64_MAX / 4;  // one thread per env
-  static const int64_t w = [] {
-    const char* v = getenv("UUV_STEP_WAVES");
-    return v ? std::max<int64_t>(1, atoll(v)) : (int64_t)1;
-  }();
-  return w;
-}
-
 template <typename R, int NT, bool DR, int AC, bool DM = false>
 uuv_status launch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd, int64_t cmd_ld,
                        int32_t K, double dt, cudaStream_t s, const HostOut* out = nullptr,
@@ -1594,9 +1552,7 @@ uuv_status launch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd,
   const bool hi = kHiOk && st->n_envs >= hi_min && K == 1;
   auto kern = hi ? k_step<R, NT, DR, AC, DM, kHiOk> : k_step<R, NT, DR, AC, DM, false>;
   const int64_t wave = one_wave_ctas(kern);
-  // persistent (grid-stride + register prefetch) beyond one wave; UUV_STEP_WAVES overrides
-  const int64_t waves = step_waves();
-  const int64_t grid = waves >= need ? need : std::min<int64_t>(need, wave * waves);
+  const int64_t grid = need;  // one thread per env
   // dependent-launch trigger: small grids (<= 64 CTAs) release the next step as
   // soon as their loads are issued (mode 3), larger grids after their stores
   // (mode 2).  Mode 3 overlaps the next step's command fetch with this step's
