@@ -300,10 +300,11 @@ class DeviceTimer:
         self.submit_us = None
         self.cycles_per_us = 1965.0  # B200 max SM clock: a spin of >= gate_us at any clock
 
-    def run(self, enqueue, gate=True):
+    def run(self, enqueue, gate=True, flush=True):
         torch = self.torch
-        with torch.cuda.stream(self.stream):
-            self.flush.fill_(1)
+        if flush:
+            with torch.cuda.stream(self.stream):
+                self.flush.fill_(1)
         self.barrier()
         torch.cuda.synchronize(self.dev)
         with torch.cuda.stream(self.stream):
