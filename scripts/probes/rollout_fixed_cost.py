@@ -35,4 +35,15 @@ for mode in ("cold", "warm"):
         us.append(t)
     slope, icpt = np.polyfit(ks, us, 1)
     fits[mode] = {"per_step_us": slope, "fixed_us": icpt}
+# reference points in the same harness: one step_batch launch, and a 1-element torch fill
+# (event + launch overhead of any kernel)
+tiny = torch.zeros(1, device=dev)
+for name, enq in (("step_batch_1", lambda: E.step_batch(st, ring[3])),
+                  ("torch_fill_1", lambda: tiny.fill_(1.0))):
+    timer.run(enq)
+    out[name] = float(np.mean([timer.run(enq) for _ in range(50)])) * 1e6
+for k in (1, 20):  # means over 50 launches (the event clock ticks in ~1 us steps)
+    def enq(k=k):
+        E.rollout(st, ring, k, start=7)
+    out[f"mean50_cold_{k}"] = float(np.mean([timer.run(enq) for _ in range(50)])) * 1e6
 print(json.dumps({"us": out, "fit": fits}))
