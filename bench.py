@@ -387,6 +387,21 @@ def at_scale_blocks(ctx, timer, stream, steps, gen):
     measure("cfg2_1m", n, lambda t: E.step_batch(st, ring[t % len(ring)]),
             lambda t: E.step_batch(st, ring[t]), RF.frame_bytes(6, 4), RF.substep_flops("bluerov"),
             "cfg2 workload at 1,048,576 envs/GPU")
+    # the headline kernel (k_rollout) where it is not latency-bound: the same 1M envs,
+    # 20 steps in one launch, fresh command slots from the same ring
+    def roll():
+        E.rollout(st, ring, steps, start=3)
+
+    roll()
+    timer.run(roll)
+    el = allreduce_max(timer.run(roll), dev)
+    us = el / steps * 1e6
+    out["cfg2_rollout_1m"] = {
+        "workload": "cfg2 workload at 1,048,576 envs/GPU, 20 steps as one engine.rollout launch",
+        "envs_per_gpu": n, "steps": steps, "us_per_step": us,
+        "env_frames_per_s": ctx.world * n / (el / steps),
+        "roofline": RF.roofline(us, n, RF.rollout_frame_bytes(6, 4, steps),
+                                RF.substep_flops("bluerov"))}
     del st, ring
 
     # configs[2]: all five vehicles mixed, 262,144 envs (contiguous per-type runs)
