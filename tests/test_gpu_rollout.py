@@ -149,6 +149,19 @@ def test_rollout_waits_for_the_device_command_ring():
     same(a, b)
 
 
+def test_rollout_large_batch_build():
+    """From 262,144 envs the 168-register rollout build runs (and k_step's 96-register
+    build): still bit for bit the launched steps."""
+    n, T = 262_144, 6
+    a, b = pair(cfg2(n, torch.float32))
+    ring = torch.rand((T, n, 6), device="cuda", generator=torch.Generator(
+        device="cuda").manual_seed(3)) * 2 - 1
+    for t in range(T):
+        E.step_batch(a, ring[t])
+    E.rollout(b, ring)
+    same(a, b)
+
+
 def test_rollout_argument_errors():
     st = cfg2(64, torch.float32)()
     with pytest.raises(E.EngineError, match="commands"):
