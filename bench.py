@@ -400,8 +400,13 @@ def at_scale_blocks(ctx, timer, stream, steps, gen):
         "workload": "cfg2 workload at 1,048,576 envs/GPU, 20 steps as one engine.rollout launch",
         "envs_per_gpu": n, "steps": steps, "us_per_step": us,
         "env_frames_per_s": ctx.world * n / (el / steps),
-        "roofline": RF.roofline(us, n, RF.rollout_frame_bytes(6, 4, steps),
-                                RF.substep_flops("bluerov"))}
+        # bytes this kernel must move (commands per step; state, counters and DR record
+        # once per launch): FP32-bound; `per_step_model_frac` is the SURVEY per-frame
+        # model (state round trip every step) that the rollout beats by construction
+        "roofline": dict(RF.roofline(us, n, RF.rollout_frame_bytes(6, 4, steps),
+                                     RF.substep_flops("bluerov")),
+                         per_step_model_frac=RF.roofline(us, n, RF.frame_bytes(6, 4),
+                                                         RF.substep_flops("bluerov"))["frac"])}
     del st, ring
 
     # configs[2]: all five vehicles mixed, 262,144 envs (contiguous per-type runs)
@@ -528,13 +533,19 @@ def run_b200(args):
     value = frames / el_max
     ms_per_step = 1e3 * el_max / k_total
     us_step = el / k_total * 1e6
-    roof = RF.roofline(us_step, n, RF.rollout_frame_bytes(A_BLUEROV, len(DR_KEYS), k_total),
-                       RF.substep_flops("bluerov"))
+    # the contract's algorithmic bytes: SURVEY.md §8(d)'s per-frame figure (state read +
+    # written, commands, counters, the DR record: 218 B for cfg2) x the frames one launch
+    # processes -- the same per-frame work as K step_batch calls.  k_rollout moves far
+    # less (the state stays in registers between steps): `traffic` (ncu) and
+    # `kernel_bytes_per_frame` give what it actually moves.
+    roof = RF.roofline(us_step, n, algorithmic_bytes_per_frame(), RF.substep_flops("bluerov"))
     traffic, traffic_src = load_traffic()
     roof.update(traffic=traffic, traffic_note=f"ncu dram bytes read + written by one launch of the "
                 f"dominant kernel ({traffic_src}/ncu_traffic.json: 20 steps, cold cache)"
                 if traffic_src else None,
                 algorithmic_bytes_per_launch=n * k_total * roof["bytes_per_frame"],
+                kernel_bytes_per_frame=RF.rollout_frame_bytes(A_BLUEROV, len(DR_KEYS), k_total),
+                fp32_frac=n * RF.substep_flops("bluerov") / us_step / 1e6 / RF.fp32_peak()[0],
                 kernel="k_rollout<float,1,DR,6,DM>")
     roof_graph = RF.roofline(el_graph / k_total * 1e6, n, algorithmic_bytes_per_frame(),
                              RF.substep_flops("bluerov"))
