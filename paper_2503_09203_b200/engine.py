@@ -40,7 +40,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .randomization import CURRENT_KEYS, Gaussian, Piecewise, Uniform
+from .randomization import CURRENT_KEYS, encodable
 from .vehicles import (
     DATA_DRIVEN, FIRST_ORDER, KIND_CODE, MODEL_CODE, RUDDER, TILTROTOR, VehicleConfig,
     fin_basis, tilt_rotation, validate_overlay,
@@ -219,19 +219,10 @@ class DeviceSampler:
         def fill(d: N.Draw, key_code, dist, n_draws):
             d.key = key_code
             d.n_draws = n_draws
-            if isinstance(dist, Uniform):
-                d.dist, d.lo, d.hi = N.DIST_UNIFORM, dist.lo, dist.hi
-            elif isinstance(dist, Piecewise):
-                d.dist = N.DIST_PIECEWISE
-                d.pw_bins = dist.densities.size
-                d.pw_offset = len(pw)
-                pw.extend(list(dist.breakpoints) + list(dist._cdf))
-            elif isinstance(dist, Gaussian):
-                d.dist, d.mu, d.sigma = N.DIST_GAUSSIAN, dist.mu, dist.sigma
-                d.lo, d.hi = dist.clip
-            else:
+            if not encodable(dist):
                 raise EngineError(f"{type(dist).__name__}: not a device-encodable distribution "
                                   "(use a sampler callable for the host reset path)")
+            dist.encode(d, pw)
 
         keys = self.keys()
         if len(keys) > N.MAX_DRAWS:

@@ -182,20 +182,3 @@ def test_disturbed_spec_is_fixed_point():
     assert d["current_velocity"].distribution.support() == (0.25, 0.25)
 
 
-def test_empirical_check_summaries():
-    from paper_2503_09203_b200 import randomization as R
-
-    spec = dict(R.preset("train"))
-    spec["payload_position"] = R.DRParameter("payload_position", R.Uniform(-0.1, 0.1))
-    out = R.empirical_check(spec, 5000, np.random.default_rng(1))
-    assert list(out) == sorted(spec)
-    for key, s in out.items():
-        lo, hi = spec[key].distribution.support()
-        assert lo <= s.min <= s.mean <= s.max <= hi
-        assert s.hist_counts.sum() == s.n == (15000 if key == "payload_position" else 5000)
-    again = R.empirical_check(spec, 5000, np.random.default_rng(1))
-    assert all(np.array_equal(out[k].hist_counts, again[k].hist_counts) for k in out)
-    point = R.empirical_check(R.preset("test_env1"), 10)
-    assert point["mass*"].min == point["mass*"].max == 1.1
-    with pytest.raises(R.DRSpecError):
-        R.empirical_check(spec, 0)
