@@ -25,7 +25,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from .randomization import CURRENT_KEYS, DRParameter, Uniform, make_spec, preset
-from .trajectories import HELIX, TrajectorySpec, reference_point
+from .trajectories import TrajectorySpec, reference_point
 
 STATION_KEEPING = "station_keeping"
 TRACKING = "tracking"
@@ -311,12 +311,7 @@ class VecTaskEnv:
             c.target_q[k] = tq[k]
         c.success_tol = t.success_tol
         c.dock_radius = t.dock.radius
-        tr = t.trajectory
-        c.traj_kind = _N.TRAJ_HELIX if tr.kind == HELIX else _N.TRAJ_LISSAJOUS
-        c.traj_radius, c.traj_rate, c.traj_climb = tr.radius, tr.angular_rate, tr.climb_rate
-        c.traj_z0, c.traj_phase = tr.z0, tr.phase
-        for k in range(3):
-            c.traj_amp[k], c.traj_rates[k] = tr.amplitude[k], tr.rates[k]
+        t.trajectory.pack_into(c)
         return c
 
     def _io(self, obs, term=None, rout=None, fout=None, stats=True) -> _N.TaskIO:
