@@ -229,9 +229,17 @@ struct uuv_ctx {
   mutable std::vector<cudaEvent_t> done;
   mutable cudaEvent_t forked = nullptr;
   ~uuv_ctx() {
+    // A context is often released by a garbage collector at an arbitrary point --
+    // possibly while another stream of the process is being captured into a CUDA
+    // graph, where (in the default global capture mode) destroying a stream or an
+    // event is a prohibited call that invalidates that capture.  These handles were
+    // never captured, so destroy them in relaxed mode.
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    cudaThreadExchangeStreamCaptureMode(&mode);
     for (cudaStream_t s : fork) cudaStreamDestroy(s);
     for (cudaEvent_t e : done) cudaEventDestroy(e);
     if (forked) cudaEventDestroy(forked);
+    cudaThreadExchangeStreamCaptureMode(&mode);
   }
 };
 

@@ -538,3 +538,28 @@ def test_pdl_modes_bitwise():
             assert r.returncode == 0, r.stderr[-2000:]
             out[(n, mode)] = r.stdout.strip().splitlines()[-1]
         assert len({out[(n, m)] for m in ("0", "2", "3", "4")}) == 1, out
+
+
+def test_batch_released_during_a_graph_capture():
+    """A fleet batch whose per-run dispatch created fork streams is garbage-collected
+    while another stream is being captured: its context must not invalidate the capture."""
+    import gc
+
+    names = ("bluerov", "lauv", "hauv")
+    n = 131_073
+    counts = [n // 3, n // 3, n - 2 * (n // 3)]
+    st = E.make_fleet_batch([load_vehicle(v) for v in names], counts,
+                            E.SimConfig(batch_size=n))
+    E.reset_envs(st, np.ones(n, bool))
+    E.step_batch(st, torch.zeros((n, st.a_max), device="cuda"))  # forks the run streams
+    torch.cuda.synchronize()
+    x = torch.zeros(8, device="cuda")
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        x.add_(1.0)
+        del st
+        gc.collect()
+        x.add_(1.0)
+    g.replay()
+    torch.cuda.synchronize()
+    assert float(x[0]) == 2.0
