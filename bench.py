@@ -328,12 +328,14 @@ def capture_steps(step, k_total, stream, chunk=256):
     """CUDA graphs of exactly k_total calls step(t) (chunks of <= chunk launches)."""
     import torch
 
+    from paper_2503_09203_b200 import engine as E
+
     graphs, done = [], 0
     while done < k_total:
         c = min(chunk, k_total - done)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.stream(stream):
-            with torch.cuda.graph(g, stream=stream):
+            with torch.cuda.graph(g, stream=stream), E.no_gc():
                 for s in range(c):
                     step(done + s)
         graphs.append(g)

@@ -591,6 +591,27 @@ def _cmd_width(state: BatchState) -> int:
         state.vehicle.action_dim
 
 
+class no_gc:
+    """Keep Python's cyclic garbage collector off while a CUDA graph is captured: a
+    collection inside the capture may free an older graph or stream (a previous
+    env's episode loop, say), and destroying one is a prohibited call that
+    invalidates the capture in progress."""
+
+    def __enter__(self):
+        import gc
+
+        self._was = gc.isenabled()
+        gc.disable()
+        return self
+
+    def __exit__(self, *exc):
+        import gc
+
+        if self._was:
+            gc.enable()
+        return False
+
+
 class HostStepOut:
     """Pinned host buffers for one step's result (``uuv_host_out``): every field the
     reference's ``step_batch`` mutates in place (engine.py:418, 444-449).
@@ -1052,7 +1073,7 @@ def throughput_probe(sim: SimConfig, vehicle: VehicleConfig, duration: float = 2
         g = torch.cuda.CUDAGraph()
         with torch.cuda.stream(s):
             step_batch(st, cmds)
-            with torch.cuda.graph(g, stream=s):
+            with torch.cuda.graph(g, stream=s), no_gc():
                 for _ in range(chunk):
                     step_batch(st, cmds)
         torch.cuda.current_stream(st.device).wait_stream(s)
