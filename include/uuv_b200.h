@@ -83,7 +83,7 @@ typedef struct DLManagedTensor {
 } DLManagedTensor;
 #endif
 
-#define UUV_ABI_VERSION 5
+#define UUV_ABI_VERSION 6
 #define UUV_MAX_RUNS 8
 #define UUV_MAX_ACT 8        /* actuator columns per vehicle type             */
 #define UUV_MAX_TYPES 6      /* vehicle types in one batch (mixed fleets)     */
@@ -461,6 +461,18 @@ uuv_status uuv_task_step(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task
 uuv_status uuv_policy_step(uuv_ctx* ctx, const uuv_state* state, const uuv_task* task,
                            const uuv_sampler* sampler, uint64_t seed, const uuv_policy* policy,
                            int32_t substeps, double dt, const uuv_task_io* io, void* stream);
+/* A whole episode loop of uuv_policy_step (t = 1 .. length) in ONE launch, the state
+ * held in registers across the steps; it stops after the first step at which no
+ * row of the batch is pending -- exactly the reference loop's break
+ * (baseline._rollout_returns, baseline.py:109-127).  Needs the episode buffers
+ * (ret, metric, success, pending) and live[length + 2]: live[0] = initial pending
+ * count, live[1..length] zeroed, live[length + 1] zeroed (the kernel's arrival
+ * counter).  Returns UUV_ERR_UNSUPPORTED when the grid cannot be co-resident
+ * (the per-step loop then applies). */
+uuv_status uuv_policy_episode(uuv_ctx* ctx, const uuv_state* state, const uuv_task* task,
+                              const uuv_sampler* sampler, uint64_t seed, const uuv_policy* policy,
+                              int32_t length, int32_t substeps, double dt,
+                              const uuv_task_io* io, void* stream);
 /* Reset masked rows (prev_u and dev_sum zeroed too), then observe all rows.
  * Replaces VecTaskEnv.reset (tasks/core.py:294-301). */
 uuv_status uuv_task_reset(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task,

@@ -1070,10 +1070,11 @@ UUV_D void task_in_global(const TaskArgs<R>& a, int64_t i, bool load_cmd, TaskIn
 // One env of VecTaskEnv.step (tasks/core.py:328-370): clip, physics (K substeps),
 // reward / termination / info, auto-reset, next observation (staged at srow),
 // state / prev_u / dev_sum stores, trace record, statistics into st.  The DR
-// record is read at (ov, ov_ld, ov_i): global memory or a staged slab.  STAGED:
-// previous command, current and deviation sum come from `in` (the slab); else they
-// are loaded from global memory where they are used (shorter live ranges).
-template <typename R, bool DR, int AC, bool DM, bool POL, bool STAGED = false>
+// record is read at (ov, ov_ld, ov_i).  CARRY (the fused episode loop): previous
+// command, current and deviation sum come from `in`, and the step's result is
+// written back into `in` for the next step; otherwise they are loaded from global
+// memory where they are used (shorter live ranges for the one-step kernel).
+template <typename R, bool DR, int AC, bool DM, bool POL, bool CARRY = false>
 UUV_D void task_env(const TaskArgs<R>& a, int64_t i, TaskIn<R>& in, const double* ov,
                     int64_t ov_ld, int64_t ov_i, R* srow, double* st, bool& live) {
   const StateView<R>& sv = a.sv;
@@ -1085,7 +1086,7 @@ UUV_D void task_env(const TaskArgs<R>& a, int64_t i, TaskIn<R>& in, const double
     // the observation the last step returned, recomputed from the stored state
     R pu[UUV_MAX_ACT];
 #pragma unroll
-    for (int j = 0; j < UUV_MAX_ACT; ++j) pu[j] = j < A ? a.prev_u[j * ld + i] : R(0);
+    for (int j = 0; j < UUV_MAX_ACT; ++j) pu[j] = j < A ? (CARRY ? in.pu[j] : a.prev_u[j * ld + i]) : R(0);
     observe_row<R>(T, A, in.px, in.py, in.pz, in.q, in.nu, pu, in.steps, a.dt, srow, nullptr);
     policy_command<R>(a, A, T.obs_dim, i, srow, in.raw);
   }
@@ -1095,7 +1096,7 @@ UUV_D void task_env(const TaskArgs<R>& a, int64_t i, TaskIn<R>& in, const double
   for (int j = 0; j < UUV_MAX_ACT; ++j) {
     if (j < A) {
       u[j] = clip_<R>(in.raw[j], R(-1), R(1));
-      du[j] = u[j] - (STAGED ? in.pu[j] : a.prev_u[j * ld + i]);
+      du[j] = u[j] - (CARRY ? in.pu[j] : a.prev_u[j * ld + i]);
     } else {
       u[j] = R(0);
       du[j] = R(0);
@@ -1108,14 +1109,14 @@ UUV_D void task_env(const TaskArgs<R>& a, int64_t i, TaskIn<R>& in, const double
   bool div = in.div;
   int32_t steps = in.steps;
   if (!div) {
-    if (STAGED)
+    if (CARRY)
       div = physics_at<R, DR, AC, DM>(H, sv, i, ov, ov_ld, ov_i, in.has_cur, in.cur, a.K,
                                       a.dt_sub, u, px, py, pz, q, nu, act);
     else
       div = physics<R, DR, AC, DM>(H, sv, i, a.K, a.dt_sub, u, px, py, pz, q, nu, act);
   }
   steps += 1;
-  R dev = STAGED ? in.dev : (a.dev_sum != nullptr ? a.dev_sum[i] : R(0));
+  R dev = CARRY ? in.dev : (a.dev_sum != nullptr ? a.dev_sum[i] : R(0));
   TaskOut<R> o;
   task_eval<R>(T, A, px, py, pz, q, nu, du, steps, div, a.dt, &dev, o);
   if (a.rout != nullptr) {
@@ -1151,12 +1152,12 @@ UUV_D void task_env(const TaskArgs<R>& a, int64_t i, TaskIn<R>& in, const double
       }
     }
   }
-  {  // statistics: one env per thread sets them, the staged (persistent) kernel sums its envs
+  {  // statistics: one env per thread sets them, the fused episode loop sums its steps
     const double v[UUV_ST_COUNT] = {(double)o.reward, (double)o.finished, (double)o.success,
                                     (double)o.failure, (double)o.truncated,
                                     o.finished ? (double)o.metric : 0.0, (double)div, 1.0};
 #pragma unroll
-    for (int k = 0; k < UUV_ST_COUNT; ++k) st[k] = STAGED ? st[k] + v[k] : v[k];
+    for (int k = 0; k < UUV_ST_COUNT; ++k) st[k] = CARRY ? st[k] + v[k] : v[k];
   }
   if (o.finished) {
     if (a.term_obs != nullptr)  // final observation of the ended episode
@@ -1168,6 +1169,7 @@ UUV_D void task_env(const TaskArgs<R>& a, int64_t i, TaskIn<R>& in, const double
     steps = 0;
     div = false;
     dev = R(0);
+    if (CARRY) in.cur = cur;
   }
   // (the policy episode loop passes no obs buffer: its next launch recomputes
   // the observation from the stored state)
@@ -1194,6 +1196,15 @@ UUV_D void task_env(const TaskArgs<R>& a, int64_t i, TaskIn<R>& in, const double
     tr[UUV_TRACE_REWARD * tl] = o.reward;
     tr[UUV_TRACE_T * tl] = (R)(__dmul_rn((double)steps, a.dt64));
     for (int j = 0; j < A; ++j) tr[(UUV_TRACE_CMD + j) * tl] = in.raw[j];
+  }
+  if (CARRY) {  // the next step continues from registers (nu, act were updated in place)
+    in.px = px; in.py = py; in.pz = pz;
+    in.q = q;
+    in.steps = steps;
+    in.div = div;
+    in.dev = dev;
+#pragma unroll
+    for (int j = 0; j < UUV_MAX_ACT; ++j) in.pu[j] = u[j];
   }
 }
 
@@ -1255,6 +1266,66 @@ __global__ void __launch_bounds__(kBlock, MinBTask<R>::value) k_task_step(const 
   __syncthreads();
   if (a.obs != nullptr) flush_obs<R>(s_obs, a.obs, a.obs_ld, od, row0, sv.n);
   if (a.stats != nullptr) cta_stats(st, s_red, a.stats + blockIdx.x * UUV_ST_COUNT);
+}
+
+// ------------------------------------------------------------------ fused policy episode
+// One whole episode loop of baseline._rollout_returns (baseline.py:109-127) in ONE
+// launch: every thread keeps its env's state in registers across the steps
+// (task_env<CARRY>) -- policy command, physics, reward / termination, auto-reset,
+// return bookkeeping -- and the grid stops after the first step t at which no row
+// of the WHOLE batch is pending, exactly where the reference loop breaks: per step,
+// each CTA adds its pending count to live[t], then arrives on a counter
+// (live[length + 1]) and waits for every CTA before reading live[t].  The grid must
+// be co-resident (checked on the host); same per-step results as `length`
+// uuv_policy_step launches.
+UUV_D uint32_t ld_acquire_gpu_i32(const int32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <typename R, bool DR, int AC, bool DM>
+__global__ void __launch_bounds__(kBlock, MinBTask<R>::value)
+    k_policy_episode(const __grid_constant__ TaskArgs<R> a, int32_t length) {
+  __shared__ __align__(16) R s_obs[kBlock * kObsMax];
+  __shared__ int s_go;
+  const StateView<R>& sv = a.sv;
+  const int A = a.hull[0].r.n_act;
+  const int od = a.task.obs_dim;
+  const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+  const bool on = i < sv.n;
+  const int64_t ld = sv.ld;
+  int32_t* arrive = a.ep_live + length + 1;
+  TaskIn<R> in;
+  if (on) {
+    task_in_global<R>(a, i, false, in);
+#pragma unroll
+    for (int j = 0; j < UUV_MAX_ACT; ++j) in.pu[j] = j < A ? a.prev_u[j * ld + i] : R(0);
+    in.dev = a.dev_sum != nullptr ? a.dev_sum[i] : R(0);
+    in.has_cur = sv.cur != nullptr;
+    in.cur = V3<R>{R(0), R(0), R(0)};
+    if (in.has_cur) in.cur = V3<R>{sv.cur[i], sv.cur[ld + i], sv.cur[2 * ld + i]};
+  }
+  double st[UUV_ST_COUNT];
+#pragma unroll
+  for (int k = 0; k < UUV_ST_COUNT; ++k) st[k] = 0.0;
+  for (int t = 1; t <= length; ++t) {
+    bool live = false;
+    if (on)
+      task_env<R, DR, AC, DM, true, true>(a, i, in, sv.ov, sv.ld, i, s_obs + threadIdx.x * od, st,
+                                          live);
+    const int cnt = __syncthreads_count(live);
+    if (threadIdx.x == 0) {
+      if (cnt != 0) atomicAdd(a.ep_live + t, cnt);
+      __threadfence();
+      atomicAdd(arrive, 1);
+      const uint32_t target = (uint32_t)t * gridDim.x;
+      while (ld_acquire_gpu_i32(arrive) < target) __nanosleep(20);
+      s_go = ld_acquire_gpu_i32(a.ep_live + t) != 0;
+    }
+    __syncthreads();
+    if (!s_go) break;  // no row of the batch is pending: the reference loop's break
+  }
 }
 
 // Task reset (mode 1: masked rows reset, prev_u / dev_sum cleared) + observe all rows.
@@ -1872,6 +1943,35 @@ void launch_task_step(bool dr, int ac, bool dm, unsigned g, cudaStream_t cs, con
   }
 }
 
+// The fused episode loop (k_policy_episode): false when the grid cannot be co-resident
+// (its per-step grid-wide wait needs every CTA running), so the caller falls back to
+// one uuv_policy_step launch per step.
+template <typename R, bool DR, int AC, bool DM>
+bool launch_episode_k(unsigned g, cudaStream_t cs, const TaskArgs<R>& a, int32_t length) {
+  auto kern = k_policy_episode<R, DR, AC, DM>;
+  UUV_REGISTER(k_policy_episode<R, DR, AC, DM>);
+  if ((int64_t)g > one_wave_ctas(kern)) return false;
+  kern<<<g, kBlock, 0, cs>>>(a, length);
+  return true;
+}
+
+template <typename R>
+bool launch_episode(bool dr, int ac, bool dm, unsigned g, cudaStream_t cs, const TaskArgs<R>& a,
+                    int32_t length) {
+  auto pick = [&](auto dr_c) {
+    constexpr bool D = decltype(dr_c)::value;
+    if (ac == 6) return dm ? launch_episode_k<R, D, 6, true>(g, cs, a, length)
+                           : launch_episode_k<R, D, 6, false>(g, cs, a, length);
+    if (ac == 8) return dm ? launch_episode_k<R, D, 8, true>(g, cs, a, length)
+                           : launch_episode_k<R, D, 8, false>(g, cs, a, length);
+    if (ac == kFinLayout) return dm ? launch_episode_k<R, D, kFinLayout, true>(g, cs, a, length)
+                                    : launch_episode_k<R, D, kFinLayout, false>(g, cs, a, length);
+    return dm ? launch_episode_k<R, D, 0, true>(g, cs, a, length)
+              : launch_episode_k<R, D, 0, false>(g, cs, a, length);
+  };
+  return dr ? pick(std::true_type{}) : pick(std::false_type{});
+}
+
 uuv_status check_task(const uuv_ctx* ctx, const uuv_state* st, const uuv_task* task,
                       const uuv_task_io* io, bool obs_optional = false) {
   if (task == nullptr || io == nullptr) return fail(UUV_ERR_ARG, "null task or io");
@@ -1897,6 +1997,9 @@ uuv_status step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd, int64_
                 int32_t K, double dt, cudaStream_t s, const HostOut* out);
 template <typename R, bool POL>
 void task(bool dr, int ac, bool dm, unsigned g, cudaStream_t cs, const TaskArgs<R>& a);
+template <typename R>
+bool episode(bool dr, int ac, bool dm, unsigned g, cudaStream_t cs, const TaskArgs<R>& a,
+             int32_t length);
 template <typename R>
 uuv_status rollout(const uuv_ctx* ctx, const uuv_state* st, const RolloutSpec& sp, int32_t K,
                    double dt, cudaStream_t s);
@@ -2026,6 +2129,15 @@ template void task<double, false>(bool, int, bool, unsigned, cudaStream_t, const
 #if UUV_TU_POLICY
 template void task<float, true>(bool, int, bool, unsigned, cudaStream_t, const TaskArgs<float>&);
 template void task<double, true>(bool, int, bool, unsigned, cudaStream_t, const TaskArgs<double>&);
+template <typename R>
+bool episode(bool dr, int ac, bool dm, unsigned g, cudaStream_t cs, const TaskArgs<R>& a,
+             int32_t length) {
+  return launch_episode<R>(dr, ac, dm, g, cs, a, length);
+}
+template bool episode<float>(bool, int, bool, unsigned, cudaStream_t, const TaskArgs<float>&,
+                             int32_t);
+template bool episode<double>(bool, int, bool, unsigned, cudaStream_t, const TaskArgs<double>&,
+                              int32_t);
 #endif
 }  // namespace uuv_tu
 
@@ -2514,9 +2626,10 @@ uuv_status uuv_task_step(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task
   return check_launch("uuv_task_step");
 }
 
-uuv_status uuv_policy_step(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task,
-                           const uuv_sampler* sampler, uint64_t seed, const uuv_policy* pol,
-                           int32_t substeps, double dt, const uuv_task_io* io, void* stream) {
+static uuv_status policy_impl(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task,
+                              const uuv_sampler* sampler, uint64_t seed, const uuv_policy* pol,
+                              int32_t substeps, double dt, const uuv_task_io* io,
+                              int32_t length, void* stream) {
   uuv_status s = check_state(ctx, st);
   if (s != UUV_OK) return s;
   if ((s = check_task(ctx, st, task, io, true)) != UUV_OK) return s;
@@ -2529,8 +2642,10 @@ uuv_status uuv_policy_step(uuv_ctx* ctx, const uuv_state* st, const uuv_task* ta
     return fail(UUV_ERR_SHAPE, "policy: theta row stride < action_dim * obs_dim + action_dim");
   if (pol->ret != nullptr &&
       (pol->metric == nullptr || pol->success == nullptr || pol->pending == nullptr ||
-       pol->live == nullptr || pol->t < 1))
+       pol->live == nullptr || (length == 0 && pol->t < 1)))
     return fail(UUV_ERR_ARG, "policy: episode buffers incomplete or t < 1");
+  if (length > 0 && pol->ret == nullptr)
+    return fail(UUV_ERR_ARG, "policy episode: needs the return / pending / live buffers");
   if (substeps < 1 || !(dt > 0)) return fail(UUV_ERR_ARG, "substeps >= 1 and dt > 0 required");
   if (st->n_envs == 0) return UUV_OK;
   cudaStream_t cs = (cudaStream_t)stream;
@@ -2549,18 +2664,42 @@ uuv_status uuv_policy_step(uuv_ctx* ctx, const uuv_state* st, const uuv_task* ta
     a.ep_live = pol->ret != nullptr ? pol->live : nullptr;
     a.ep_t = pol->t;
   };
+  bool launched = true;
   if (st->dtype == UUV_F32) {
     TaskArgs<float> a;
     fill_task_args<float>(ctx, st, task, sampler, seed, dt, substeps, io, a);
     fill_pol(a, (const float*)pol->theta);
-    uuv_tu::task<float, true>(dr, act_class(ctx), diag_mass(ctx, st), g, cs, a);
+    if (length > 0)
+      launched = uuv_tu::episode<float>(dr, act_class(ctx), diag_mass(ctx, st), g, cs, a, length);
+    else
+      uuv_tu::task<float, true>(dr, act_class(ctx), diag_mass(ctx, st), g, cs, a);
   } else {
     TaskArgs<double> a;
     fill_task_args<double>(ctx, st, task, sampler, seed, dt, substeps, io, a);
     fill_pol(a, (const double*)pol->theta);
-    uuv_tu::task<double, true>(dr, act_class(ctx), diag_mass(ctx, st), g, cs, a);
+    if (length > 0)
+      launched = uuv_tu::episode<double>(dr, act_class(ctx), diag_mass(ctx, st), g, cs, a, length);
+    else
+      uuv_tu::task<double, true>(dr, act_class(ctx), diag_mass(ctx, st), g, cs, a);
   }
-  return check_launch("uuv_policy_step");
+  if (!launched)
+    return fail(UUV_ERR_UNSUPPORTED, "policy episode: %u CTAs do not fit one wave (launch one "
+                "uuv_policy_step per step instead)", g);
+  return check_launch(length > 0 ? "uuv_policy_episode" : "uuv_policy_step");
+}
+
+uuv_status uuv_policy_step(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task,
+                           const uuv_sampler* sampler, uint64_t seed, const uuv_policy* pol,
+                           int32_t substeps, double dt, const uuv_task_io* io, void* stream) {
+  return policy_impl(ctx, st, task, sampler, seed, pol, substeps, dt, io, 0, stream);
+}
+
+uuv_status uuv_policy_episode(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task,
+                              const uuv_sampler* sampler, uint64_t seed, const uuv_policy* pol,
+                              int32_t length, int32_t substeps, double dt,
+                              const uuv_task_io* io, void* stream) {
+  if (length < 1) return fail(UUV_ERR_ARG, "policy episode: length must be >= 1");
+  return policy_impl(ctx, st, task, sampler, seed, pol, substeps, dt, io, length, stream);
 }
 
 uuv_status uuv_task_reset(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task,

@@ -90,6 +90,33 @@ def test_device_loop_matches_host_loop_and_graph_replay():
     assert np.array_equal(cb[2], e1[2])
 
 
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_fused_episode_kernel_equals_per_step_launches(dtype):
+    """uuv_policy_episode (one launch, state in registers, grid-wide stop) == one
+    uuv_policy_step launch per step: returns, metrics, successes, the live counts and the
+    env state / episode counters after the loop (which later episodes depend on)."""
+    pol = B.Policy(weights=np.random.default_rng(1).uniform(-0.3, 0.3, (8, 21)),
+                   bias=np.array([0.2, -0.1, 0.0, 0.1, -0.4, -0.6, -0.5, -0.3]))
+    res = []
+    for fused in (True, False):
+        env = dock_env(batch=300, dtype=dtype)  # 3 CTAs: the grid-wide stop is exercised
+        r = B.EpisodeRunner(env, 3, 100, graph=True, fused=fused)
+        th = np.stack([pol.theta() * (1.0 + 0.1 * k) for k in range(3)])
+        out = [r.run(th), r.run(th * 0.5)]
+        assert r._fused is fused
+        st = env.state
+        res.append((out, r.live.cpu().numpy()[:r.length + 1], r.steps_run(),
+                    st.p.cpu().numpy(), st.nu.cpu().numpy(), st.episodes.cpu().numpy(),
+                    st.steps.cpu().numpy()))
+    (o1, l1, s1, *st1), (o2, l2, s2, *st2) = res
+    assert s1 == s2 and np.array_equal(l1, l2)
+    for a, b in zip(o1, o2):
+        for x, y in zip(a, b):
+            assert np.array_equal(np.asarray(x), np.asarray(y))
+    for x, y in zip(st1, st2):
+        assert np.array_equal(x, y)
+
+
 def test_cem_deterministic_monotone_and_zero_variance():
     curves = [B.cem_train(small_env(), population=10, iterations=3, seed=5).curve
               for _ in range(2)]
