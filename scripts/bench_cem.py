@@ -50,7 +50,8 @@ def gpu_case(task, envs, population, iterations):
     t0 = time.perf_counter()
     B.cem_train(env, population=population, iterations=iterations, seed=1)
     full = (time.perf_counter() - t0) / iterations
-    return {"impl": "device", "envs": envs, "population": population,
+    return {"impl": "device", "fused_episode": bool(runner._fused), "envs": envs,
+            "population": population,
             "episode_length": task.episode_length, "steps_last_iteration": steps,
             "s_per_iteration_device": dev_s, "s_per_iteration_cem_train": full,
             "env_frames_per_s": envs * steps / dev_s, "enqueue_wall_s": wall / iterations}
