@@ -465,10 +465,10 @@ uuv_status uuv_policy_step(uuv_ctx* ctx, const uuv_state* state, const uuv_task*
  * held in registers across the steps; it stops after the first step at which no
  * row of the batch is pending -- exactly the reference loop's break
  * (baseline._rollout_returns, baseline.py:109-127).  Needs the episode buffers
- * (ret, metric, success, pending) and live[length + 2]: live[0] = initial pending
- * count, live[1..length] zeroed, live[length + 1] zeroed (the kernel's arrival
- * counter).  Returns UUV_ERR_UNSUPPORTED when the grid cannot be co-resident
- * (the per-step loop then applies). */
+ * (ret, metric, success, pending) and live[2 * (length + 1)]: live[0] = initial
+ * pending count, live[1..length] zeroed (pending after step t), the second half
+ * zeroed (the kernel's per-step arrival counters).  Returns UUV_ERR_UNSUPPORTED
+ * when the grid cannot be co-resident (the per-step loop then applies). */
 uuv_status uuv_policy_episode(uuv_ctx* ctx, const uuv_state* state, const uuv_task* task,
                               const uuv_sampler* sampler, uint64_t seed, const uuv_policy* policy,
                               int32_t length, int32_t substeps, double dt,

@@ -1274,10 +1274,12 @@ __global__ void __launch_bounds__(kBlock, MinBTask<R>::value) k_task_step(const 
 // (task_env<CARRY>) -- policy command, physics, reward / termination, auto-reset,
 // return bookkeeping -- and the grid stops after the first step t at which no row
 // of the WHOLE batch is pending, exactly where the reference loop breaks: per step,
-// each CTA adds its pending count to live[t], then arrives on a counter
-// (live[length + 1]) and waits for every CTA before reading live[t].  The grid must
-// be co-resident (checked on the host); same per-step results as `length`
-// uuv_policy_step launches.
+// each CTA adds its pending count to live[t] and arrives on that step's counter
+// (live[length + 1 + t]).  A CTA that still has pending rows knows the loop goes on
+// and continues at once; only a CTA with none waits for every CTA's step-t arrival
+// before reading live[t] (if all of them have none, all of them wait, read 0 and
+// stop together).  The grid must be co-resident (checked on the host); same
+// per-step results as `length` uuv_policy_step launches.
 UUV_D uint32_t ld_acquire_gpu_i32(const int32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -1295,7 +1297,7 @@ __global__ void __launch_bounds__(kBlock, MinBTask<R>::value)
   const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
   const bool on = i < sv.n;
   const int64_t ld = sv.ld;
-  int32_t* arrive = a.ep_live + length + 1;
+  int32_t* arrive = a.ep_live + length + 1;  // arrive[t]: CTAs done with step t
   TaskIn<R> in;
   if (on) {
     task_in_global<R>(a, i, false, in);
@@ -1318,10 +1320,13 @@ __global__ void __launch_bounds__(kBlock, MinBTask<R>::value)
     if (threadIdx.x == 0) {
       if (cnt != 0) atomicAdd(a.ep_live + t, cnt);
       __threadfence();
-      atomicAdd(arrive, 1);
-      const uint32_t target = (uint32_t)t * gridDim.x;
-      while (ld_acquire_gpu_i32(arrive) < target) __nanosleep(20);
-      s_go = ld_acquire_gpu_i32(a.ep_live + t) != 0;
+      atomicAdd(arrive + t, 1);
+      if (cnt != 0) {
+        s_go = 1;  // this CTA's own rows keep the loop going
+      } else {
+        while (ld_acquire_gpu_i32(arrive + t) < gridDim.x) __nanosleep(20);
+        s_go = ld_acquire_gpu_i32(a.ep_live + t) != 0;
+      }
     }
     __syncthreads();
     if (!s_go) break;  // no row of the batch is pending: the reference loop's break
