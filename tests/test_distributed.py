@@ -94,3 +94,38 @@ def test_two_rank_gloo_shards_equal_single_batch(tmp_path):
     for p in parts:
         assert np.allclose(p["stats"], want, rtol=1e-12)
         assert float(p["tmax"]) == 2.0
+
+
+_LAUNCHED = r"""
+import os, sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2503_09203_b200 import distributed as D
+ctx = D.init("gloo")
+t = torch.tensor([float(ctx.rank + 1), 1.0], dtype=torch.float64)
+D.allreduce_sum(t)
+off, cnt = D.shard_range(11, ctx.rank, ctx.world)
+np.savez(os.path.join(sys.argv[2], f"r{ctx.rank}.npz"), sum=t.numpy(), world=ctx.world,
+         rank=ctx.rank, off=off, cnt=cnt, dist=ctx.distributed, tmax=D.allreduce_max(
+             float(ctx.rank), "cpu"))
+D.finalize(ctx)
+"""
+
+
+def test_launch_and_init_two_cpu_ranks(tmp_path):
+    """distributed.launch re-executes a script as two ranks (torch.distributed.run on
+    127.0.0.1); distributed.init joins the gloo group from the environment -- the path
+    bench.py --gpus N takes, on CPU."""
+    from paper_2503_09203_b200 import distributed as D
+
+    script = tmp_path / "w.py"
+    script.write_text(_LAUNCHED)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {"CUDA_VISIBLE_DEVICES": ""}
+    assert D.launch(str(script), [root, str(tmp_path)], 2, env=env) == 0
+    r = [np.load(tmp_path / f"r{k}.npz") for k in range(2)]
+    for k, p in enumerate(r):
+        assert int(p["rank"]) == k and int(p["world"]) == 2 and bool(p["dist"])
+        assert p["sum"].tolist() == [3.0, 2.0] and float(p["tmax"]) == 1.0
+    assert [(int(p["off"]), int(p["cnt"])) for p in r] == [(0, 5), (5, 6)]
+    ctx = D.init()  # no WORLD_SIZE: a single process, no group
+    assert not ctx.distributed and ctx.world == 1
