@@ -480,9 +480,16 @@ UUV_D void step_env(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in) {
 
 // Mixed fleets: every env takes its vehicle type's specialised path (types are
 // contiguous env blocks, so the switch is warp-uniform except at block edges).
+// The float64 (validation) fleet kernels take the two generic paths only: eight
+// inlined specialisations left them at 255 registers with ~2 KB of spills.
+UUV_D bool diag_class(int8_t c) { return c == 1 || c == 2 || c == 5 || c == 6; }
+
 template <typename R, int NT, bool DR, int AC, bool DM, bool BRANCHLESS = false>
 UUV_D void step_any(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in) {
-  if constexpr (NT > 1) {
+  if constexpr (NT > 1 && sizeof(R) == 8) {
+    if (diag_class(a.cls[in.ty])) step_env<R, NT, DR, 0, true>(a, i, in);
+    else step_env<R, NT, DR, 0, false>(a, i, in);
+  } else if constexpr (NT > 1) {
     switch (a.cls[in.ty]) {
       case 1: step_env<R, NT, DR, 6, true>(a, i, in); return;
       case 2: step_env<R, NT, DR, 8, true>(a, i, in); return;
@@ -702,7 +709,10 @@ __global__ void __launch_bounds__(kBlock, HI ? 3 : 1) k_rollout(const __grid_con
   in.steps = sv.steps[i];
   in.div = sv.diverged[i];
   load_state(sv, i, A, in.px, in.py, in.pz, in.q, in.nu, in.act);
-  if constexpr (NT > 1) {
+  if constexpr (NT > 1 && sizeof(R) == 8) {
+    if (diag_class(ra.step.cls[in.ty])) rollout_env<R, NT, DR, 0, true>(ra, i, in);
+    else rollout_env<R, NT, DR, 0, false>(ra, i, in);
+  } else if constexpr (NT > 1) {
     switch (ra.step.cls[in.ty]) {
       case 1: rollout_env<R, NT, DR, 6, true>(ra, i, in); return;
       case 2: rollout_env<R, NT, DR, 8, true>(ra, i, in); return;
@@ -914,7 +924,10 @@ __global__ void __launch_bounds__(kBlock, (NT > 1 && sizeof(R) == 4) ? 3 : MinB<
       for (int j = 0; j < UUV_MAX_ACT; ++j)
         in.u[j] = (j < A) ? clip_<R>(crow[j], R(-1), R(1)) : R(0);
       if (stamp) sa.ctl->stamp[2] = global_ns() + (uint64_t)(in.u[0] > R(2));
-      if constexpr (NT > 1) {
+      if constexpr (NT > 1 && sizeof(R) == 8) {
+        if (diag_class(a.cls[in.ty])) serve_env<R, NT, DR, 0, true>(a, i, in, s_out);
+        else serve_env<R, NT, DR, 0, false>(a, i, in, s_out);
+      } else if constexpr (NT > 1) {
         switch (a.cls[in.ty]) {
           case 1: serve_env<R, NT, DR, 6, true>(a, i, in, s_out); break;
           case 2: serve_env<R, NT, DR, 8, true>(a, i, in, s_out); break;
@@ -1822,9 +1835,11 @@ uuv_status launch_rollout(const uuv_ctx* ctx, const uuv_state* st, const Rollout
   ra.trace_ld = sp.trace_ld;
   ra.ready = sp.ready;
   UUV_REGISTER(k_rollout<R, NT, DR, AC, DM, false>);
-  UUV_REGISTER(k_rollout<R, NT, DR, AC, DM, true>);
-  auto kern = st->n_envs >= kRolloutHiMinEnvs ? k_rollout<R, NT, DR, AC, DM, true>
-                                              : k_rollout<R, NT, DR, AC, DM, false>;
+  if constexpr (sizeof(R) == 4) UUV_REGISTER(k_rollout<R, NT, DR, AC, DM, true>);
+  auto kern = k_rollout<R, NT, DR, AC, DM, false>;
+  if constexpr (sizeof(R) == 4) {  // (the float64 validation build keeps every register)
+    if (st->n_envs >= kRolloutHiMinEnvs) kern = k_rollout<R, NT, DR, AC, DM, true>;
+  }
   kern<<<(unsigned)grid_for(st->n_envs), kBlock, 0, s>>>(ra);
   return check_launch("uuv_rollout");
 }
