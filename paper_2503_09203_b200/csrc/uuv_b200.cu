@@ -351,7 +351,8 @@ UUV_D void store_state(const StateView<R>& sv, int64_t i, int A, R px, R py, R p
 
 // Physics of one control step for env i; returns the post-step diverged flag.
 // K substeps for one env.  The overlay record is read at (ov, ov_ld, ov_i) — global
-// memory or a shared-memory slab; jitter always comes from the global record.
+// memory (a base pointer, leading dimension and row index); jitter always comes from
+// the global record.
 template <typename R, bool DR, int AC, bool DM, bool PRE = false>
 UUV_D bool physics_at(const Hull<R>& H, const StateView<R>& sv, int64_t i, const double* ov,
                       int64_t ov_ld, int64_t ov_i, bool has_cur, V3<R> cur, int K, R dt,
@@ -1052,7 +1053,8 @@ UUV_D void policy_command(const TaskArgs<R>& a, int A, int od, int64_t i, const 
   }
 }
 
-// Inputs of one env's task step, loaded from global memory or a staged slab.
+// Inputs of one env's task step (loaded from global memory, or carried in registers
+// across the steps of the fused policy episode).
 template <typename R> struct TaskIn {
   R raw[UUV_MAX_ACT];  // commands as given (unclipped; recorded in the trace)
   R pu[UUV_MAX_ACT];   // previous clipped command (tasks/core.py:333-335)
