@@ -13,6 +13,9 @@ pinned oracle and the reference's own fixtures (tests/golden/make_config_golden.
   compared with per-vehicle oracle batches.
 * Piecewise / Gaussian / vector mount-jitter DR drawn on the device, bit for
   bit against the reference's sample_overlay (Philox and PCG64 streams).
+* At the stated full sizes (cfg2, configs[3], configs[4] at 1,048,576 envs):
+  rows of the full batch equal small env_offset shards bit for bit, so the
+  fixture-checked small-batch behaviour holds at full size.
 
 Tolerances as tests/test_gpu_parity.py: float64 1e-12 per step, float32 1e-5
 relative / 1e-6 absolute per step; DR draws and counters bit-exact.
@@ -206,3 +209,76 @@ def test_device_piecewise_gaussian_jitter_draws(name, rng):
             ok, err = rowwise_close(host(arr), g[f"traj_{k}"][t], F64_RTOL, 1e-300)
             assert ok, (t, k, err)
         prev = tuple(g[f"traj_{k}"][t] for k in ("p", "q", "nu", "act"))
+
+
+# ------------------------------------------------------------------ full-size properties
+
+
+def _rows_of_big_equal_small(make, n_big, picks, m, steps, cmd_fn, fields):
+    """make(size, env_offset) -> object with .step(commands) and .state; the rows
+    [k, k + m) of the big batch must equal a small batch at env_offset k."""
+    big = make(n_big, 0)
+    smalls = [(k, make(m, k)) for k in picks]
+    for t in range(steps):
+        cmd = cmd_fn(t, n_big)
+        big.step(cmd)
+        for k, s in smalls:
+            s.step(cmd[k:k + m])
+    for k, s in smalls:
+        for f in fields:
+            a = getattr(big.state, f)[k:k + m]
+            b = getattr(s.state, f)
+            assert torch.equal(a, b), (k, f)
+
+
+@pytest.mark.parametrize("kind", ["tracking_k8", "docking_dr"])
+def test_task_configs_at_full_size_equal_small_shards(kind):
+    """BASELINE configs[3] / [4] at their stated 1,048,576 envs per GPU: rows of the full
+    batch (random streams keyed by the global env index, auto-resets on) equal the same
+    rows stepped as small batches with env_offset -- bit for bit, so the fixture-checked
+    small-batch behaviour holds at full size (and under any sharding)."""
+    from paper_2503_09203_b200.tasks import TaskConfig, make_env
+
+    if kind == "tracking_k8":
+        task = TaskConfig(task="tracking", vehicle="bluerov", level="disturbed",
+                          episode_length=6)
+        substeps = 8
+    else:
+        task = TaskConfig(task="docking", vehicle="bluerov_heavy", level="disturbed_dr",
+                          episode_length=6)
+        substeps = 1
+    n = 1 << 20
+
+    def make(size, off):
+        env = make_env(task, E.SimConfig(batch_size=size, substeps=substeps), seed=0,
+                       env_offset=off)
+        env.reset()
+        return env
+
+    g = torch.Generator(device="cuda").manual_seed(3)
+    cmds = [torch.rand((n, 8 if kind == "docking_dr" else 6), device="cuda", generator=g) * 2 - 1
+            for _ in range(9)]
+    _rows_of_big_equal_small(make, n, (0, 333_333, n - 500), 500, 9, lambda t, _: cmds[t],
+                             ("p", "q", "nu", "act", "steps", "episodes", "diverged"))
+
+
+def test_config2_at_full_size_equals_small_shards():
+    """cfg2 at 1M envs (the 96-register large-batch build, DR record prefetch) == the same
+    rows as 4096-env shards (the small-batch build), bit for bit."""
+    n, m = 1 << 20, 4096
+    spec = cfg2_spec()
+
+    class Shard:
+        def __init__(self, size, off):
+            self.state = E.make_batch(product_vehicle("bluerov"), E.SimConfig(batch_size=size),
+                                      master_seed=0, env_offset=off)
+            E.reset_envs(self.state, torch.ones(size, dtype=torch.bool, device="cuda"),
+                         E.spec_sampler(spec))
+
+        def step(self, cmd):
+            E.step_batch(self.state, cmd)
+
+    g = torch.Generator(device="cuda").manual_seed(4)
+    cmds = [torch.rand((n, 6), device="cuda", generator=g) * 2 - 1 for _ in range(5)]
+    _rows_of_big_equal_small(Shard, n, (0, 500_000, n - m), m, 5, lambda t, _: cmds[t],
+                             ("p", "q", "nu", "act", "steps", "diverged"))
