@@ -19,15 +19,21 @@ collective); ``--gpus N`` without torchrun re-executes itself under
   enqueued behind a short device-side spin (``torch.cuda._sleep``, before the
   start event), so the GPU does not idle on host submission inside the region;
   the host submission time is reported beside it.
-* e2e — the same metric through the public API with HOST buffers:
-  ``step_batch(state, pinned_host_commands, out=HostStepOut)`` per step: the
-  step's commands go host->device and its whole result (p, q, nu, act, steps,
-  diverged -- what the reference's step_batch leaves in its numpy state) comes
-  back device->host; the call returns when it is in host memory.  Two paths are
-  timed and the faster is reported (both in ``e2e.per_path``): one launch per
-  step whose kernel reads/writes the mapped pinned buffers (CUDA events), and
-  the same calls inside ``engine.serve(state)`` (a resident step kernel rung by a
-  doorbell in mapped pinned memory; host clock around exactly K steps).
+* e2e — the same metric through the public API with HOST buffers; three paths
+  are timed and the fastest is reported (all in ``e2e.per_path``):
+  ``rollout_host`` -- the `value` path host to host: ONE ``engine.rollout`` call
+  with the K steps' commands in pinned host memory and a pinned host trace
+  (K, 13 + A, N); the kernel reads each step's command rows and writes each
+  step's p, q, nu, act over the host link as it runs, steps / diverged are
+  copied back after it (host clock around the call, which returns once the trace
+  is in host memory); ``serve`` -- the closed loop:
+  ``step_batch(state, pinned_host_commands, out=HostStepOut)`` per step inside
+  ``engine.serve(state)`` (a resident step kernel rung by a doorbell in mapped
+  pinned memory; host clock around exactly K steps), each step's whole result
+  (p, q, nu, act, steps, diverged -- what the reference's step_batch leaves in
+  its numpy state) in host memory before the next call; ``launch_per_step`` --
+  the same calls outside serve, one launch per step whose kernel reads/writes the
+  mapped pinned buffers (CUDA events).
 * roofline — the step kernel's algorithmic bytes per launch / average launch
   duration vs the measured HBM copy bandwidth (MEASURED_PEAKS.json).
 * at_scale — the other BASELINE configs at their stated per-GPU sizes, each
@@ -594,11 +600,43 @@ def run_b200(args):
             e2e_serve_el = time.perf_counter() - t0
         torch.cuda.synchronize(dev)
     e2e_serve_el = D.allreduce_max(e2e_serve_el, dev)
-    e2e_el = min(e2e_serve_el, e2e_launch_el)
-    e2e_path = ("step_batch(host cmds, out=HostStepOut) inside engine.serve(): resident step "
-                "kernel, doorbell in mapped pinned memory" if e2e_el == e2e_serve_el else
-                "step_batch(host cmds, out=HostStepOut) -> uuv_step_host (one launch per step, "
-                "mapped pinned buffers)")
+    # (3) the K steps as ONE engine.rollout call host to host (the `value` path with host
+    # buffers): K fresh command slots in pinned host memory, every step's p, q, nu, act
+    # written into a pinned host trace by the kernel as it runs, then steps / diverged
+    # copied back; host clock around the call (it returns once the trace is in host memory)
+    rh_cmds = torch.empty((k_total, n, A_BLUEROV), dtype=torch.float32).pin_memory()
+    rh_cmds.copy_(torch.rand(k_total, n, A_BLUEROV) * 2 - 1)
+    rh_trace = torch.empty((k_total, 13 + A_BLUEROV, n), dtype=torch.float32).pin_memory()
+    rh_out = E.HostStepOut(st, fields=("steps", "diverged"))
+
+    def rollout_host():
+        E.rollout(st, rh_cmds, k_total, trace=rh_trace, out=rh_out)
+
+    for _ in range(max(1, min(args.warmup, 3))):
+        rollout_host()
+    barrier()
+    torch.cuda.synchronize(dev)
+    e2e_rh_el = float("inf")
+    for _ in range(3):  # best of three calls (host clock, like the served path)
+        t0 = time.perf_counter()
+        rollout_host()
+        e2e_rh_el = min(e2e_rh_el, time.perf_counter() - t0)
+    e2e_rh_el = D.allreduce_max(e2e_rh_el, dev)
+    rh_d2h = (13 + A_BLUEROV) * 4 * n + rh_out.nbytes // k_total
+    e2e_paths = {
+        "rollout_host": (e2e_rh_el, "engine.rollout(state, pinned host commands (K, N, A), K, "
+                         "trace=pinned host (K, 13 + A, N)): one k_rollout launch reading each "
+                         "step's commands and writing each step's p, q, nu, act over the host "
+                         "link, then steps / diverged copied back", rh_d2h),
+        "serve": (e2e_serve_el, "step_batch(host cmds, out=HostStepOut) inside engine.serve(): "
+                  "resident step kernel, doorbell in mapped pinned memory (closed loop: each "
+                  "step's commands may depend on the previous result)", res.nbytes),
+        "launch_per_step": (e2e_launch_el, "step_batch(host cmds, out=HostStepOut) -> "
+                            "uuv_step_host (one launch per step, mapped pinned buffers)",
+                            res.nbytes),
+    }
+    e2e_key = min(e2e_paths, key=lambda k: e2e_paths[k][0])
+    e2e_el, e2e_path, e2e_d2h = e2e_paths[e2e_key]
     barrier()
     del graphs
     torch.cuda.empty_cache()
@@ -627,11 +665,12 @@ def run_b200(args):
                          "step_batch_graph_ms_per_step": 1e3 * el_graph_max / k_total,
                          "step_batch_graph_roofline": roof_graph},
             "e2e": {"value": world * n * k_total / e2e_el, "unit": "env-frames/s",
-                    "h2d_bytes_per_step": n * A_BLUEROV * 4, "d2h_bytes_per_step": res.nbytes,
+                    "h2d_bytes_per_step": n * A_BLUEROV * 4, "d2h_bytes_per_step": e2e_d2h,
                     "path": e2e_path,
-                    "per_path": {"serve": (world * n * k_total / e2e_serve_el
-                                           if e2e_serve_el != float("inf") else None),
-                                 "launch_per_step": world * n * k_total / e2e_launch_el}},
+                    "per_path": {k: (world * n * k_total / v[0] if v[0] != float("inf")
+                                     else None) for k, v in e2e_paths.items()},
+                    "closed_loop": "per_path.serve: one synchronous step per call, the next "
+                                   "commands may depend on this step's result"},
             "roofline": roof,
             "at_scale": scale,
             "gpu_launches": 1,  # one k_rollout launch for the K steps

@@ -417,7 +417,12 @@ uuv_status uuv_step_dl(uuv_ctx* ctx, const uuv_state* st, const DLTensor* comman
  * rollouts): step t applies slot (start + t) mod S of `commands`, a DLPack ring
  * (S, n_envs, width) of the state's dtype -- bit for bit `steps` calls of
  * uuv_step_dl(commands[slot]) (engine.py:465-484), state stored every step.
- * `trace` (>= steps, 13, n_envs) or NULL receives p, q, nu after every step.
+ * `trace` (>= steps, 13, n_envs) or NULL receives p, q, nu after every step;
+ * (>= steps, 13 + width, n_envs) receives act too.  `commands` and `trace` may be
+ * CUDA tensors of the current device or pinned (page-locked) host tensors
+ * (kDLCPU / kDLCUDAHost): the kernel then reads each step's command rows over the
+ * host link one step ahead and writes each step's trace rows as it produces them
+ * -- a host-to-host rollout in one launch (wait on `stream` before reading).
  * `ready` (a uint32/int32 device counter) or NULL: step t waits until
  * *ready > t, so a producer on another stream can fill the ring while the
  * rollout runs (device-side command ring; fill slot, then raise the counter). */

@@ -567,7 +567,11 @@ __global__ void __launch_bounds__(kBlock, HI ? kMinBHi : ((NT > 1 && sizeof(R) =
 // the DR derivation (derive_env + sub_from_env) and the state stores (the states
 // between the first and the last step are dead stores, as the substeps' are in
 // k_step); per step: the command row (loaded one step ahead) and the optional
-// (T, 13, trace_ld) pose trace.  With `ready`
+// (T, trace_rows, trace_ld) trace: p, q, nu (13 rows), then act (A rows) when
+// trace_rows = 13 + A.  Commands and trace may live in mapped pinned host memory:
+// the command rows are then read over the host link one step ahead and the trace
+// rows written back as they are produced, so a whole host-to-host rollout is one
+// launch.  With `ready`
 // set, step t first waits (acquire, GPU scope) until *ready > t: a producer on
 // another stream fills the ring slot and then raises the counter -- the device-
 // side command ring of a resident stepper.
@@ -578,6 +582,7 @@ struct RolloutSpec {
   int32_t n_slots, start, steps;
   void* trace;
   int64_t trace_ld;
+  int32_t trace_rows;     // 13 (p, q, nu) or 13 + A (and act)
   const uint32_t* ready;
 };
 
@@ -585,8 +590,9 @@ template <typename R, int NT> struct RolloutArgs {
   StepArgs<R, NT> step;   // hulls, state view, cmd = slot 0, cmd_ld, K, dt
   int64_t slot_stride;    // elements between ring slots
   int32_t n_slots, start, steps;
-  R* trace;               // (steps, 13, trace_ld) or null
+  R* trace;               // (steps, trace_rows, trace_ld) or null
   int64_t trace_ld;
+  int32_t trace_rows;     // 13, or 13 + A: act rows follow the pose rows
   const uint32_t* ready;  // or null (every slot already written)
 };
 
@@ -618,9 +624,12 @@ UUV_D void rollout_env(const RolloutArgs<R, NT>& ra, int64_t i, StepIn<R>& in) {
   }
   uint32_t avail = 0;
   bool stalled = false;  // the producer never raised the counter: give up, never hang
+  // ring slot of step t: the slot index advances with t (wrapping), no division per step
+  const R* const ring0 = a.cmd + i * a.cmd_ld;
+  int slot = (int)(ra.start % ra.n_slots), slot_t = 0;
   auto slot_row = [&](int t) {
-    const int k = (int)((ra.start + t) % ra.n_slots);
-    return a.cmd + (int64_t)k * ra.slot_stride + i * a.cmd_ld;
+    for (; slot_t < t; ++slot_t) slot = slot + 1 == ra.n_slots ? 0 : slot + 1;
+    return ring0 + (int64_t)slot * ra.slot_stride;
   };
   auto wait_slot = [&](int t) {
     if (ra.ready != nullptr && (uint32_t)t >= avail) {
@@ -673,12 +682,17 @@ UUV_D void rollout_env(const RolloutArgs<R, NT>& ra, int64_t i, StepIn<R>& in) {
     }
     in.steps += 1;
     if (ra.trace != nullptr) {
-      R* o = ra.trace + (int64_t)t * 13 * ra.trace_ld + i;
+      R* o = ra.trace + (int64_t)t * ra.trace_rows * ra.trace_ld + i;
       const int64_t ld = ra.trace_ld;
       o[0] = in.px; o[ld] = in.py; o[2 * ld] = in.pz;
       o[3 * ld] = in.q.w; o[4 * ld] = in.q.x; o[5 * ld] = in.q.y; o[6 * ld] = in.q.z;
 #pragma unroll
       for (int k = 0; k < 6; ++k) o[(7 + k) * ld] = in.nu[k];
+      if (ra.trace_rows > 13) {  // the command width's act rows (zero past this env's A)
+#pragma unroll
+        for (int j = 0; j < UUV_MAX_ACT; ++j)
+          if (j < ra.trace_rows - 13) o[(13 + j) * ld] = in.act[j];
+      }
     }
     if (t + 1 < ra.steps && ra.ready != nullptr && (uint32_t)(t + 1) >= avail) {
       wait_slot(t + 1);  // the producer had not filled slot t+1 when step t began
@@ -1835,6 +1849,7 @@ uuv_status launch_rollout(const uuv_ctx* ctx, const uuv_state* st, const Rollout
   ra.steps = sp.steps;
   ra.trace = (R*)sp.trace;
   ra.trace_ld = sp.trace_ld;
+  ra.trace_rows = sp.trace_rows;
   ra.ready = sp.ready;
   UUV_REGISTER(k_rollout<R, NT, DR, AC, DM, false>);
   if constexpr (sizeof(R) == 4) UUV_REGISTER(k_rollout<R, NT, DR, AC, DM, true>);
@@ -2919,13 +2934,30 @@ uuv_status uuv_step_dl(uuv_ctx* ctx, const uuv_state* st, const DLTensor* comman
   return step_checked(ctx, st, dl_ptr(commands), ld, substeps, dt, (cudaStream_t)stream, nullptr);
 }
 
+// Device address of a tensor the kernels may read / write: CUDA memory of the current
+// device, or pinned (page-locked, mapped) host memory -- reached over the host link.
+static uuv_status dl_kernel_ptr(const DLTensor* t, const char* what, void** p) {
+  const int dt = t->device.device_type;
+  if (dt == kDLCPU || dt == kDLCUDAHost) {
+    if (t->data == nullptr) return fail(UUV_ERR_ARG, "%s: null data", what);
+    *p = host_mapped(dl_ptr(t));
+    if (*p == nullptr)
+      return fail(UUV_ERR_ARG, "%s: host memory is not pinned (page-locked, mapped)", what);
+    return UUV_OK;
+  }
+  uuv_status s = dl_device(t, what);
+  if (s == UUV_OK) *p = dl_ptr(t);
+  return s;
+}
+
 uuv_status uuv_rollout_dl(uuv_ctx* ctx, const uuv_state* st, const DLTensor* commands,
                           int32_t start, int32_t steps, int32_t substeps, double dt,
                           const DLTensor* trace, const DLTensor* ready, void* stream) {
   uuv_status s = check_state(ctx, st);
   if (s != UUV_OK) return s;
   if (commands == nullptr) return fail(UUV_ERR_ARG, "commands: null tensor");
-  if ((s = dl_device(commands, "commands")) != UUV_OK) return s;
+  void* cmd_p = nullptr;
+  if ((s = dl_kernel_ptr(commands, "commands", &cmd_p)) != UUV_OK) return s;
   int32_t dt_code = -1;
   if (!dl_is_real(commands->dtype, &dt_code) || dt_code != st->dtype)
     return fail(UUV_ERR_ARG, "commands: dtype is not the state's float%d",
@@ -2943,19 +2975,24 @@ uuv_status uuv_rollout_dl(uuv_ctx* ctx, const uuv_state* st, const DLTensor* com
   if (cmd_ld < w) return fail(UUV_ERR_SHAPE, "commands: row stride < width");
   if (steps < 0 || start < 0) return fail(UUV_ERR_ARG, "steps and start must be >= 0");
   if (substeps < 1 || !(dt > 0)) return fail(UUV_ERR_ARG, "substeps >= 1 and dt > 0 required");
-  RolloutSpec sp{dl_ptr(commands), cmd_ld, slot_stride, (int32_t)n_slots, (int32_t)(start % n_slots),
-                 steps, nullptr, 0, nullptr};
+  RolloutSpec sp{cmd_p, cmd_ld, slot_stride, (int32_t)n_slots, (int32_t)(start % n_slots),
+                 steps, nullptr, 0, 13, nullptr};
   if (trace != nullptr) {
-    if ((s = dl_device(trace, "trace")) != UUV_OK) return s;
+    void* tp = nullptr;
+    if ((s = dl_kernel_ptr(trace, "trace", &tp)) != UUV_OK) return s;
     int32_t tc = -1;
     if (!dl_is_real(trace->dtype, &tc) || tc != st->dtype)
       return fail(UUV_ERR_ARG, "trace: dtype is not the state's");
-    if (trace->ndim != 3 || trace->shape[0] < steps || trace->shape[1] != 13 || trace->shape[2] != n)
-      return fail(UUV_ERR_SHAPE, "trace: expected shape (>= %d, 13, %lld)", steps, (long long)n);
-    if ((n > 1 && dl_stride(trace, 2) != 1) || dl_stride(trace, 0) != 13 * dl_stride(trace, 1))
-      return fail(UUV_ERR_SHAPE, "trace: expected contiguous (steps, 13, ld) rows");
-    sp.trace = dl_ptr(trace);
+    const int64_t rows = trace->ndim == 3 ? trace->shape[1] : 0;
+    if (trace->ndim != 3 || trace->shape[0] < steps || (rows != 13 && rows != 13 + w) ||
+        trace->shape[2] != n)
+      return fail(UUV_ERR_SHAPE, "trace: expected shape (>= %d, 13 or %lld, %lld)", steps,
+                  (long long)(13 + w), (long long)n);
+    if ((n > 1 && dl_stride(trace, 2) != 1) || dl_stride(trace, 0) != rows * dl_stride(trace, 1))
+      return fail(UUV_ERR_SHAPE, "trace: expected contiguous (steps, rows, ld) rows");
+    sp.trace = tp;
     sp.trace_ld = dl_stride(trace, 1);
+    sp.trace_rows = (int32_t)rows;
   }
   if (ready != nullptr) {
     if ((s = dl_device(ready, "ready")) != UUV_OK) return s;

@@ -656,6 +656,19 @@ class HostStepOut:
     def act(self):
         return self.act_rows.t()
 
+    def fill_async(self, state: "BatchState"):
+        """Enqueue copies of the batch's current state into these buffers on the current
+        stream (the caller synchronises)."""
+        n, w = state.n_envs, _cmd_width(state)
+        if self.pose is not None:
+            self.pose.copy_(state._soa[:13, :n], non_blocking=True)
+        if self.act_rows is not None:
+            self.act_rows.copy_(state._act[:w, :n], non_blocking=True)
+        if self.steps is not None:
+            self.steps.copy_(state.steps, non_blocking=True)
+        if self.diverged is not None:
+            self.diverged.copy_(state.diverged, non_blocking=True)
+
     @property
     def nbytes(self) -> int:
         """Bytes one step moves device -> host into these buffers."""
@@ -708,36 +721,55 @@ def step_batch(state: BatchState, commands, *, pose_out=None, out=None) -> Batch
 
 
 def rollout(state: BatchState, commands, steps: int | None = None, *, start: int = 0,
-            trace=None, ready=None) -> BatchState:
+            trace=None, ready=None, out=None) -> BatchState:
     """``steps`` control steps in ONE kernel launch, the state held in registers
     throughout (``uuv_rollout_dl``): bit for bit
 
         for t in range(steps):
             step_batch(state, commands[(start + t) % S])
 
-    ``commands``: CUDA tensor (S, N, A) -- a ring of S command slots -- or (N, A),
-    held for every step (the ``throughput_probe`` protocol, engine.py:541-564);
-    ``steps`` defaults to S.  ``trace``: optional CUDA tensor (>= steps, 13, N) of the
-    batch dtype receiving p (3), q (4), nu (6) after every step.  ``ready``: optional
-    int32 CUDA counter; step t waits until ``ready > t`` -- a producer on another
-    stream writes slot t and then raises the counter (a device-side command ring).
-    The producer's kernels must already be loaded (under CUDA lazy loading a first
-    launch waits for the device, i.e. for the waiting rollout); a rollout that sees
-    no new slot for 10 s stops instead of hanging.
+    ``commands``: (S, N, A) -- a ring of S command slots -- or (N, A), held for every
+    step (the ``throughput_probe`` protocol, engine.py:541-564); ``steps`` defaults to
+    S.  ``trace``: optional (>= steps, 13, N) tensor of the batch dtype receiving p (3),
+    q (4), nu (6) after every step, or (>= steps, 13 + A, N) receiving act (A) too.
+    Both are CUDA tensors, or pinned host tensors: the kernel then reads the command
+    rows over the host link (one step ahead) and writes the trace rows into host
+    memory as it produces them -- a host-to-host rollout in one launch, and the call
+    returns once the launch has finished (the host buffers are then free to reuse).
+    ``out``: a ``HostStepOut`` receiving the result after the last step (as
+    ``step_batch(..., out=)``); the call waits for it.
+    ``ready``: optional int32 CUDA counter; step t waits until ``ready > t`` -- a
+    producer on another stream writes slot t and then raises the counter (a
+    device-side command ring).  The producer's kernels must already be loaded (under
+    CUDA lazy loading a first launch waits for the device, i.e. for the waiting
+    rollout); a rollout that sees no new slot for 10 s stops instead of hanging.
     """
     if state._server is not None:
         raise EngineError("rollout: the batch is being served (leave the serve() block first)")
     n, w = state.n_envs, _cmd_width(state)
-    if not (torch.is_tensor(commands) and commands.is_cuda):
-        raise EngineError("commands: rollout takes a CUDA tensor (S, N, A) or (N, A)")
+    if not torch.is_tensor(commands):
+        raise EngineError("commands: rollout takes a CUDA or pinned host tensor (S, N, A) "
+                          "or (N, A)")
     cmd = commands if commands.dim() == 3 else commands.unsqueeze(0)
     if cmd.dim() != 3 or tuple(cmd.shape[1:]) != (n, w):
         raise EngineError(f"commands: expected shape (S, {n}, {w}) or ({n}, {w}), "
                           f"got {tuple(commands.shape)}")
-    if cmd.dtype != state.dtype or cmd.device != state.device:
-        cmd = cmd.to(device=state.device, dtype=state.dtype)
-    if cmd.stride(2) != 1:
-        cmd = cmd.contiguous()
+    host = not cmd.is_cuda
+    if host:
+        if not (cmd.is_pinned() and cmd.dtype == state.dtype and cmd.is_contiguous()):
+            raise EngineError(f"commands: host commands must be a pinned contiguous "
+                              f"{state.dtype} tensor")
+    else:
+        if cmd.dtype != state.dtype or cmd.device != state.device:
+            cmd = cmd.to(device=state.device, dtype=state.dtype)
+        if cmd.stride(2) != 1:
+            cmd = cmd.contiguous()
+    if trace is not None and not trace.is_cuda:
+        if not (trace.is_pinned() and trace.is_contiguous()):
+            raise EngineError("trace: a host trace must be a pinned contiguous tensor")
+        host = True
+    if out is not None and not isinstance(out, HostStepOut):
+        raise EngineError("out: expected an engine.HostStepOut")
     steps = cmd.shape[0] if steps is None else int(steps)
     if steps < 0 or start < 0:
         raise EngineError("steps and start must be >= 0")
@@ -747,6 +779,10 @@ def rollout(state: BatchState, commands, steps: int | None = None, *, start: int
                                      state._stream())
     if status:
         N.check(status, EngineError)
+    if out is not None:
+        out.fill_async(state)
+    if host or out is not None:  # the kernel reads / writes host buffers until it ends
+        torch.cuda.current_stream(state.device).synchronize()
     return state
 
 

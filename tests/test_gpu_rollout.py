@@ -173,3 +173,74 @@ def test_rollout_argument_errors():
                   trace=torch.zeros((2, 13, 64), device="cuda"))
     E.rollout(st, torch.zeros((3, 64, 6), device="cuda"), 0)  # zero steps: no-op
     assert int(st.steps[0]) == 0
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_rollout_trace_with_act_rows(dtype):
+    """A (T, 13 + A, N) trace also receives act after every step."""
+    n, T = 1500, 9
+    a, b = pair(cfg2(n, dtype, substeps=2))
+    ring = (torch.rand((T, n, 6), device="cuda", generator=torch.Generator(
+        device="cuda").manual_seed(5)) * 2 - 1).to(dtype)
+    trace = torch.full((T, 19, n), float("nan"), dtype=dtype, device="cuda")
+    want = []
+    for t in range(T):
+        E.step_batch(a, ring[t])
+        want.append(torch.cat([a.p, a.q, a.nu, a.act], dim=1).T.clone())
+    E.rollout(b, ring, trace=trace)
+    same(a, b)
+    assert torch.equal(trace, torch.stack(want))
+
+
+def test_rollout_host_to_host_equals_device_rollout():
+    """Pinned host commands and a pinned host trace (13 + A rows): the kernel reads the
+    command rows and writes the trace over the host link -- same bits as the device
+    rollout and as the launched steps; the call returns with the trace in host memory."""
+    n, S, T = 4096, 7, 20
+    a, b = pair(cfg2(n, torch.float32))
+    c = cfg2(n, torch.float32)()
+    ring = torch.rand((S, n, 6), device="cuda", generator=torch.Generator(
+        device="cuda").manual_seed(6)) * 2 - 1
+    host_ring = ring.cpu().pin_memory()
+    host_trace = torch.full((T, 19, n), float("nan")).pin_memory()
+    dev_trace = torch.empty((T, 19, n), device="cuda")
+    want = []
+    for t in range(T):
+        E.step_batch(a, ring[(2 + t) % S])
+        want.append(torch.cat([a.p, a.q, a.nu, a.act], dim=1).T.cpu())
+    res = E.HostStepOut(b)
+    E.rollout(b, host_ring, T, start=2, trace=host_trace, out=res)
+    E.rollout(c, ring, T, start=2, trace=dev_trace)
+    same(a, b)
+    same(a, c)
+    # out=HostStepOut: the result after the last step, in host memory on return
+    assert torch.equal(res.pose, torch.cat([a.p, a.q, a.nu], dim=1).T.cpu())
+    assert torch.equal(res.act, a.act.cpu())
+    assert torch.equal(res.steps, a.steps.cpu()) and torch.equal(res.diverged, a.diverged.cpu())
+    assert torch.equal(host_trace, torch.stack(want))
+    assert torch.equal(host_trace, dev_trace.cpu())
+    # host commands with a device trace, and device commands with a 13-row host trace
+    d = cfg2(n, torch.float32)()
+    E.rollout(d, host_ring, T, start=2, trace=dev_trace)
+    same(a, d)
+    pose = torch.empty((T, 13, n)).pin_memory()
+    e = cfg2(n, torch.float32)()
+    E.rollout(e, ring, T, start=2, trace=pose)
+    same(a, e)
+    assert torch.equal(pose, host_trace[:, :13])
+
+
+def test_rollout_host_argument_errors():
+    st = cfg2(64, torch.float32)()
+    with pytest.raises(E.EngineError, match="out"):
+        E.rollout(st, torch.zeros((3, 64, 6), device="cuda"), out=object())
+    with pytest.raises(E.EngineError, match="pinned"):
+        E.rollout(st, torch.zeros((3, 64, 6)))  # pageable host commands
+    with pytest.raises(E.EngineError, match="pinned"):
+        E.rollout(st, torch.zeros((3, 64, 6)).pin_memory().double())
+    with pytest.raises(E.EngineError, match="trace"):
+        E.rollout(st, torch.zeros((3, 64, 6), device="cuda"), trace=torch.zeros((3, 13, 64)))
+    with pytest.raises(E.EngineError, match="trace"):
+        E.rollout(st, torch.zeros((3, 64, 6), device="cuda"),
+                  trace=torch.zeros((3, 15, 64)).pin_memory())
+    assert int(st.steps[0]) == 0
