@@ -584,6 +584,7 @@ struct RolloutSpec {
   int64_t trace_ld;
   int32_t trace_rows;     // 13 (p, q, nu) or 13 + A (and act)
   const uint32_t* ready;
+  bool cmd_device;        // commands in device memory (not mapped host memory)
 };
 
 template <typename R, int NT> struct RolloutArgs {
@@ -593,6 +594,7 @@ template <typename R, int NT> struct RolloutArgs {
   R* trace;               // (steps, trace_rows, trace_ld) or null
   int64_t trace_ld;
   int32_t trace_rows;     // 13, or 13 + A: act rows follow the pose rows
+  int32_t prefetch;       // commands in device memory: L2-prefetch two steps ahead
   const uint32_t* ready;  // or null (every slot already written)
 };
 
@@ -604,7 +606,9 @@ UUV_D uint32_t ld_acquire_gpu_u32(const uint32_t* p) {
   return v;
 }
 
-template <typename R, int NT, bool DR, int AC, bool DM>
+// PLAIN: no trace, no ready counter, one substep per step -- the loop body of the
+// held-command / command-ring rollout without the branches it does not take
+template <typename R, int NT, bool DR, int AC, bool DM, bool PLAIN = false>
 UUV_D void rollout_env(const RolloutArgs<R, NT>& ra, int64_t i, StepIn<R>& in) {
   const StepArgs<R, NT>& a = ra.step;
   const StateView<R>& sv = a.sv;
@@ -622,6 +626,9 @@ UUV_D void rollout_env(const RolloutArgs<R, NT>& ra, int64_t i, StepIn<R>& in) {
     sub_from_env<R, DM, true, AC>(H.r, e, s);
     if (sv.slot[UUV_OV_JITTER] >= 0) jit = sv.ov + sv.slot[UUV_OV_JITTER] * sv.ld + i;
   }
+  const uint32_t* const ready = PLAIN ? nullptr : ra.ready;
+  R* const trace = PLAIN ? nullptr : ra.trace;
+  const int K = PLAIN ? 1 : a.K;
   uint32_t avail = 0;
   bool stalled = false;  // the producer never raised the counter: give up, never hang
   // ring slot of step t: the slot index advances with t (wrapping), no division per step
@@ -632,10 +639,10 @@ UUV_D void rollout_env(const RolloutArgs<R, NT>& ra, int64_t i, StepIn<R>& in) {
     return ring0 + (int64_t)slot * ra.slot_stride;
   };
   auto wait_slot = [&](int t) {
-    if (ra.ready != nullptr && (uint32_t)t >= avail) {
+    if (ready != nullptr && (uint32_t)t >= avail) {
       uint64_t t0;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-      while ((avail = ld_acquire_gpu_u32(ra.ready)) <= (uint32_t)t) {
+      while ((avail = ld_acquire_gpu_u32(ready)) <= (uint32_t)t) {
         __nanosleep(100);
         uint64_t t1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
@@ -646,28 +653,38 @@ UUV_D void rollout_env(const RolloutArgs<R, NT>& ra, int64_t i, StepIn<R>& in) {
       }
     }
   };
+  // the next step's command row is loaded during this step; the row after next is
+  // pulled into L2 (prefetch, no register) so that load hits L2: a row from HBM
+  // takes longer than one step's compute (cold ring: 0.66 vs 0.51 us per step)
+  const bool pf = ra.prefetch && ready == nullptr;
   R un[UUV_MAX_ACT];
-  wait_slot(0);
-  {
-    const R* c = slot_row(0);
+  auto load_row = [&](int t) {
+    const R* c = slot_row(t);
 #pragma unroll
     for (int j = 0; j < UUV_MAX_ACT; ++j) un[j] = (j < NA && j < A) ? c[j] : R(0);
-  }
+  };
+  constexpr int kAhead = 4;  // L2 prefetch distance in steps
+  auto prefetch_row = [&](int t) {
+    int k = slot + (t - slot_t);  // slot of step t (t - slot_t < kAhead steps ahead)
+    while (k >= ra.n_slots) k -= ra.n_slots;
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(ring0 + (int64_t)k * ra.slot_stride));
+  };
+  wait_slot(0);
+  load_row(0);
+  if (pf)
+    for (int t = 1; t < kAhead && t < ra.steps; ++t) prefetch_row(t);
   for (int t = 0; t < ra.steps && !stalled; ++t) {
     R u[UUV_MAX_ACT];
 #pragma unroll
     for (int j = 0; j < UUV_MAX_ACT; ++j) u[j] = clip_<R>(un[j], R(-1), R(1));
     if (t + 1 < ra.steps) {  // the next step's command row, in flight during this step
-      if (ra.ready == nullptr || (uint32_t)(t + 1) < avail) {
-        const R* c = slot_row(t + 1);
-#pragma unroll
-        for (int j = 0; j < UUV_MAX_ACT; ++j) un[j] = (j < NA && j < A) ? c[j] : R(0);
-      }
+      if (ready == nullptr || (uint32_t)(t + 1) < avail) load_row(t + 1);
+      if (pf && t + kAhead < ra.steps) prefetch_row(t + kAhead);
     }
     if (!in.div) {
       bool ok = true;
       auto run = [&](auto with_jit) {
-        for (int k = 0; k < a.K; ++k) {
+        for (int k = 0; k < K; ++k) {
           if (!substep<R, DR, false, AC, DM, decltype(with_jit)::value, true>(
                   H.r, s, jit, sv.ld, in.px, in.py, in.pz, in.q, in.nu, in.act, u, has_cur, cur,
                   a.dt, nullptr)) {
@@ -681,8 +698,8 @@ UUV_D void rollout_env(const RolloutArgs<R, NT>& ra, int64_t i, StepIn<R>& in) {
       if (!ok) in.div = 1;  // frozen from here on at its last finite state
     }
     in.steps += 1;
-    if (ra.trace != nullptr) {
-      R* o = ra.trace + (int64_t)t * ra.trace_rows * ra.trace_ld + i;
+    if (trace != nullptr) {
+      R* o = trace + (int64_t)t * ra.trace_rows * ra.trace_ld + i;
       const int64_t ld = ra.trace_ld;
       o[0] = in.px; o[ld] = in.py; o[2 * ld] = in.pz;
       o[3 * ld] = in.q.w; o[4 * ld] = in.q.x; o[5 * ld] = in.q.y; o[6 * ld] = in.q.z;
@@ -694,11 +711,9 @@ UUV_D void rollout_env(const RolloutArgs<R, NT>& ra, int64_t i, StepIn<R>& in) {
           if (j < ra.trace_rows - 13) o[(13 + j) * ld] = in.act[j];
       }
     }
-    if (t + 1 < ra.steps && ra.ready != nullptr && (uint32_t)(t + 1) >= avail) {
+    if (t + 1 < ra.steps && ready != nullptr && (uint32_t)(t + 1) >= avail) {
       wait_slot(t + 1);  // the producer had not filled slot t+1 when step t began
-      const R* c = slot_row(t + 1);
-#pragma unroll
-      for (int j = 0; j < UUV_MAX_ACT; ++j) un[j] = (j < NA && j < A) ? c[j] : R(0);
+      load_row(t + 1);
     }
   }
   // the state after the last step: intermediate states live only in registers (and the
@@ -713,7 +728,7 @@ UUV_D void rollout_env(const RolloutArgs<R, NT>& ra, int64_t i, StepIn<R>& in) {
 // more latency (bench at_scale: 1M envs 26.1 -> 21.9 us per step, 0.27 -> 0.32 of FP32;
 // 128 registers spills and loses at 4096 envs: 1.08 -> 1.61 us)
 constexpr int64_t kRolloutHiMinEnvs = 262144;
-template <typename R, int NT, bool DR, int AC, bool DM, bool HI = false>
+template <typename R, int NT, bool DR, int AC, bool DM, bool HI = false, bool PLAIN = false>
 __global__ void __launch_bounds__(kBlock, HI ? 3 : 1) k_rollout(const __grid_constant__ RolloutArgs<R, NT> ra) {
   const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
   if (i >= ra.step.sv.n) return;
@@ -739,7 +754,7 @@ __global__ void __launch_bounds__(kBlock, HI ? 3 : 1) k_rollout(const __grid_con
       default: rollout_env<R, NT, DR, 0, false>(ra, i, in); return;
     }
   } else {
-    rollout_env<R, NT, DR, AC, DM>(ra, i, in);
+    rollout_env<R, NT, DR, AC, DM, PLAIN>(ra, i, in);
   }
 }
 
@@ -1850,12 +1865,20 @@ uuv_status launch_rollout(const uuv_ctx* ctx, const uuv_state* st, const Rollout
   ra.trace = (R*)sp.trace;
   ra.trace_ld = sp.trace_ld;
   ra.trace_rows = sp.trace_rows;
+  ra.prefetch = sp.cmd_device && sp.steps > 2 ? 1 : 0;
   ra.ready = sp.ready;
   UUV_REGISTER(k_rollout<R, NT, DR, AC, DM, false>);
   if constexpr (sizeof(R) == 4) UUV_REGISTER(k_rollout<R, NT, DR, AC, DM, true>);
   auto kern = k_rollout<R, NT, DR, AC, DM, false>;
   if constexpr (sizeof(R) == 4) {  // (the float64 validation build keeps every register)
-    if (st->n_envs >= kRolloutHiMinEnvs) kern = k_rollout<R, NT, DR, AC, DM, true>;
+    const bool hi = st->n_envs >= kRolloutHiMinEnvs;
+    if (hi) kern = k_rollout<R, NT, DR, AC, DM, true>;
+    if constexpr (NT == 1) {
+      UUV_REGISTER(k_rollout<R, NT, DR, AC, DM, false, true>);
+      UUV_REGISTER(k_rollout<R, NT, DR, AC, DM, true, true>);
+      if (K == 1 && sp.trace == nullptr && sp.ready == nullptr)
+        kern = hi ? k_rollout<R, NT, DR, AC, DM, true, true> : k_rollout<R, NT, DR, AC, DM, false, true>;
+    }
   }
   kern<<<(unsigned)grid_for(st->n_envs), kBlock, 0, s>>>(ra);
   return check_launch("uuv_rollout");
@@ -2976,7 +2999,7 @@ uuv_status uuv_rollout_dl(uuv_ctx* ctx, const uuv_state* st, const DLTensor* com
   if (steps < 0 || start < 0) return fail(UUV_ERR_ARG, "steps and start must be >= 0");
   if (substeps < 1 || !(dt > 0)) return fail(UUV_ERR_ARG, "substeps >= 1 and dt > 0 required");
   RolloutSpec sp{cmd_p, cmd_ld, slot_stride, (int32_t)n_slots, (int32_t)(start % n_slots),
-                 steps, nullptr, 0, 13, nullptr};
+                 steps, nullptr, 0, 13, nullptr, commands->device.device_type == kDLCUDA};
   if (trace != nullptr) {
     void* tp = nullptr;
     if ((s = dl_kernel_ptr(trace, "trace", &tp)) != UUV_OK) return s;
