@@ -353,7 +353,9 @@ UUV_D void store_state(const StateView<R>& sv, int64_t i, int A, R px, R py, R p
 // K substeps for one env.  The overlay record is read at (ov, ov_ld, ov_i) — global
 // memory (a base pointer, leading dimension and row index); jitter always comes from
 // the global record.
-template <typename R, bool DR, int AC, bool DM, bool PRE = false>
+// LEAN (a lean batch, see lean_batch: K = 1, no current / reaction / jitter): the
+// branch-free substep<LEAN>, as every step-family kernel takes it for such batches.
+template <typename R, bool DR, int AC, bool DM, bool PRE = false, bool LEAN = false>
 UUV_D bool physics_at(const Hull<R>& H, const StateView<R>& sv, int64_t i, const double* ov,
                       int64_t ov_ld, int64_t ov_i, bool has_cur, V3<R> cur, int K, R dt,
                       const R* u, R& px, R& py, R& pz, Q4<R>& q, R* nu, R* act) {
@@ -363,8 +365,11 @@ UUV_D bool physics_at(const Hull<R>& H, const StateView<R>& sv, int64_t i, const
     EnvD e;
     derive_env(H.d, ov, ov_ld, ov_i, sv.slot, e);
     sub_from_env<R, DM, PRE, AC>(H.r, e, s);
-    if (sv.slot[UUV_OV_JITTER] >= 0) jit = sv.ov + sv.slot[UUV_OV_JITTER] * sv.ld + i;
+    if (!LEAN && sv.slot[UUV_OV_JITTER] >= 0) jit = sv.ov + sv.slot[UUV_OV_JITTER] * sv.ld + i;
   }
+  if constexpr (LEAN)
+    return !substep<R, DR, false, AC, DM, false, PRE, true>(H.r, s, nullptr, sv.ld, px, py, pz, q,
+                                                           nu, act, u, false, cur, dt, nullptr);
   bool ok = true;
   // the jitter record is present for every env of a launch or for none: one
   // specialisation per case keeps its code out of the common loop
@@ -382,14 +387,14 @@ UUV_D bool physics_at(const Hull<R>& H, const StateView<R>& sv, int64_t i, const
   return !ok;
 }
 
-template <typename R, bool DR, int AC, bool DM, bool PRE = false>
+template <typename R, bool DR, int AC, bool DM, bool PRE = false, bool LEAN = false>
 UUV_D bool physics(const Hull<R>& H, const StateView<R>& sv, int64_t i, int K, R dt, const R* u,
                    R& px, R& py, R& pz, Q4<R>& q, R* nu, R* act) {
-  const bool has_cur = sv.cur != nullptr;
+  const bool has_cur = !LEAN && sv.cur != nullptr;
   V3<R> cur{R(0), R(0), R(0)};
   if (has_cur) cur = V3<R>{sv.cur[i], sv.cur[sv.ld + i], sv.cur[2 * sv.ld + i]};
-  return physics_at<R, DR, AC, DM, PRE>(H, sv, i, sv.ov, sv.ld, i, has_cur, cur, K, dt, u, px, py, pz,
-                                   q, nu, act);
+  return physics_at<R, DR, AC, DM, PRE, LEAN>(H, sv, i, sv.ov, sv.ld, i, has_cur, cur, K, dt, u, px,
+                                              py, pz, q, nu, act);
 }
 
 // Inputs of one env's step, all loaded before any arithmetic (one memory round trip).
@@ -440,7 +445,7 @@ UUV_D void put_host_out(const HostOut& o, int64_t i, int64_t n, const StepIn<R>&
   if (o.div != nullptr) o.div[i] = div;
 }
 
-template <typename R, int NT, bool DR, int AC, bool DM, bool BRANCHLESS = false>
+template <typename R, int NT, bool DR, int AC, bool DM, bool BRANCHLESS = false, bool LEAN = false>
 UUV_D void step_env(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in) {
   const StateView<R>& sv = a.sv;
   if (!BRANCHLESS) {
@@ -451,8 +456,8 @@ UUV_D void step_env(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in) {
     }
     const Hull<R>& H = a.hull[in.ty];
     const int A = AC > 0 ? AC : H.r.n_act;
-    const bool div = physics<R, DR, AC, DM, true>(H, sv, i, a.K, a.dt, in.u, in.px, in.py, in.pz,
-                                                  in.q, in.nu, in.act);
+    const bool div = physics<R, DR, AC, DM, true, LEAN>(H, sv, i, a.K, a.dt, in.u, in.px, in.py,
+                                                        in.pz, in.q, in.nu, in.act);
     store_state(sv, i, A, in.px, in.py, in.pz, in.q, in.nu, in.act);
     sv.diverged[i] = div ? 1 : 0;
     sv.steps[i] = in.steps + 1;
@@ -467,8 +472,8 @@ UUV_D void step_env(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in) {
   // the branch (register pressure; +40% otherwise).
   const Hull<R>& H = a.hull[in.ty];
   const int A = AC > 0 ? AC : H.r.n_act;
-  const bool div = physics<R, DR, AC, DM, true>(H, sv, i, a.K, a.dt, in.u, in.px, in.py, in.pz, in.q,
-                                          in.nu, in.act);
+  const bool div = physics<R, DR, AC, DM, true, LEAN>(H, sv, i, a.K, a.dt, in.u, in.px, in.py, in.pz,
+                                                      in.q, in.nu, in.act);
   if (!in.div) {
     store_state(sv, i, A, in.px, in.py, in.pz, in.q, in.nu, in.act);
     sv.diverged[i] = div ? 1 : 0;
@@ -485,7 +490,7 @@ UUV_D void step_env(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in) {
 // inlined specialisations left them at 255 registers with ~2 KB of spills.
 UUV_D bool diag_class(int8_t c) { return c == 1 || c == 2 || c == 5 || c == 6; }
 
-template <typename R, int NT, bool DR, int AC, bool DM, bool BRANCHLESS = false>
+template <typename R, int NT, bool DR, int AC, bool DM, bool BRANCHLESS = false, bool LEAN = false>
 UUV_D void step_any(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in) {
   if constexpr (NT > 1 && sizeof(R) == 8) {
     if (diag_class(a.cls[in.ty])) step_env<R, NT, DR, 0, true>(a, i, in);
@@ -503,7 +508,7 @@ UUV_D void step_any(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in) {
     }
   } else {
     // the small-batch DR build issues every load before the diverged-flag branch
-    step_env<R, NT, DR, AC, DM, BRANCHLESS && DR>(a, i, in);
+    step_env<R, NT, DR, AC, DM, BRANCHLESS && DR, LEAN>(a, i, in);
   }
 }
 
@@ -521,7 +526,7 @@ UUV_D void prefetch_overlay_l2(const StateView<R>& sv, int64_t i) {
 // HI: the high-occupancy build of the float DR kernel (register cap 96 instead of
 // 128, a few spills to L1), launched for large batches where more resident warps
 // hide HBM latency; the default build serves the latency-bound small batches.
-template <typename R, int NT, bool DR, int AC, bool DM, bool HI = false>
+template <typename R, int NT, bool DR, int AC, bool DM, bool HI = false, bool LEAN = false>
 __global__ void __launch_bounds__(kBlock, HI ? kMinBHi : ((NT > 1 && sizeof(R) == 4) ? 3 : MinB<R>::value))
     k_step(const __grid_constant__ StepArgs<R, NT> a) {
   if (a.early_trigger == 1) pdl_trigger();
@@ -554,7 +559,7 @@ __global__ void __launch_bounds__(kBlock, HI ? kMinBHi : ((NT > 1 && sizeof(R) =
   // already past its own wait here, so at most two grids are in flight, and the
   // next step's command prefetch overlaps this step's compute
   if (a.early_trigger == 3) pdl_trigger();
-  step_any<R, NT, DR, AC, DM, !HI>(a, i, cur);
+  step_any<R, NT, DR, AC, DM, !HI, LEAN>(a, i, cur);
 }
 
 // ------------------------------------------------------------------ multi-step rollout
@@ -606,16 +611,20 @@ UUV_D uint32_t ld_acquire_gpu_u32(const uint32_t* p) {
   return v;
 }
 
-// PLAIN: no trace, no ready counter, one substep per step -- the loop body of the
-// held-command / command-ring rollout without the branches it does not take
-template <typename R, int NT, bool DR, int AC, bool DM, bool PLAIN = false>
+// LEAN: a lean batch (lean_batch: K = 1, no current, no reaction torques, no mount
+// jitter) -- the branch-free substep<LEAN> every step-family kernel takes for it.
+// PLAIN (implies LEAN): also no trace, no ready counter and commands in device memory
+// -- the whole control step is one basic block (frozen rows computed and not
+// committed; the next rows always loaded / prefetched: the ring slot is valid past
+// the last step).
+template <typename R, int NT, bool DR, int AC, bool DM, bool LEAN = false, bool PLAIN = false>
 UUV_D void rollout_env(const RolloutArgs<R, NT>& ra, int64_t i, StepIn<R>& in) {
   const StepArgs<R, NT>& a = ra.step;
   const StateView<R>& sv = a.sv;
   const Hull<R>& H = a.hull[in.ty];
   const int A = AC > 0 ? AC : H.r.n_act;
   constexpr int NA = AC > 0 ? AC : UUV_MAX_ACT;
-  const bool has_cur = sv.cur != nullptr;
+  const bool has_cur = !LEAN && sv.cur != nullptr;
   V3<R> cur{R(0), R(0), R(0)};
   if (has_cur) cur = V3<R>{sv.cur[i], sv.cur[sv.ld + i], sv.cur[2 * sv.ld + i]};
   Sub<R> s;
@@ -624,7 +633,7 @@ UUV_D void rollout_env(const RolloutArgs<R, NT>& ra, int64_t i, StepIn<R>& in) {
     EnvD e;
     derive_env(H.d, sv.ov, sv.ld, i, sv.slot, e);
     sub_from_env<R, DM, true, AC>(H.r, e, s);
-    if (sv.slot[UUV_OV_JITTER] >= 0) jit = sv.ov + sv.slot[UUV_OV_JITTER] * sv.ld + i;
+    if (!LEAN && sv.slot[UUV_OV_JITTER] >= 0) jit = sv.ov + sv.slot[UUV_OV_JITTER] * sv.ld + i;
   }
   const uint32_t* const ready = PLAIN ? nullptr : ra.ready;
   R* const trace = PLAIN ? nullptr : ra.trace;
@@ -634,8 +643,11 @@ UUV_D void rollout_env(const RolloutArgs<R, NT>& ra, int64_t i, StepIn<R>& in) {
   // ring slot of step t: the slot index advances with t (wrapping), no division per step
   const R* const ring0 = a.cmd + i * a.cmd_ld;
   int slot = (int)(ra.start % ra.n_slots), slot_t = 0;
-  auto slot_row = [&](int t) {
-    for (; slot_t < t; ++slot_t) slot = slot + 1 == ra.n_slots ? 0 : slot + 1;
+  auto slot_row = [&](int t) {  // t advances by at most one per call
+    if (slot_t < t) {
+      ++slot_t;
+      slot = slot + 1 == ra.n_slots ? 0 : slot + 1;
+    }
     return ring0 + (int64_t)slot * ra.slot_stride;
   };
   auto wait_slot = [&](int t) {
@@ -664,24 +676,37 @@ UUV_D void rollout_env(const RolloutArgs<R, NT>& ra, int64_t i, StepIn<R>& in) {
     for (int j = 0; j < UUV_MAX_ACT; ++j) un[j] = (j < NA && j < A) ? c[j] : R(0);
   };
   constexpr int kAhead = 4;  // L2 prefetch distance in steps
-  auto prefetch_row = [&](int t) {
-    int k = slot + (t - slot_t);  // slot of step t (t - slot_t < kAhead steps ahead)
-    while (k >= ra.n_slots) k -= ra.n_slots;
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(ring0 + (int64_t)k * ra.slot_stride));
+  int pslot = slot;           // ring slot of the last prefetched step
+  auto prefetch_next = [&]() {
+    pslot = pslot + 1 == ra.n_slots ? 0 : pslot + 1;
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(ring0 + (int64_t)pslot * ra.slot_stride));
   };
   wait_slot(0);
   load_row(0);
   if (pf)
-    for (int t = 1; t < kAhead && t < ra.steps; ++t) prefetch_row(t);
+    for (int t = 1; t < kAhead && t < ra.steps; ++t) prefetch_next();
   for (int t = 0; t < ra.steps && !stalled; ++t) {
     R u[UUV_MAX_ACT];
 #pragma unroll
     for (int j = 0; j < UUV_MAX_ACT; ++j) u[j] = clip_<R>(un[j], R(-1), R(1));
-    if (t + 1 < ra.steps) {  // the next step's command row, in flight during this step
+    if (PLAIN) {  // unconditionally (device ring, see the host checks): no branch
+      load_row(t + 1);
+      prefetch_next();
+    } else if (t + 1 < ra.steps) {  // the next step's command row, in flight during this step
       if (ready == nullptr || (uint32_t)(t + 1) < avail) load_row(t + 1);
-      if (pf && t + kAhead < ra.steps) prefetch_row(t + kAhead);
+      if (pf && t + kAhead < ra.steps) prefetch_next();  // step t + kAhead
     }
-    if (!in.div) {
+    if constexpr (PLAIN) {
+      const bool ok = substep<R, DR, false, AC, DM, false, true, true>(
+          H.r, s, nullptr, sv.ld, in.px, in.py, in.pz, in.q, in.nu, in.act, u, false, cur, a.dt,
+          nullptr, in.div != 0);
+      in.div = (in.div != 0 || !ok) ? 1 : 0;  // frozen from here on at its last finite state
+    } else if (LEAN && !in.div) {
+      if (!substep<R, DR, false, AC, DM, false, true, true>(H.r, s, nullptr, sv.ld, in.px, in.py,
+                                                           in.pz, in.q, in.nu, in.act, u, false,
+                                                           cur, a.dt, nullptr))
+        in.div = 1;
+    } else if (!in.div) {
       bool ok = true;
       auto run = [&](auto with_jit) {
         for (int k = 0; k < K; ++k) {
@@ -728,7 +753,8 @@ UUV_D void rollout_env(const RolloutArgs<R, NT>& ra, int64_t i, StepIn<R>& in) {
 // more latency (bench at_scale: 1M envs 26.1 -> 21.9 us per step, 0.27 -> 0.32 of FP32;
 // 128 registers spills and loses at 4096 envs: 1.08 -> 1.61 us)
 constexpr int64_t kRolloutHiMinEnvs = 262144;
-template <typename R, int NT, bool DR, int AC, bool DM, bool HI = false, bool PLAIN = false>
+template <typename R, int NT, bool DR, int AC, bool DM, bool HI = false, bool LEAN = false,
+          bool PLAIN = false>
 __global__ void __launch_bounds__(kBlock, HI ? 3 : 1) k_rollout(const __grid_constant__ RolloutArgs<R, NT> ra) {
   const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
   if (i >= ra.step.sv.n) return;
@@ -754,7 +780,7 @@ __global__ void __launch_bounds__(kBlock, HI ? 3 : 1) k_rollout(const __grid_con
       default: rollout_env<R, NT, DR, 0, false>(ra, i, in); return;
     }
   } else {
-    rollout_env<R, NT, DR, AC, DM, PLAIN>(ra, i, in);
+    rollout_env<R, NT, DR, AC, DM, LEAN, PLAIN>(ra, i, in);
   }
 }
 
@@ -832,15 +858,15 @@ UUV_D uint64_t global_ns() {
   return t;
 }
 
-template <typename R, int NT, bool DR, int AC, bool DM>
+template <typename R, int NT, bool DR, int AC, bool DM, bool LEAN = false>
 UUV_D void serve_env(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in, const HostOut& out) {
   const StateView<R>& sv = a.sv;
   in.steps += 1;
   if (!in.div) {
     const Hull<R>& H = a.hull[in.ty];
     const int A = AC > 0 ? AC : H.r.n_act;
-    const bool div = physics<R, DR, AC, DM, true>(H, sv, i, a.K, a.dt, in.u, in.px, in.py, in.pz,
-                                                  in.q, in.nu, in.act);
+    const bool div = physics<R, DR, AC, DM, true, LEAN>(H, sv, i, a.K, a.dt, in.u, in.px, in.py,
+                                                        in.pz, in.q, in.nu, in.act);
     store_state(sv, i, A, in.px, in.py, in.pz, in.q, in.nu, in.act);
     in.div = div ? 1 : 0;
     sv.diverged[i] = in.div;
@@ -849,7 +875,7 @@ UUV_D void serve_env(const StepArgs<R, NT>& a, int64_t i, StepIn<R>& in, const H
   put_host_out(out, i, sv.n, in, in.steps, in.div);
 }
 
-template <typename R, int NT, bool DR, int AC, bool DM>
+template <typename R, int NT, bool DR, int AC, bool DM, bool LEAN = false>
 __global__ void __launch_bounds__(kBlock, (NT > 1 && sizeof(R) == 4) ? 3 : MinB<R>::value)
     k_serve(const __grid_constant__ ServeArgs<R, NT> sa) {
   __shared__ uint64_t s_seq, s_cmd;
@@ -969,7 +995,7 @@ __global__ void __launch_bounds__(kBlock, (NT > 1 && sizeof(R) == 4) ? 3 : MinB<
           default: serve_env<R, NT, DR, 0, false>(a, i, in, s_out); break;
         }
       } else {
-        serve_env<R, NT, DR, AC, DM>(a, i, in, s_out);
+        serve_env<R, NT, DR, AC, DM, LEAN>(a, i, in, s_out);
       }
     }
     if (stamp) sa.ctl->stamp[3] = global_ns() + (uint64_t)(in.px > R(1e30));
@@ -1658,6 +1684,22 @@ void fill_hulls(const uuv_ctx* ctx, Hull<R>* dst, double dt_sub, int first = 0) 
   }
 }
 
+// A lean batch: float32, one hull, K = 1, no current, no reaction torques, no mount
+// jitter.  Every step-family kernel (k_step, k_rollout, k_serve) takes the branch-free
+// substep<LEAN> for it and the general one otherwise, so their results stay
+// bit-identical to each other (the compiler contracts multiply-adds per basic block:
+// one substep body with and one without branches round differently in the last bit).
+template <typename R>
+bool lean_batch(const uuv_ctx* ctx, const uuv_state* st, int32_t K) {
+  if (sizeof(R) != 4 || K != 1 || ctx->hulls.size() != 1 || st->type_id != nullptr) return false;
+  if (st->current_ned != nullptr) return false;
+  if (st->overlay != nullptr && st->slot[UUV_OV_JITTER] >= 0) return false;
+  const uuv_hull& h = ctx->hulls[0];
+  for (int j = 0; j < h.n_act; ++j)
+    if (h.reaction[j] != 0.0) return false;
+  return true;
+}
+
 template <typename R, int NT, bool DR, int AC, bool DM = false>
 uuv_status launch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd, int64_t cmd_ld,
                        int32_t K, double dt, cudaStream_t s, const HostOut* out = nullptr,
@@ -1684,6 +1726,12 @@ uuv_status launch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd,
   // build is faster (cfg2 K = 8: 1M envs 129.4 -> 127.3 us, 4M 503.8 -> 495.1 us)
   const bool hi = kHiOk && st->n_envs >= hi_min && K == 1;
   auto kern = hi ? k_step<R, NT, DR, AC, DM, kHiOk> : k_step<R, NT, DR, AC, DM, false>;
+  if constexpr (NT == 1 && sizeof(R) == 4) {
+    UUV_REGISTER(k_step<R, NT, DR, AC, DM, false, true>);
+    UUV_REGISTER(k_step<R, NT, DR, AC, DM, kHiOk, true>);
+    if (hull0 == 0 && lean_batch<R>(ctx, st, K))
+      kern = hi ? k_step<R, NT, DR, AC, DM, kHiOk, true> : k_step<R, NT, DR, AC, DM, false, true>;
+  }
   const int64_t wave = one_wave_ctas(kern);
   const int64_t grid = need;  // one thread per env
   // dependent-launch trigger: small grids (<= 64 CTAs) release the next step as
@@ -1876,8 +1924,15 @@ uuv_status launch_rollout(const uuv_ctx* ctx, const uuv_state* st, const Rollout
     if constexpr (NT == 1) {
       UUV_REGISTER(k_rollout<R, NT, DR, AC, DM, false, true>);
       UUV_REGISTER(k_rollout<R, NT, DR, AC, DM, true, true>);
-      if (K == 1 && sp.trace == nullptr && sp.ready == nullptr)
-        kern = hi ? k_rollout<R, NT, DR, AC, DM, true, true> : k_rollout<R, NT, DR, AC, DM, false, true>;
+      UUV_REGISTER(k_rollout<R, NT, DR, AC, DM, false, true, true>);
+      UUV_REGISTER(k_rollout<R, NT, DR, AC, DM, true, true, true>);
+      if (lean_batch<R>(ctx, st, K)) {
+        if (sp.trace == nullptr && sp.ready == nullptr && sp.cmd_device)
+          kern = hi ? k_rollout<R, NT, DR, AC, DM, true, true, true>
+                    : k_rollout<R, NT, DR, AC, DM, false, true, true>;
+        else
+          kern = hi ? k_rollout<R, NT, DR, AC, DM, true, true> : k_rollout<R, NT, DR, AC, DM, false, true>;
+      }
     }
   }
   kern<<<(unsigned)grid_for(st->n_envs), kBlock, 0, s>>>(ra);
@@ -2124,12 +2179,17 @@ uuv_status serve_kernel(const uuv_ctx* ctx, const uuv_state* st, int32_t K, doub
   sa.n_act = ctx->hulls.size() > 1 || st->type_id != nullptr ? st->a_max : ctx->hulls[0].n_act;
 
   const int64_t grid = grid_for(st->n_envs);
-  if (grid > one_wave_ctas(k_serve<R, NT, DR, AC, DM>))
+  auto kern = k_serve<R, NT, DR, AC, DM>;
+  UUV_REGISTER(k_serve<R, NT, DR, AC, DM>);
+  if constexpr (NT == 1 && sizeof(R) == 4) {
+    UUV_REGISTER(k_serve<R, NT, DR, AC, DM, true>);
+    if (lean_batch<R>(ctx, st, K)) kern = k_serve<R, NT, DR, AC, DM, true>;
+  }
+  if (grid > one_wave_ctas(kern))
     return fail(UUV_ERR_UNSUPPORTED, "step server: %lld CTAs do not fit one wave",
                 (long long)grid);
   *grid_out = grid;
-  UUV_REGISTER(k_serve<R, NT, DR, AC, DM>);
-  k_serve<R, NT, DR, AC, DM><<<(unsigned)grid, kBlock, 0, s>>>(sa);
+  kern<<<(unsigned)grid, kBlock, 0, s>>>(sa);
   return check_launch("uuv_server_start");
 }
 
