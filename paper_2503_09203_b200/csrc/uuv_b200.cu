@@ -665,43 +665,60 @@ UUV_D void rollout_env(const RolloutArgs<R, NT>& ra, int64_t i, StepIn<R>& in) {
       }
     }
   };
-  // the next step's command row is loaded during this step; the row after next is
-  // pulled into L2 (prefetch, no register) so that load hits L2: a row from HBM
-  // takes longer than one step's compute (cold ring: 0.66 vs 0.51 us per step)
+  // the next step's command row is loaded during this step (PLAIN: the one after
+  // next, see below); rows further ahead are pulled into L2 (prefetch, no register)
+  // so those loads hit L2: a row from HBM takes longer than one step's compute
+  // (cold ring: 0.66 vs 0.51 us per step)
   const bool pf = ra.prefetch && ready == nullptr;
   R un[UUV_MAX_ACT];
-  auto load_row = [&](int t) {
+  auto load_row = [&](int t, R* dst) {
     const R* c = slot_row(t);
 #pragma unroll
-    for (int j = 0; j < UUV_MAX_ACT; ++j) un[j] = (j < NA && j < A) ? c[j] : R(0);
+    for (int j = 0; j < UUV_MAX_ACT; ++j) dst[j] = (j < NA && j < A) ? c[j] : R(0);
   };
-  constexpr int kAhead = 4;  // L2 prefetch distance in steps
+  constexpr int kAhead = 8;  // L2 prefetch distance in steps
   int pslot = slot;           // ring slot of the last prefetched step
   auto prefetch_next = [&]() {
     pslot = pslot + 1 == ra.n_slots ? 0 : pslot + 1;
     asm volatile("prefetch.global.L2 [%0];" ::"l"(ring0 + (int64_t)pslot * ra.slot_stride));
   };
   wait_slot(0);
-  load_row(0);
+  load_row(0, un);
   if (pf)
     for (int t = 1; t < kAhead && t < ra.steps; ++t) prefetch_next();
-  for (int t = 0; t < ra.steps && !stalled; ++t) {
-    R u[UUV_MAX_ACT];
+  if constexpr (PLAIN) {
+    // two command rows in registers, used alternately by a two-step loop body (no
+    // register copies): each row has two steps' compute to arrive from L2
+    R ub[UUV_MAX_ACT];
+    load_row(1, ub);
+    auto one = [&](R* buf, int next) {
+      R u[UUV_MAX_ACT];
 #pragma unroll
-    for (int j = 0; j < UUV_MAX_ACT; ++j) u[j] = clip_<R>(un[j], R(-1), R(1));
-    if (PLAIN) {  // unconditionally (device ring, see the host checks): no branch
-      load_row(t + 1);
+      for (int j = 0; j < UUV_MAX_ACT; ++j) u[j] = clip_<R>(buf[j], R(-1), R(1));
+      load_row(next, buf);  // unconditionally (the ring slot is valid): no branch
       prefetch_next();
-    } else if (t + 1 < ra.steps) {  // the next step's command row, in flight during this step
-      if (ready == nullptr || (uint32_t)(t + 1) < avail) load_row(t + 1);
-      if (pf && t + kAhead < ra.steps) prefetch_next();  // step t + kAhead
-    }
-    if constexpr (PLAIN) {
       const bool ok = substep<R, DR, false, AC, DM, false, true, true>(
           H.r, s, nullptr, sv.ld, in.px, in.py, in.pz, in.q, in.nu, in.act, u, false, cur, a.dt,
           nullptr, in.div != 0);
       in.div = (in.div != 0 || !ok) ? 1 : 0;  // frozen from here on at its last finite state
-    } else if (LEAN && !in.div) {
+      in.steps += 1;
+    };
+    int t = 0;
+    for (; t + 1 < ra.steps; t += 2) {
+      one(un, t + 2);
+      one(ub, t + 3);
+    }
+    if (t < ra.steps) one(un, t + 2);
+  }
+  for (int t = 0; !PLAIN && t < ra.steps && !stalled; ++t) {
+    R u[UUV_MAX_ACT];
+#pragma unroll
+    for (int j = 0; j < UUV_MAX_ACT; ++j) u[j] = clip_<R>(un[j], R(-1), R(1));
+    if (t + 1 < ra.steps) {  // the next step's command row, in flight during this step
+      if (ready == nullptr || (uint32_t)(t + 1) < avail) load_row(t + 1, un);
+      if (pf && t + kAhead < ra.steps) prefetch_next();  // step t + kAhead
+    }
+    if (LEAN && !in.div) {
       if (!substep<R, DR, false, AC, DM, false, true, true>(H.r, s, nullptr, sv.ld, in.px, in.py,
                                                            in.pz, in.q, in.nu, in.act, u, false,
                                                            cur, a.dt, nullptr))
@@ -738,7 +755,7 @@ UUV_D void rollout_env(const RolloutArgs<R, NT>& ra, int64_t i, StepIn<R>& in) {
     }
     if (t + 1 < ra.steps && ready != nullptr && (uint32_t)(t + 1) >= avail) {
       wait_slot(t + 1);  // the producer had not filled slot t+1 when step t began
-      load_row(t + 1);
+      load_row(t + 1, un);
     }
   }
   // the state after the last step: intermediate states live only in registers (and the
