@@ -627,14 +627,6 @@ UUV_D void rollout_env(const RolloutArgs<R, NT>& ra, int64_t i, StepIn<R>& in) {
   const bool has_cur = !LEAN && sv.cur != nullptr;
   V3<R> cur{R(0), R(0), R(0)};
   if (has_cur) cur = V3<R>{sv.cur[i], sv.cur[sv.ld + i], sv.cur[2 * sv.ld + i]};
-  Sub<R> s;
-  const double* jit = nullptr;
-  if (DR) {
-    EnvD e;
-    derive_env(H.d, sv.ov, sv.ld, i, sv.slot, e);
-    sub_from_env<R, DM, true, AC>(H.r, e, s);
-    if (!LEAN && sv.slot[UUV_OV_JITTER] >= 0) jit = sv.ov + sv.slot[UUV_OV_JITTER] * sv.ld + i;
-  }
   const uint32_t* const ready = PLAIN ? nullptr : ra.ready;
   R* const trace = PLAIN ? nullptr : ra.trace;
   const int K = PLAIN ? 1 : a.K;
@@ -682,15 +674,25 @@ UUV_D void rollout_env(const RolloutArgs<R, NT>& ra, int64_t i, StepIn<R>& in) {
     pslot = pslot + 1 == ra.n_slots ? 0 : pslot + 1;
     asm volatile("prefetch.global.L2 [%0];" ::"l"(ring0 + (int64_t)pslot * ra.slot_stride));
   };
+  // the first command rows are requested before the per-env DR derivation, whose
+  // float64 chain would otherwise delay their DRAM round trip to after it
   wait_slot(0);
   load_row(0, un);
+  // PLAIN: two command rows in registers, used alternately by a two-step loop body
+  // (no register copies): each row has two steps' compute to arrive from L2
+  R ub[UUV_MAX_ACT];
+  if (PLAIN) load_row(1, ub);
   if (pf)
     for (int t = 1; t < kAhead && t < ra.steps; ++t) prefetch_next();
+  Sub<R> s;
+  const double* jit = nullptr;
+  if (DR) {
+    EnvD e;
+    derive_env(H.d, sv.ov, sv.ld, i, sv.slot, e);
+    sub_from_env<R, DM, true, AC>(H.r, e, s);
+    if (!LEAN && sv.slot[UUV_OV_JITTER] >= 0) jit = sv.ov + sv.slot[UUV_OV_JITTER] * sv.ld + i;
+  }
   if constexpr (PLAIN) {
-    // two command rows in registers, used alternately by a two-step loop body (no
-    // register copies): each row has two steps' compute to arrive from L2
-    R ub[UUV_MAX_ACT];
-    load_row(1, ub);
     auto one = [&](R* buf, int next) {
       R u[UUV_MAX_ACT];
 #pragma unroll
