@@ -756,7 +756,7 @@ def rollout(state: BatchState, commands, steps: int | None = None, *, start: int
                           f"got {tuple(commands.shape)}")
     host = not cmd.is_cuda
     if host:
-        if not (cmd.is_pinned() and cmd.dtype == state.dtype and cmd.is_contiguous()):
+        if not (cmd.dtype == state.dtype and cmd.is_contiguous() and _is_pinned(state, cmd)):
             raise EngineError(f"commands: host commands must be a pinned contiguous "
                               f"{state.dtype} tensor")
     else:
@@ -765,7 +765,7 @@ def rollout(state: BatchState, commands, steps: int | None = None, *, start: int
         if cmd.stride(2) != 1:
             cmd = cmd.contiguous()
     if trace is not None and not trace.is_cuda:
-        if not (trace.is_pinned() and trace.is_contiguous()):
+        if not (trace.is_contiguous() and _is_pinned(state, trace)):
             raise EngineError("trace: a host trace must be a pinned contiguous tensor")
         host = True
     if out is not None and not isinstance(out, HostStepOut):
@@ -856,7 +856,12 @@ class serve:
         return False
 
 
-def _pinned_ok(state: BatchState, t, shape) -> bool:
+def _is_pinned(state: BatchState, t) -> bool:
+    """``t.is_pinned()``, cached per tensor object like ``_pinned_ok``."""
+    return _pinned_ok(state, t, tuple(t.shape), dtype=t.dtype)
+
+
+def _pinned_ok(state: BatchState, t, shape, dtype=None) -> bool:
     """Pinned, contiguous, batch dtype and shape.  Cached per tensor object (a weak
     reference plus its data address), so a freed buffer whose address is reused
     is checked afresh."""
@@ -864,8 +869,8 @@ def _pinned_ok(state: BatchState, t, shape) -> bool:
     hit = state._pinned_cache.get(key)
     if hit is not None and hit[0]() is t and hit[1] == t.data_ptr():
         return hit[2]
-    ok = (tuple(t.shape) == shape and t.dtype == state.dtype and t.is_contiguous()
-          and t.is_pinned())
+    ok = (tuple(t.shape) == shape and t.dtype == (state.dtype if dtype is None else dtype)
+          and t.is_contiguous() and t.is_pinned())
     if len(state._pinned_cache) > 64:
         state._pinned_cache.clear()
     state._pinned_cache[key] = (weakref.ref(t), t.data_ptr(), ok)
