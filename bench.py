@@ -617,7 +617,7 @@ def run_b200(args):
     barrier()
     torch.cuda.synchronize(dev)
     e2e_rh_el = float("inf")
-    for _ in range(3):  # best of three calls (host clock, like the served path)
+    for _ in range(10):  # best of ten calls (host clock, like the served path)
         t0 = time.perf_counter()
         rollout_host()
         e2e_rh_el = min(e2e_rh_el, time.perf_counter() - t0)

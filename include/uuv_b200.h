@@ -83,7 +83,7 @@ typedef struct DLManagedTensor {
 } DLManagedTensor;
 #endif
 
-#define UUV_ABI_VERSION 6
+#define UUV_ABI_VERSION 7
 #define UUV_MAX_RUNS 8
 #define UUV_MAX_ACT 8        /* actuator columns per vehicle type             */
 #define UUV_MAX_TYPES 6      /* vehicle types in one batch (mixed fleets)     */
@@ -423,12 +423,16 @@ uuv_status uuv_step_dl(uuv_ctx* ctx, const uuv_state* st, const DLTensor* comman
  * (kDLCPU / kDLCUDAHost): the kernel then reads each step's command rows over the
  * host link one step ahead and writes each step's trace rows as it produces them
  * -- a host-to-host rollout in one launch (wait on `stream` before reading).
+ * `out` (or NULL): mapped pinned host rows receiving the result after the last
+ * step (as uuv_step_host's: p, q, nu, act, steps, diverged; any field NULL),
+ * written by the kernel itself.
  * `ready` (a uint32/int32 device counter) or NULL: step t waits until
  * *ready > t, so a producer on another stream can fill the ring while the
  * rollout runs (device-side command ring; fill slot, then raise the counter). */
 uuv_status uuv_rollout_dl(uuv_ctx* ctx, const uuv_state* st, const DLTensor* commands,
                           int32_t start, int32_t steps, int32_t substeps, double dt,
-                          const DLTensor* trace, const DLTensor* ready, void* stream);
+                          const DLTensor* trace, const DLTensor* ready,
+                          const uuv_host_out* out, void* stream);
 
 /* uuv_reset with the mask as a DLPack tensor (n_envs,) bool/uint8, unit stride,
  * or NULL for every row (reset_envs, engine.py:487-512). */

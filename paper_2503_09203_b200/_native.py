@@ -35,7 +35,7 @@ OV_WIDTH["payload_position"] = 3
 OV_WIDTH["mount_position_jitter"] = 3 * MAX_ACT
 OV_IDENTITY = {k: (1.0 if i <= OV_INDEX["thrust_coeff*"] else 0.0) for i, k in enumerate(OV_KEYS)}
 
-ABI_VERSION = 6
+ABI_VERSION = 7
 MAX_RUNS = 8  # UUV_MAX_RUNS
 DIST_UNIFORM, DIST_PIECEWISE, DIST_GAUSSIAN = 0, 1, 2
 START_IDENTITY, START_BOX = 0, 1
@@ -213,7 +213,8 @@ EXPORTS = {
     "uuv_step_dl": (C.c_int, [C.c_void_p, C.POINTER(State), C.c_void_p, C.c_int32, C.c_double,
                               C.c_void_p]),
     "uuv_rollout_dl": (C.c_int, [C.c_void_p, C.POINTER(State), C.c_void_p, C.c_int32, C.c_int32,
-                                 C.c_int32, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]),
+                                 C.c_int32, C.c_double, C.c_void_p, C.c_void_p,
+                                 C.POINTER(HostOut), C.c_void_p]),
     "uuv_reset_dl": (C.c_int, [C.c_void_p, C.POINTER(State), C.c_void_p, C.POINTER(Sampler),
                                C.c_uint64, C.c_void_p]),
     "uuv_task_step_dl": (C.c_int, [C.c_void_p, C.POINTER(State), C.POINTER(Task),

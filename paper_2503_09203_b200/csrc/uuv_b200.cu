@@ -590,6 +590,7 @@ struct RolloutSpec {
   int32_t trace_rows;     // 13 (p, q, nu) or 13 + A (and act)
   const uint32_t* ready;
   bool cmd_device;        // commands in device memory (not mapped host memory)
+  HostOut out;            // mapped host rows for the result after the last step
 };
 
 template <typename R, int NT> struct RolloutArgs {
@@ -765,6 +766,7 @@ UUV_D void rollout_env(const RolloutArgs<R, NT>& ra, int64_t i, StepIn<R>& in) {
   store_state(sv, i, A, in.px, in.py, in.pz, in.q, in.nu, in.act);
   sv.diverged[i] = in.div;
   sv.steps[i] = in.steps;
+  put_host_out(a.out, i, sv.n, in, in.steps, in.div);
 }
 
 // Two builds: the latency-bound small batches get every register they want (one CTA
@@ -1933,6 +1935,7 @@ uuv_status launch_rollout(const uuv_ctx* ctx, const uuv_state* st, const Rollout
   ra.trace_ld = sp.trace_ld;
   ra.trace_rows = sp.trace_rows;
   ra.prefetch = sp.cmd_device && sp.steps > 2 ? 1 : 0;
+  a.out = sp.out;
   ra.ready = sp.ready;
   UUV_REGISTER(k_rollout<R, NT, DR, AC, DM, false>);
   if constexpr (sizeof(R) == 4) UUV_REGISTER(k_rollout<R, NT, DR, AC, DM, true>);
@@ -3054,7 +3057,8 @@ static uuv_status dl_kernel_ptr(const DLTensor* t, const char* what, void** p) {
 
 uuv_status uuv_rollout_dl(uuv_ctx* ctx, const uuv_state* st, const DLTensor* commands,
                           int32_t start, int32_t steps, int32_t substeps, double dt,
-                          const DLTensor* trace, const DLTensor* ready, void* stream) {
+                          const DLTensor* trace, const DLTensor* ready,
+                          const uuv_host_out* out, void* stream) {
   uuv_status s = check_state(ctx, st);
   if (s != UUV_OK) return s;
   if (commands == nullptr) return fail(UUV_ERR_ARG, "commands: null tensor");
@@ -3078,7 +3082,9 @@ uuv_status uuv_rollout_dl(uuv_ctx* ctx, const uuv_state* st, const DLTensor* com
   if (steps < 0 || start < 0) return fail(UUV_ERR_ARG, "steps and start must be >= 0");
   if (substeps < 1 || !(dt > 0)) return fail(UUV_ERR_ARG, "substeps >= 1 and dt > 0 required");
   RolloutSpec sp{cmd_p, cmd_ld, slot_stride, (int32_t)n_slots, (int32_t)(start % n_slots),
-                 steps, nullptr, 0, 13, nullptr, commands->device.device_type == kDLCUDA};
+                 steps, nullptr, 0, 13, nullptr, commands->device.device_type == kDLCUDA, HostOut{}};
+  if (!map_host_out(out, out_act_rows(ctx, st), sp.out))
+    return fail(UUV_ERR_ARG, "out: result buffers are not pinned (page-locked) host memory");
   if (trace != nullptr) {
     void* tp = nullptr;
     if ((s = dl_kernel_ptr(trace, "trace", &tp)) != UUV_OK) return s;

@@ -656,19 +656,6 @@ class HostStepOut:
     def act(self):
         return self.act_rows.t()
 
-    def fill_async(self, state: "BatchState"):
-        """Enqueue copies of the batch's current state into these buffers on the current
-        stream (the caller synchronises)."""
-        n, w = state.n_envs, _cmd_width(state)
-        if self.pose is not None:
-            self.pose.copy_(state._soa[:13, :n], non_blocking=True)
-        if self.act_rows is not None:
-            self.act_rows.copy_(state._act[:w, :n], non_blocking=True)
-        if self.steps is not None:
-            self.steps.copy_(state.steps, non_blocking=True)
-        if self.diverged is not None:
-            self.diverged.copy_(state.diverged, non_blocking=True)
-
     @property
     def nbytes(self) -> int:
         """Bytes one step moves device -> host into these buffers."""
@@ -737,7 +724,8 @@ def rollout(state: BatchState, commands, steps: int | None = None, *, start: int
     memory as it produces them -- a host-to-host rollout in one launch, and the call
     returns once the launch has finished (the host buffers are then free to reuse).
     ``out``: a ``HostStepOut`` receiving the result after the last step (as
-    ``step_batch(..., out=)``); the call waits for it.
+    ``step_batch(..., out=)``), written into its pinned rows by the kernel; the call
+    waits for it.
     ``ready``: optional int32 CUDA counter; step t waits until ``ready > t`` -- a
     producer on another stream writes slot t and then raises the counter (a
     device-side command ring).  The producer's kernels must already be loaded (under
@@ -776,11 +764,9 @@ def rollout(state: BatchState, commands, steps: int | None = None, *, start: int
     args = [N.DLArg(cmd), N.dl(trace), N.dl(ready)]
     status = N.load().uuv_rollout_dl(state._ctx, C.byref(state._cstate()), args[0], int(start),
                                      steps, state.sim.substeps, state.sim.dt, args[1], args[2],
-                                     state._stream())
+                                     None if out is None else C.byref(out._c), state._stream())
     if status:
         N.check(status, EngineError)
-    if out is not None:
-        out.fill_async(state)
     if host or out is not None:  # the kernel reads / writes host buffers until it ends
         torch.cuda.current_stream(state.device).synchronize()
     return state

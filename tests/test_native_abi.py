@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_struct_sizes_and_version():
     lib = N.load()
-    assert lib.uuv_abi_version() == N.ABI_VERSION == 6
+    assert lib.uuv_abi_version() == N.ABI_VERSION == 7
     sizes = (C.c_int64 * 6)()
     lib.uuv_abi_sizes(sizes)
     assert list(sizes) == [C.sizeof(N.Hull), C.sizeof(N.State), C.sizeof(N.Sampler),
