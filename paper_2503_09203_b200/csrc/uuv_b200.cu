@@ -353,9 +353,12 @@ UUV_D void store_state(const StateView<R>& sv, int64_t i, int A, R px, R py, R p
 // K substeps for one env.  The overlay record is read at (ov, ov_ld, ov_i) — global
 // memory (a base pointer, leading dimension and row index); jitter always comes from
 // the global record.
-// LEAN (a lean batch, see lean_batch: K = 1, no current / reaction / jitter): the
+// LEAN 1 (a lean batch, see lean_batch: K = 1, no current / reaction / jitter): the
 // branch-free substep<LEAN>, as every step-family kernel takes it for such batches.
-template <typename R, bool DR, int AC, bool DM, bool PRE = false, bool LEAN = false>
+// LEAN 2 / 3 (a lean task batch, see lean_task: any K, no reaction / jitter, without /
+// with the current): the K substeps run to the end, an earlier failure holds the
+// state (the same result as stopping at it), as every task-family kernel takes it.
+template <typename R, bool DR, int AC, bool DM, bool PRE = false, int LEAN = 0>
 UUV_D bool physics_at(const Hull<R>& H, const StateView<R>& sv, int64_t i, const double* ov,
                       int64_t ov_ld, int64_t ov_i, bool has_cur, V3<R> cur, int K, R dt,
                       const R* u, R& px, R& py, R& pz, Q4<R>& q, R* nu, R* act) {
@@ -367,9 +370,17 @@ UUV_D bool physics_at(const Hull<R>& H, const StateView<R>& sv, int64_t i, const
     sub_from_env<R, DM, PRE, AC>(H.r, e, s);
     if (!LEAN && sv.slot[UUV_OV_JITTER] >= 0) jit = sv.ov + sv.slot[UUV_OV_JITTER] * sv.ld + i;
   }
-  if constexpr (LEAN)
-    return !substep<R, DR, false, AC, DM, false, PRE, true>(H.r, s, nullptr, sv.ld, px, py, pz, q,
-                                                           nu, act, u, false, cur, dt, nullptr);
+  if constexpr (LEAN == 1)
+    return !substep<R, DR, false, AC, DM, false, PRE, 1>(H.r, s, nullptr, sv.ld, px, py, pz, q, nu,
+                                                        act, u, false, cur, dt, nullptr);
+  if constexpr (LEAN >= 2) {
+    bool failed = false;
+    for (int k = 0; k < K; ++k)
+      failed |= !substep<R, DR, false, AC, DM, false, PRE, LEAN>(H.r, s, nullptr, sv.ld, px, py, pz,
+                                                                 q, nu, act, u, has_cur, cur, dt,
+                                                                 nullptr, failed);
+    return failed;
+  }
   bool ok = true;
   // the jitter record is present for every env of a launch or for none: one
   // specialisation per case keeps its code out of the common loop
@@ -387,10 +398,10 @@ UUV_D bool physics_at(const Hull<R>& H, const StateView<R>& sv, int64_t i, const
   return !ok;
 }
 
-template <typename R, bool DR, int AC, bool DM, bool PRE = false, bool LEAN = false>
+template <typename R, bool DR, int AC, bool DM, bool PRE = false, int LEAN = 0>
 UUV_D bool physics(const Hull<R>& H, const StateView<R>& sv, int64_t i, int K, R dt, const R* u,
                    R& px, R& py, R& pz, Q4<R>& q, R* nu, R* act) {
-  const bool has_cur = !LEAN && sv.cur != nullptr;
+  const bool has_cur = LEAN ? LEAN == 3 : sv.cur != nullptr;
   V3<R> cur{R(0), R(0), R(0)};
   if (has_cur) cur = V3<R>{sv.cur[i], sv.cur[sv.ld + i], sv.cur[2 * sv.ld + i]};
   return physics_at<R, DR, AC, DM, PRE, LEAN>(H, sv, i, sv.ov, sv.ld, i, has_cur, cur, K, dt, u, px,
@@ -1165,7 +1176,7 @@ UUV_D void task_in_global(const TaskArgs<R>& a, int64_t i, bool load_cmd, TaskIn
 // command, current and deviation sum come from `in`, and the step's result is
 // written back into `in` for the next step; otherwise they are loaded from global
 // memory where they are used (shorter live ranges for the one-step kernel).
-template <typename R, bool DR, int AC, bool DM, bool POL, bool CARRY = false>
+template <typename R, bool DR, int AC, bool DM, bool POL, bool CARRY = false, int LEAN = 0>
 UUV_D void task_env(const TaskArgs<R>& a, int64_t i, TaskIn<R>& in, const double* ov,
                     int64_t ov_ld, int64_t ov_i, R* srow, double* st, bool& live) {
   const StateView<R>& sv = a.sv;
@@ -1201,10 +1212,10 @@ UUV_D void task_env(const TaskArgs<R>& a, int64_t i, TaskIn<R>& in, const double
   int32_t steps = in.steps;
   if (!div) {
     if (CARRY)
-      div = physics_at<R, DR, AC, DM>(H, sv, i, ov, ov_ld, ov_i, in.has_cur, in.cur, a.K,
+      div = physics_at<R, DR, AC, DM, false, LEAN>(H, sv, i, ov, ov_ld, ov_i, in.has_cur, in.cur, a.K,
                                       a.dt_sub, u, px, py, pz, q, nu, act);
     else
-      div = physics<R, DR, AC, DM>(H, sv, i, a.K, a.dt_sub, u, px, py, pz, q, nu, act);
+      div = physics<R, DR, AC, DM, false, LEAN>(H, sv, i, a.K, a.dt_sub, u, px, py, pz, q, nu, act);
   }
   steps += 1;
   R dev = CARRY ? in.dev : (a.dev_sum != nullptr ? a.dev_sum[i] : R(0));
@@ -1318,7 +1329,7 @@ UUV_D void cta_stats(const double* st, double (*s_red)[UUV_ST_COUNT], double* sl
   }
 }
 
-template <typename R, bool DR, int AC, bool DM, bool POL = false>
+template <typename R, bool DR, int AC, bool DM, bool POL = false, int LEAN = 0>
 __global__ void __launch_bounds__(kBlock, MinBTask<R>::value) k_task_step(const __grid_constant__ TaskArgs<R> a) {
   __shared__ __align__(16) R s_obs[kBlock * kObsMax];
   __shared__ double s_red[kBlock / 32][UUV_ST_COUNT];
@@ -1346,7 +1357,8 @@ __global__ void __launch_bounds__(kBlock, MinBTask<R>::value) k_task_step(const 
   if (i < sv.n) {
     TaskIn<R> in;
     task_in_global<R>(a, i, !POL, in);
-    task_env<R, DR, AC, DM, POL>(a, i, in, sv.ov, sv.ld, i, s_obs + threadIdx.x * od, st, live);
+    task_env<R, DR, AC, DM, POL, false, LEAN>(a, i, in, sv.ov, sv.ld, i, s_obs + threadIdx.x * od,
+                                              st, live);
   }
   if constexpr (POL) {
     if (a.ep_live != nullptr) {
@@ -1377,7 +1389,7 @@ UUV_D uint32_t ld_acquire_gpu_i32(const int32_t* p) {
   return v;
 }
 
-template <typename R, bool DR, int AC, bool DM>
+template <typename R, bool DR, int AC, bool DM, int LEAN = 0>
 __global__ void __launch_bounds__(kBlock, MinBTask<R>::value)
     k_policy_episode(const __grid_constant__ TaskArgs<R> a, int32_t length) {
   __shared__ __align__(16) R s_obs[kBlock * kObsMax];
@@ -1405,8 +1417,8 @@ __global__ void __launch_bounds__(kBlock, MinBTask<R>::value)
   for (int t = 1; t <= length; ++t) {
     bool live = false;
     if (on)
-      task_env<R, DR, AC, DM, true, true>(a, i, in, sv.ov, sv.ld, i, s_obs + threadIdx.x * od, st,
-                                          live);
+      task_env<R, DR, AC, DM, true, true, LEAN>(a, i, in, sv.ov, sv.ld, i,
+                                                s_obs + threadIdx.x * od, st, live);
     const int cnt = __syncthreads_count(live);
     if (threadIdx.x == 0) {
       if (cnt != 0) atomicAdd(a.ep_live + t, cnt);
@@ -1719,6 +1731,20 @@ bool lean_batch(const uuv_ctx* ctx, const uuv_state* st, int32_t K) {
   for (int j = 0; j < h.n_act; ++j)
     if (h.reaction[j] != 0.0) return false;
   return true;
+}
+
+// A lean task batch (float32 task / policy launches): a six- or eight-thruster hull, no
+// reaction torques, no mount jitter -- every task-family kernel (task step, policy
+// step, fused episode) then takes the branch-free substep<LEAN>: 3 with the current
+// compiled in, 2 without.  0: the general substep.
+inline int lean_task(const uuv_ctx* ctx, const uuv_state* st) {
+  const uuv_hull& h = ctx->hulls[0];
+  const int ac = hull_act_class(h);
+  if (ctx->hulls.size() != 1 || (ac != 6 && ac != 8)) return 0;
+  if (st->overlay != nullptr && st->slot[UUV_OV_JITTER] >= 0) return 0;
+  for (int j = 0; j < h.n_act; ++j)
+    if (h.reaction[j] != 0.0) return 0;
+  return st->current_ned != nullptr ? 3 : 2;
 }
 
 template <typename R, int NT, bool DR, int AC, bool DM = false>
@@ -2055,22 +2081,33 @@ void fill_task_args(const uuv_ctx* ctx, const uuv_state* st, const uuv_task* tas
   a.prefetch = st->n_envs >= ((int64_t)1 << 19);
 }
 
-template <typename R, int AC, bool DM, bool POL>
+template <typename R, int AC, bool DM, bool POL, int LEAN = 0>
 void launch_task_dr(bool dr, unsigned g, cudaStream_t cs, const TaskArgs<R>& a) {
-  UUV_REGISTER(k_task_step<R, true, AC, DM, POL>);
-  UUV_REGISTER(k_task_step<R, false, AC, DM, POL>);
-  if (dr) k_task_step<R, true, AC, DM, POL><<<g, kBlock, 0, cs>>>(a);
-  else k_task_step<R, false, AC, DM, POL><<<g, kBlock, 0, cs>>>(a);
+  UUV_REGISTER(k_task_step<R, true, AC, DM, POL, LEAN>);
+  UUV_REGISTER(k_task_step<R, false, AC, DM, POL, LEAN>);
+  if (dr) k_task_step<R, true, AC, DM, POL, LEAN><<<g, kBlock, 0, cs>>>(a);
+  else k_task_step<R, false, AC, DM, POL, LEAN><<<g, kBlock, 0, cs>>>(a);
+}
+
+// lean (0, 2, 3; lean_task): the six- / eight-thruster classes only
+template <typename R, int AC, bool DM, bool POL>
+void launch_task_lean(int lean, bool dr, unsigned g, cudaStream_t cs, const TaskArgs<R>& a) {
+  if constexpr (sizeof(R) == 4) {
+    if (lean == 2) return launch_task_dr<R, AC, DM, POL, 2>(dr, g, cs, a);
+    if (lean == 3) return launch_task_dr<R, AC, DM, POL, 3>(dr, g, cs, a);
+  }
+  launch_task_dr<R, AC, DM, POL>(dr, g, cs, a);
 }
 
 template <typename R, bool POL = false>
-void launch_task_step(bool dr, int ac, bool dm, unsigned g, cudaStream_t cs, const TaskArgs<R>& a) {
+void launch_task_step(bool dr, int ac, bool dm, int lean, unsigned g, cudaStream_t cs,
+                      const TaskArgs<R>& a) {
   if (ac == 6) {
-    if (dm) launch_task_dr<R, 6, true, POL>(dr, g, cs, a);
-    else launch_task_dr<R, 6, false, POL>(dr, g, cs, a);
+    if (dm) launch_task_lean<R, 6, true, POL>(lean, dr, g, cs, a);
+    else launch_task_lean<R, 6, false, POL>(lean, dr, g, cs, a);
   } else if (ac == 8) {
-    if (dm) launch_task_dr<R, 8, true, POL>(dr, g, cs, a);
-    else launch_task_dr<R, 8, false, POL>(dr, g, cs, a);
+    if (dm) launch_task_lean<R, 8, true, POL>(lean, dr, g, cs, a);
+    else launch_task_lean<R, 8, false, POL>(lean, dr, g, cs, a);
   } else if (ac == kFinLayout) {
     if (dm) launch_task_dr<R, kFinLayout, true, POL>(dr, g, cs, a);
     else launch_task_dr<R, kFinLayout, false, POL>(dr, g, cs, a);
@@ -2083,24 +2120,34 @@ void launch_task_step(bool dr, int ac, bool dm, unsigned g, cudaStream_t cs, con
 // The fused episode loop (k_policy_episode): false when the grid cannot be co-resident
 // (its per-step grid-wide wait needs every CTA running), so the caller falls back to
 // one uuv_policy_step launch per step.
-template <typename R, bool DR, int AC, bool DM>
+template <typename R, bool DR, int AC, bool DM, int LEAN = 0>
 bool launch_episode_k(unsigned g, cudaStream_t cs, const TaskArgs<R>& a, int32_t length) {
-  auto kern = k_policy_episode<R, DR, AC, DM>;
-  UUV_REGISTER(k_policy_episode<R, DR, AC, DM>);
+  auto kern = k_policy_episode<R, DR, AC, DM, LEAN>;
+  UUV_REGISTER(k_policy_episode<R, DR, AC, DM, LEAN>);
   if ((int64_t)g > one_wave_ctas(kern)) return false;
   kern<<<g, kBlock, 0, cs>>>(a, length);
   return true;
 }
 
+template <typename R, bool DR, int AC, bool DM>
+bool launch_episode_lean(int lean, unsigned g, cudaStream_t cs, const TaskArgs<R>& a,
+                         int32_t length) {
+  if constexpr (sizeof(R) == 4) {
+    if (lean == 2) return launch_episode_k<R, DR, AC, DM, 2>(g, cs, a, length);
+    if (lean == 3) return launch_episode_k<R, DR, AC, DM, 3>(g, cs, a, length);
+  }
+  return launch_episode_k<R, DR, AC, DM>(g, cs, a, length);
+}
+
 template <typename R>
-bool launch_episode(bool dr, int ac, bool dm, unsigned g, cudaStream_t cs, const TaskArgs<R>& a,
-                    int32_t length) {
+bool launch_episode(bool dr, int ac, bool dm, int lean, unsigned g, cudaStream_t cs,
+                    const TaskArgs<R>& a, int32_t length) {
   auto pick = [&](auto dr_c) {
     constexpr bool D = decltype(dr_c)::value;
-    if (ac == 6) return dm ? launch_episode_k<R, D, 6, true>(g, cs, a, length)
-                           : launch_episode_k<R, D, 6, false>(g, cs, a, length);
-    if (ac == 8) return dm ? launch_episode_k<R, D, 8, true>(g, cs, a, length)
-                           : launch_episode_k<R, D, 8, false>(g, cs, a, length);
+    if (ac == 6) return dm ? launch_episode_lean<R, D, 6, true>(lean, g, cs, a, length)
+                           : launch_episode_lean<R, D, 6, false>(lean, g, cs, a, length);
+    if (ac == 8) return dm ? launch_episode_lean<R, D, 8, true>(lean, g, cs, a, length)
+                           : launch_episode_lean<R, D, 8, false>(lean, g, cs, a, length);
     if (ac == kFinLayout) return dm ? launch_episode_k<R, D, kFinLayout, true>(g, cs, a, length)
                                     : launch_episode_k<R, D, kFinLayout, false>(g, cs, a, length);
     return dm ? launch_episode_k<R, D, 0, true>(g, cs, a, length)
@@ -2133,9 +2180,9 @@ template <typename R>
 uuv_status step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd, int64_t cmd_ld,
                 int32_t K, double dt, cudaStream_t s, const HostOut* out);
 template <typename R, bool POL>
-void task(bool dr, int ac, bool dm, unsigned g, cudaStream_t cs, const TaskArgs<R>& a);
+void task(bool dr, int ac, bool dm, int lean, unsigned g, cudaStream_t cs, const TaskArgs<R>& a);
 template <typename R>
-bool episode(bool dr, int ac, bool dm, unsigned g, cudaStream_t cs, const TaskArgs<R>& a,
+bool episode(bool dr, int ac, bool dm, int lean, unsigned g, cudaStream_t cs, const TaskArgs<R>& a,
              int32_t length);
 template <typename R>
 uuv_status rollout(const uuv_ctx* ctx, const uuv_state* st, const RolloutSpec& sp, int32_t K,
@@ -2260,26 +2307,28 @@ template uuv_status serve<double>(const uuv_ctx*, const uuv_state*, int32_t, dou
 
 #if UUV_TU_TASK || UUV_TU_POLICY
 template <typename R, bool POL>
-void task(bool dr, int ac, bool dm, unsigned g, cudaStream_t cs, const TaskArgs<R>& a) {
-  launch_task_step<R, POL>(dr, ac, dm, g, cs, a);
+void task(bool dr, int ac, bool dm, int lean, unsigned g, cudaStream_t cs, const TaskArgs<R>& a) {
+  launch_task_step<R, POL>(dr, ac, dm, lean, g, cs, a);
 }
 #endif
 #if UUV_TU_TASK
-template void task<float, false>(bool, int, bool, unsigned, cudaStream_t, const TaskArgs<float>&);
-template void task<double, false>(bool, int, bool, unsigned, cudaStream_t, const TaskArgs<double>&);
+template void task<float, false>(bool, int, bool, int, unsigned, cudaStream_t, const TaskArgs<float>&);
+template void task<double, false>(bool, int, bool, int, unsigned, cudaStream_t,
+                                  const TaskArgs<double>&);
 #endif
 #if UUV_TU_POLICY
-template void task<float, true>(bool, int, bool, unsigned, cudaStream_t, const TaskArgs<float>&);
-template void task<double, true>(bool, int, bool, unsigned, cudaStream_t, const TaskArgs<double>&);
+template void task<float, true>(bool, int, bool, int, unsigned, cudaStream_t, const TaskArgs<float>&);
+template void task<double, true>(bool, int, bool, int, unsigned, cudaStream_t,
+                                 const TaskArgs<double>&);
 template <typename R>
-bool episode(bool dr, int ac, bool dm, unsigned g, cudaStream_t cs, const TaskArgs<R>& a,
+bool episode(bool dr, int ac, bool dm, int lean, unsigned g, cudaStream_t cs, const TaskArgs<R>& a,
              int32_t length) {
-  return launch_episode<R>(dr, ac, dm, g, cs, a, length);
+  return launch_episode<R>(dr, ac, dm, lean, g, cs, a, length);
 }
-template bool episode<float>(bool, int, bool, unsigned, cudaStream_t, const TaskArgs<float>&,
+template bool episode<float>(bool, int, bool, int, unsigned, cudaStream_t, const TaskArgs<float>&,
                              int32_t);
-template bool episode<double>(bool, int, bool, unsigned, cudaStream_t, const TaskArgs<double>&,
-                              int32_t);
+template bool episode<double>(bool, int, bool, int, unsigned, cudaStream_t,
+                              const TaskArgs<double>&, int32_t);
 #endif
 }  // namespace uuv_tu
 
@@ -2757,13 +2806,13 @@ uuv_status uuv_task_step(uuv_ctx* ctx, const uuv_state* st, const uuv_task* task
     fill_task_args<float>(ctx, st, task, sampler, seed, dt, substeps, io, a);
     a.cmd = (const float*)commands;
     a.cmd_ld = cmd_ld;
-    uuv_tu::task<float, false>(dr, act_class(ctx), diag_mass(ctx, st), g, cs, a);
+    uuv_tu::task<float, false>(dr, act_class(ctx), diag_mass(ctx, st), lean_task(ctx, st), g, cs, a);
   } else {
     TaskArgs<double> a;
     fill_task_args<double>(ctx, st, task, sampler, seed, dt, substeps, io, a);
     a.cmd = (const double*)commands;
     a.cmd_ld = cmd_ld;
-    uuv_tu::task<double, false>(dr, act_class(ctx), diag_mass(ctx, st), g, cs, a);
+    uuv_tu::task<double, false>(dr, act_class(ctx), diag_mass(ctx, st), 0, g, cs, a);
   }
   return check_launch("uuv_task_step");
 }
@@ -2812,17 +2861,18 @@ static uuv_status policy_impl(uuv_ctx* ctx, const uuv_state* st, const uuv_task*
     fill_task_args<float>(ctx, st, task, sampler, seed, dt, substeps, io, a);
     fill_pol(a, (const float*)pol->theta);
     if (length > 0)
-      launched = uuv_tu::episode<float>(dr, act_class(ctx), diag_mass(ctx, st), g, cs, a, length);
+      launched = uuv_tu::episode<float>(dr, act_class(ctx), diag_mass(ctx, st), lean_task(ctx, st), g,
+                                        cs, a, length);
     else
-      uuv_tu::task<float, true>(dr, act_class(ctx), diag_mass(ctx, st), g, cs, a);
+      uuv_tu::task<float, true>(dr, act_class(ctx), diag_mass(ctx, st), lean_task(ctx, st), g, cs, a);
   } else {
     TaskArgs<double> a;
     fill_task_args<double>(ctx, st, task, sampler, seed, dt, substeps, io, a);
     fill_pol(a, (const double*)pol->theta);
     if (length > 0)
-      launched = uuv_tu::episode<double>(dr, act_class(ctx), diag_mass(ctx, st), g, cs, a, length);
+      launched = uuv_tu::episode<double>(dr, act_class(ctx), diag_mass(ctx, st), 0, g, cs, a, length);
     else
-      uuv_tu::task<double, true>(dr, act_class(ctx), diag_mass(ctx, st), g, cs, a);
+      uuv_tu::task<double, true>(dr, act_class(ctx), diag_mass(ctx, st), 0, g, cs, a);
   }
   if (!launched)
     return fail(UUV_ERR_UNSUPPORTED, "policy episode: %u CTAs do not fit one wave (launch one "
