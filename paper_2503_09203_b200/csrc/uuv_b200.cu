@@ -1717,17 +1717,19 @@ void fill_hulls(const uuv_ctx* ctx, Hull<R>* dst, double dt_sub, int first = 0) 
   }
 }
 
-// A lean batch: float32, one hull, K = 1, no current, no reaction torques, no mount
-// jitter.  Every step-family kernel (k_step, k_rollout, k_serve) takes the branch-free
-// substep<LEAN> for it and the general one otherwise, so their results stay
-// bit-identical to each other (the compiler contracts multiply-adds per basic block:
-// one substep body with and one without branches round differently in the last bit).
+// A lean batch: float32, K = 1, no current, no reaction torques on the hull, no mount
+// jitter.  Every single-hull step-family kernel (k_step -- also each per-type run of a
+// large fleet --, k_rollout, k_serve) takes the branch-free substep<LEAN> for it and
+// the general one otherwise, so their results stay bit-identical to each other (the
+// compiler contracts multiply-adds per basic block: one substep body with and one
+// without branches round differently in the last bit).  Mixed-fleet kernels (one
+// launch over every type) keep the general substep.
 template <typename R>
-bool lean_batch(const uuv_ctx* ctx, const uuv_state* st, int32_t K) {
-  if (sizeof(R) != 4 || K != 1 || ctx->hulls.size() != 1 || st->type_id != nullptr) return false;
+bool lean_batch(const uuv_ctx* ctx, const uuv_state* st, int32_t K, int hull = 0) {
+  if (sizeof(R) != 4 || K != 1) return false;
   if (st->current_ned != nullptr) return false;
   if (st->overlay != nullptr && st->slot[UUV_OV_JITTER] >= 0) return false;
-  const uuv_hull& h = ctx->hulls[0];
+  const uuv_hull& h = ctx->hulls[hull];
   for (int j = 0; j < h.n_act; ++j)
     if (h.reaction[j] != 0.0) return false;
   return true;
@@ -1776,7 +1778,7 @@ uuv_status launch_step(const uuv_ctx* ctx, const uuv_state* st, const void* cmd,
   if constexpr (NT == 1 && sizeof(R) == 4) {
     UUV_REGISTER(k_step<R, NT, DR, AC, DM, false, true>);
     UUV_REGISTER(k_step<R, NT, DR, AC, DM, kHiOk, true>);
-    if (hull0 == 0 && lean_batch<R>(ctx, st, K))
+    if (lean_batch<R>(ctx, st, K, hull0))
       kern = hi ? k_step<R, NT, DR, AC, DM, kHiOk, true> : k_step<R, NT, DR, AC, DM, false, true>;
   }
   const int64_t wave = one_wave_ctas(kern);
