@@ -629,6 +629,7 @@ class HostStepOut:
         if bad:
             raise EngineError(f"HostStepOut: unknown fields {sorted(bad)}")
         n, w = state.n_envs, _cmd_width(state)
+        self.n_envs, self.width, self.dtype = n, w, state.dtype
 
         def pinned(shape, dt):
             return torch.zeros(shape, dtype=dt).pin_memory()
@@ -670,9 +671,10 @@ def _host_out(state: BatchState, pose_out, out):
             raise EngineError("pass either pose_out or out, not both")
         if not isinstance(out, HostStepOut):
             raise EngineError("out: expected an engine.HostStepOut")
-        if out.pose is not None and out.pose.shape[1] != state.n_envs:
-            raise EngineError(f"out: buffers for {out.pose.shape[1]} envs, batch has "
-                              f"{state.n_envs}")
+        if (out.n_envs, out.width, out.dtype) != (state.n_envs, _cmd_width(state), state.dtype):
+            raise EngineError(f"out: buffers for {out.n_envs} envs x {out.width} actuators "
+                              f"({out.dtype}), batch has {state.n_envs} x {_cmd_width(state)} "
+                              f"({state.dtype})")
         return out._c
     if pose_out is None:
         return None
@@ -756,15 +758,14 @@ def rollout(state: BatchState, commands, steps: int | None = None, *, start: int
         if not (trace.is_contiguous() and _is_pinned(state, trace)):
             raise EngineError("trace: a host trace must be a pinned contiguous tensor")
         host = True
-    if out is not None and not isinstance(out, HostStepOut):
-        raise EngineError("out: expected an engine.HostStepOut")
+    ho = _host_out(state, None, out)
     steps = cmd.shape[0] if steps is None else int(steps)
     if steps < 0 or start < 0:
         raise EngineError("steps and start must be >= 0")
     args = [N.DLArg(cmd), N.dl(trace), N.dl(ready)]
     status = N.load().uuv_rollout_dl(state._ctx, C.byref(state._cstate()), args[0], int(start),
                                      steps, state.sim.substeps, state.sim.dt, args[1], args[2],
-                                     None if out is None else C.byref(out._c), state._stream())
+                                     None if ho is None else C.byref(ho), state._stream())
     if status:
         N.check(status, EngineError)
     if host or out is not None:  # the kernel reads / writes host buffers until it ends

@@ -234,6 +234,10 @@ def test_rollout_host_argument_errors():
     st = cfg2(64, torch.float32)()
     with pytest.raises(E.EngineError, match="out"):
         E.rollout(st, torch.zeros((3, 64, 6), device="cuda"), out=object())
+    other = cfg2(65, torch.float32)()
+    with pytest.raises(E.EngineError, match="out: buffers for 65"):
+        E.rollout(st, torch.zeros((3, 64, 6), device="cuda"),
+                  out=E.HostStepOut(other, fields=("steps",)))
     with pytest.raises(E.EngineError, match="pinned"):
         E.rollout(st, torch.zeros((3, 64, 6)))  # pageable host commands
     with pytest.raises(E.EngineError, match="pinned"):
