@@ -1329,8 +1329,13 @@ UUV_D void cta_stats(const double* st, double (*s_red)[UUV_ST_COUNT], double* sl
   }
 }
 
-template <typename R, bool DR, int AC, bool DM, bool POL = false, int LEAN = 0>
-__global__ void __launch_bounds__(kBlock, MinBTask<R>::value) k_task_step(const __grid_constant__ TaskArgs<R> a) {
+// HI: a 96-register build (5 CTAs per SM) of the lean eight-thruster task step for
+// batches past L2, where more resident warps hide more HBM latency (config 5 at 1M
+// envs 171.6 -> 163.5 us); the six-thruster K = 8 kernel is issue-bound and loses
+// with it (202 -> 213 us), as does every class at small batches.
+template <typename R, bool DR, int AC, bool DM, bool POL = false, int LEAN = 0, bool HI = false>
+__global__ void __launch_bounds__(kBlock, HI ? 5 : MinBTask<R>::value)
+    k_task_step(const __grid_constant__ TaskArgs<R> a) {
   __shared__ __align__(16) R s_obs[kBlock * kObsMax];
   __shared__ double s_red[kBlock / 32][UUV_ST_COUNT];
   if (POL && a.ep_live != nullptr && a.ep_live[a.ep_t - 1] == 0) return;  // the episode loop broke
@@ -2091,10 +2096,26 @@ void launch_task_dr(bool dr, unsigned g, cudaStream_t cs, const TaskArgs<R>& a) 
   else k_task_step<R, false, AC, DM, POL, LEAN><<<g, kBlock, 0, cs>>>(a);
 }
 
-// lean (0, 2, 3; lean_task): the six- / eight-thruster classes only
+template <typename R, int AC, bool DM, bool POL, int LEAN>
+void launch_task_hi(bool dr, unsigned g, cudaStream_t cs, const TaskArgs<R>& a) {
+  UUV_REGISTER(k_task_step<R, true, AC, DM, POL, LEAN, true>);
+  UUV_REGISTER(k_task_step<R, false, AC, DM, POL, LEAN, true>);
+  if (dr) k_task_step<R, true, AC, DM, POL, LEAN, true><<<g, kBlock, 0, cs>>>(a);
+  else k_task_step<R, false, AC, DM, POL, LEAN, true><<<g, kBlock, 0, cs>>>(a);
+}
+
+// lean (0, 2, 3; lean_task): the six- / eight-thruster classes only; the 96-register
+// build for lean eight-thruster task steps from kTaskHiMinEnvs
+constexpr int64_t kTaskHiMinEnvs = 262144;
 template <typename R, int AC, bool DM, bool POL>
 void launch_task_lean(int lean, bool dr, unsigned g, cudaStream_t cs, const TaskArgs<R>& a) {
   if constexpr (sizeof(R) == 4) {
+    if constexpr (AC == 8 && !POL) {
+      if (a.sv.n >= kTaskHiMinEnvs) {
+        if (lean == 2) return launch_task_hi<R, AC, DM, POL, 2>(dr, g, cs, a);
+        if (lean == 3) return launch_task_hi<R, AC, DM, POL, 3>(dr, g, cs, a);
+      }
+    }
     if (lean == 2) return launch_task_dr<R, AC, DM, POL, 2>(dr, g, cs, a);
     if (lean == 3) return launch_task_dr<R, AC, DM, POL, 3>(dr, g, cs, a);
   }
