@@ -15,5 +15,7 @@ python scripts/probes/rollout_host.py > $R/rollout_host.json 2>> $R/sweep.err
 CASES="k_rollout_cfg2_4096:k_rollout:0:--case cfg2 --n 4096 --steps 5 --rollout 20
 k_step_cfg2_4096:k_step:2:--case cfg2 --n 4096 --steps 5
 k_step_cfg2_1m:k_step:2:--case cfg2 --n 1048576 --steps 5
-task_cfg5_1m:k_task_step:2:--case task_cfg5 --n 1048576 --steps 5" bash scripts/gpu_profile.sh > $R/profile.log 2>&1
+task_cfg5_1m:k_task_step:2:--case task_cfg5 --n 1048576 --steps 5
+task_cfg4_1m:k_task_step:2:--case task_cfg4 --n 1048576 --steps 5
+policy_episode_512:k_policy_episode:0:--case policy --n 512 --steps 100" bash scripts/gpu_profile.sh > $R/profile.log 2>&1
 ls -la $R gpurun_out/prof
