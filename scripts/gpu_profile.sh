@@ -27,6 +27,6 @@ echo "$CASES" | while IFS= read -r c; do
   ncu -i $P/$name.ncu-rep --page source --csv --print-source sass 2>/dev/null | gzip > $P/${name}_sass.csv.gz
   ncu -i $P/$name.ncu-rep --page raw --csv 2>/dev/null | gzip > $P/${name}_raw.csv.gz
   gzip -f $P/$name.ncu-rep
-  sz=$(stat -c %s $P/$name.ncu-rep.gz); [ "$sz" -gt 20000000 ] && rm -f $P/$name.ncu-rep.gz
+  rm -f $P/$name.ncu-rep.gz  # the summaries above are what travels back (gpurun_out <= 64 MiB)
 done
 du -sh $P; ls -la $P
