@@ -1310,16 +1310,23 @@ UUV_D void task_env(const TaskArgs<R>& a, int64_t i, TaskIn<R>& in, const double
   }
 }
 
-// Deterministic CTA reduction of the per-thread statistics (fixed shuffle tree, then
-// warps in order) added to this CTA's slot.
+// Deterministic CTA reduction of the per-thread statistics of one step (fixed shuffle
+// tree, then warps in order) added to this CTA's slot.  The six counters are 0/1 per
+// thread: a ballot and a popcount per warp (exact, as the float64 sums of 0/1 are)
+// instead of five shuffle rounds of a double each.
 UUV_D void cta_stats(const double* st, double (*s_red)[UUV_ST_COUNT], double* slot) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int k = 0; k < UUV_ST_COUNT; ++k) {
-    double v = st[k];
+    if (k == UUV_ST_REWARD || k == UUV_ST_METRIC_FINISHED) {
+      double v = st[k];
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
-    if (lane == 0) s_red[warp][k] = v;
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+      if (lane == 0) s_red[warp][k] = v;
+    } else {
+      const int c = __popc(__ballot_sync(0xffffffffu, st[k] != 0.0));
+      if (lane == 0) s_red[warp][k] = (double)c;
+    }
   }
   __syncthreads();
   if (threadIdx.x < UUV_ST_COUNT) {
