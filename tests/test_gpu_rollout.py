@@ -248,3 +248,32 @@ def test_rollout_host_argument_errors():
         E.rollout(st, torch.zeros((3, 64, 6), device="cuda"),
                   trace=torch.zeros((3, 15, 64)).pin_memory())
     assert int(st.steps[0]) == 0
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_rollout_host_buffers_fleet(dtype):
+    """Mixed fleet (the generic-fleet kernel), both dtypes: host commands and a host trace
+    (13 + a_max rows) give the same bits as device commands and a device trace."""
+    names = ("bluerov", "lauv", "hauv")
+    vehs = [product_vehicle(x) for x in names]
+    counts = [300, 250, 200]
+    n, T = sum(counts), 9
+
+    def make():
+        st = E.make_fleet_batch(vehs, counts, E.SimConfig(batch_size=n, substeps=2),
+                                master_seed=6, dtype=dtype)
+        E.reset_envs(st, np.ones(n, bool), E.spec_sampler(preset("train")))
+        return st
+
+    a, b = pair(make)
+    w = a.a_max
+    ring = (torch.rand((T, n, w), device="cuda", generator=torch.Generator(
+        device="cuda").manual_seed(8)) * 2 - 1).to(dtype)
+    dev_trace = torch.empty((T, 13 + w, n), dtype=dtype, device="cuda")
+    host_trace = torch.empty((T, 13 + w, n), dtype=dtype).pin_memory()
+    res = E.HostStepOut(b)
+    E.rollout(a, ring, trace=dev_trace)
+    E.rollout(b, ring.cpu().pin_memory(), trace=host_trace, out=res)
+    same(a, b)
+    assert torch.equal(host_trace, dev_trace.cpu())
+    assert torch.equal(res.act, a.act.cpu()) and torch.equal(res.steps, a.steps.cpu())
